@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 batched NTT engine (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Headline workload = BASELINE.json configs[1] (config 2): 4096 independent
+polynomials of N=2^12 over P=998244353, uint32 residues, Pease_nc forward
+(the paper's no-copy variant); DIT on the same batch is reported alongside.
+A STEP is one batched forward transform of the whole batch (one kernel
+launch).  Inputs are seeded uniform residues, resident in
+HBM before the timed region; input/output buffers rotate over a footprint
+> 2x L2 so every step streams from HBM ("rotating buffers > L2" in config).
+Under torchrun every rank transforms its own full batch (weak scaling, no
+collective -- independent polynomials); time = max over ranks of CUDA-event
+time.  `e2e` is the same metric through the C-ABI host-buffer call
+(ntt_exec_host: pinned H2D + transform + D2H every step).
+
+--impl reference times the reference algorithm on the host cores: the
+reference (nttkit) is pure Python and cannot run on the GPU box, so its
+CPU restatement oracle/libntt_oracle.so (pinned bit-exact to the reference,
+tests/test_oracle_pins.py) runs the same workload with every host thread.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _ncu_traffic(key: str):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the GPU is loaded."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sms.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sms if mx and s > 0.5 * mx] or sms
+        med = float(np.median(loaded)) if loaded else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def cpu_oracle_rate(w, variant: str, seconds: float, rows_cap: int | None = None):
+    """Rows/s of the CPU restatement on all host threads (bounded sample)."""
+    from oracle import oracle as O
+    cores = len(os.sched_getaffinity(0))
+    rows = min(w.batch, rows_cap or w.batch)
+    from paper_2405_11353_b200.configs import seeded_input
+    x = seeded_input(w, rows)
+    plan = O.OraclePlan(w.p, w.g, w.w, w.n, variant, False, w.n1, None)
+    plan.run(x[: max(1, min(rows, cores))], nthreads=cores)   # warm
+    done, t0 = 0, time.perf_counter()
+    while True:
+        plan.run(x, nthreads=cores)
+        done += rows
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return done / el, cores, f"{done} rows of {w.batch}x2^{w.log2n} ({rows}-row chunks, {el:.1f} s wall)"
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    from paper_2405_11353_b200.configs import CONFIGS
+    if rank != 0:
+        return
+    w = CONFIGS[2]
+    rates = []
+    for _ in range(args.warmup):
+        cpu_oracle_rate(w, args.variant, 0.2)
+    sample = ""
+    cores = 1
+    for _ in range(args.steps):
+        r, cores, sample = cpu_oracle_rate(w, args.variant, 1.0)
+        rates.append(r)
+    val = float(np.median(rates))
+    line = {
+        "impl": "reference", "metric": "batched NTTs/s (N=2^12, P=998244353, pease_nc forward)",
+        "value": val, "unit": "NTT/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * w.batch / val, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded uniform residues)",
+        "config": {"workload": "config2: 4096 x 2^12, P=998244353, pease_nc forward", "global_batch": w.batch},
+        "cpu_baseline": {"value": val, "unit": "NTT/s", "cores": cores, "kind": "port",
+                         "sample": sample + "; oracle/libntt_oracle.so (C restatement of nttkit, pinned bit-exact)"},
+        "e2e": {"value": val, "unit": "NTT/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--variant", default="pease_nc")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    import paper_2405_11353_b200 as P
+    from paper_2405_11353_b200 import _lib
+    from paper_2405_11353_b200.configs import CONFIGS, GOLDEN, seeded_input
+
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.Stream(dev)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    peak, peak_src = _peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def measure(w, variant, steps, warmup, inverse=False, sampler=None, check_hash=True):
+        """Device-resident timing of `steps` batched transforms (1 step = whole batch)."""
+        params = P.FieldParams(w.p, w.g, w.w)
+        plan = P.make_plan(params, variant, w.n, P.INVERSE if inverse else P.FORWARD, n1=w.n1)
+        dp = P.algorithms.device_plan_for(plan, w.word, local_rank)
+        x_host = seeded_input(w)
+        tdt = torch.uint32 if w.word == 4 else torch.uint64
+        nbytes = x_host.nbytes
+        nset = max(2, min(8, int(np.ceil(3 * l2 / (2 * nbytes))) + 1))
+        xs = [torch.from_numpy(x_host.view(np.int32 if w.word == 4 else np.int64)).view(tdt).to(dev)]
+        for _ in range(nset - 1):
+            xs.append(xs[0].clone())
+        ys = [torch.empty_like(xs[0]) for _ in range(nset)]
+        sp = stream.cuda_stream
+        # correctness self-check on the seeded input: full-output SHA-256 vs the
+        # hash the reference itself produced
+        parity = None
+        if check_hash and not inverse and w.cfg in GOLDEN:
+            dp.exec_device(xs[0].data_ptr(), ys[0].data_ptr(), w.batch, False, sp)
+            torch.cuda.synchronize(dev)
+            out = ys[0].cpu().view(torch.int32 if w.word == 4 else torch.int64).numpy()
+            parity = hashlib.sha256(out.astype("<u4" if w.word == 4 else "<u8").tobytes()).hexdigest() == GOLDEN[w.cfg][1]
+        with torch.cuda.stream(stream):
+            for i in range(warmup):
+                dp.exec_device(xs[i % nset].data_ptr(), ys[i % nset].data_ptr(), w.batch, inverse, sp)
+            if sampler is not None:     # sustained load while clocks are sampled
+                sampler.start()
+                t_end = time.perf_counter() + 1.0
+                i = 0
+                while time.perf_counter() < t_end:
+                    for _ in range(20):
+                        dp.exec_device(xs[i % nset].data_ptr(), ys[i % nset].data_ptr(), w.batch, inverse, sp)
+                        i += 1
+                    stream.synchronize()
+            _lib.counters_reset()
+            barrier()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            ev0.record(stream)
+            for i in range(steps):
+                evs[i][0].record(stream)
+                dp.exec_device(xs[i % nset].data_ptr(), ys[i % nset].data_ptr(), w.batch, inverse, sp)
+                evs[i][1].record(stream)
+            ev1.record(stream)
+            stream.synchronize()
+            barrier()
+        clocks = sampler.stop() if sampler is not None else None
+        launches = _lib.counters_read()["kernel_launches"]
+        total_ms = max_over_ranks(ev0.elapsed_time(ev1))
+        per_launch_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+        del xs, ys
+        torch.cuda.empty_cache()
+        return {"total_ms": total_ms, "per_step_ms": per_launch_ms, "launches": launches, "parity": parity,
+                "clocks": clocks, "nset": nset, "footprint_bytes": 2 * nset * nbytes, "dp": dp}
+
+    def e2e(w, variant, steps):
+        """Through the C-ABI host-buffer call: pinned H2D + transform + D2H per step."""
+        params = P.FieldParams(w.p, w.g, w.w)
+        plan = P.make_plan(params, variant, w.n, P.FORWARD, n1=w.n1)
+        dp = P.algorithms.device_plan_for(plan, w.word, local_rank)
+        x_host = seeded_input(w)
+        tdt = torch.int32 if w.word == 4 else torch.int64
+        hin = torch.from_numpy(x_host.view(np.int32 if w.word == 4 else np.int64)).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        sp = stream.cuda_stream
+        for _ in range(2):
+            dp.exec_host(hin.data_ptr(), hout.data_ptr(), w.batch, False, sp)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            dp.exec_host(hin.data_ptr(), hout.data_ptr(), w.batch, False, sp)
+        el = max_over_ranks(time.perf_counter() - t0)
+        del tdt
+        return world * w.batch * steps / el, x_host.nbytes
+
+    _lib.counters_enable(True)
+    w = CONFIGS[2]
+    sampler = ClockSampler(local_rank)
+    m = measure(w, args.variant, args.steps, args.warmup, sampler=sampler)
+    step_s = m["total_ms"] / 1e3 / args.steps
+    value = world * w.batch / step_s
+    alg_bytes = w.algorithmic_bytes()
+    achieved = alg_bytes / (m["per_step_ms"] / 1e3) / 1e9
+    e2e_val, io_bytes = e2e(w, args.variant, max(3, min(args.steps, 20)))
+    dit = measure(w, "dit", args.steps, args.warmup)
+
+    extra = {}
+    if not args.no_extra:
+        ext_steps, ext_warm = max(3, min(args.steps, 10)), 3
+        for cfg, var, inv in ((3, "dif", False), (3, "dif", True), (4, "pease_nc", False), (5, "sixstep", False)):
+            wc = CONFIGS[cfg]
+            try:
+                r = measure(wc, var, ext_steps, ext_warm, inverse=inv)
+                t = r["total_ms"] / 1e3 / ext_steps
+                ab = wc.algorithmic_bytes()
+                extra[f"config{cfg}_{var}_{'inv' if inv else 'fwd'}"] = {
+                    "ntt_per_s": world * wc.batch / t, "ms_per_step": 1e3 * t,
+                    "gbfly_per_s": world * wc.butterflies() / t / 1e9,
+                    "hbm_alg_gbs": ab / (r["per_step_ms"] / 1e3) / 1e9,
+                    "roofline_frac": ab / (r["per_step_ms"] / 1e3) / 1e9 / peak,
+                    "launches_per_step": r["launches"] / ext_steps, "sha256_parity": r["parity"],
+                    "workload": f"{wc.batch} x 2^{wc.log2n}, p={wc.p}"}
+            except Exception as exc:  # report, do not hide
+                extra[f"config{cfg}_{var}"] = {"error": repr(exc)[:300]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, cores, sample = cpu_oracle_rate(w, args.variant, 10.0)
+        cpu = {"value": rate, "unit": "NTT/s", "cores": cores, "kind": "port",
+               "sample": sample + "; oracle/libntt_oracle.so = C restatement of nttkit, pinned bit-exact"}
+
+    if rank == 0:
+        line = {
+            "metric": "batched NTTs/s (N=2^12, P=998244353, pease_nc forward)",
+            "value": value, "unit": "NTT/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": m["total_ms"] / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (np.random.default_rng(2) uniform residues)",
+            "config": {"workload": "config2: 4096 x 2^12 polys, P=998244353, pease_nc forward",
+                       "global_batch": world * w.batch, "n": w.n, "parallelism": f"batch-sharded x{world}",
+                       "l2_policy": f"rotating {m['nset']} in/out buffer sets, footprint "
+                                    f"{m['footprint_bytes'] >> 20} MiB > L2 {l2 >> 20} MiB"},
+            "gbutterfly_per_s": world * w.butterflies() / step_s / 1e9,
+            "sha256_parity": m["parity"],
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": _ncu_traffic("config2_pease_nc"),
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": alg_bytes},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "NTT/s", "h2d_bytes_per_step": io_bytes,
+                    "d2h_bytes_per_step": io_bytes},
+            "gpu_launches": m["launches"],
+            "clocks": m["clocks"],
+            "dit": {"ntt_per_s": world * w.batch / (dit["total_ms"] / 1e3 / args.steps),
+                    "roofline_frac": alg_bytes / (dit["per_step_ms"] / 1e3) / 1e9 / peak,
+                    "sha256_parity": dit["parity"]},
+            "configs": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,283 @@
+// launch.cuh -- host-side pass planner and per-field launchers (instantiated
+// once per field in k_<field>.cu so the four fields compile in parallel).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "multipass.cuh"
+
+namespace nttb200 {
+
+// Residues a tile may hold: two buffers of this many residues = 64 KiB.
+template <class T>
+constexpr int tile_elems_log2() { return sizeof(T) == 4 ? 13 : 12; }
+// Largest log2 N handled by ONE pass (a whole row resident in shared memory).
+inline int single_pass_max_log2(int word) { return word == 4 ? 14 : 13; }
+
+template <class F>
+inline typename F::Tw make_tw(uint64_t w, uint64_t ws);
+template <> inline uint2 make_tw<F32S>(uint64_t w, uint64_t ws) { return make_uint2((uint32_t)w, (uint32_t)ws); }
+template <> inline uint2 make_tw<F32W>(uint64_t w, uint64_t ws) { return make_uint2((uint32_t)w, (uint32_t)ws); }
+template <> inline uint64_t make_tw<FGold>(uint64_t w, uint64_t) { return w; }
+template <> inline ulonglong2 make_tw<F64>(uint64_t w, uint64_t ws) { return make_ulonglong2(w, ws); }
+
+// Pass decomposition of L stages (multi-pass variants): K_i per pass.
+inline int plan_passes(int L, int word, int variant, int* K) {
+    const int elog = word == 4 ? 13 : 12;
+    const int kcap = elog - 3;                 // keep >= 8 networks per tile
+    int P = (L + kcap - 1) / kcap;
+    if (P < 2) P = 2;
+    for (int i = 0; i < P; ++i) K[i] = L / P + (i < L % P ? 1 : 0);
+    (void)variant;
+    return P;
+}
+
+template <class F, int V, int LAY>
+cudaError_t run_pass(PassArgs<F>& a, cudaStream_t s, int num_sms, int* launches) {
+    using T = typename F::T;
+    const size_t smem = 2ull * ((size_t)a.TQ << a.K) * sizeof(T);
+    auto kern = k_pass<F, V, LAY>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    const int M = LAY == LAY_VARIANT ? a.L - a.K : (LAY == LAY_SIX_A ? a.l1 : a.l2);
+    const uint64_t ntiles = a.qmode == QM_ROWS ? (a.batch + a.TQ - 1) / a.TQ
+                                               : a.batch * ((1ull << M) / a.TQ);
+    uint64_t grid = (uint64_t)num_sms * occ;
+    if (grid > ntiles) grid = ntiles;
+    if (grid == 0) return cudaSuccess;
+    kern<<<(unsigned)grid, kThreads, smem, s>>>(a);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+template <class F>
+PassArgs<F> base_args(const MultipassReq& r) {
+    PassArgs<F> a{};
+    a.batch = r.batch;
+    a.L = r.L;
+    a.tw = static_cast<const typename F::Tw*>(r.tw);
+    a.f.p = (typename F::T)r.p;
+    a.ninv = make_tw<F>(r.ninv, r.ninv_shoup);
+    a.counters = r.counters;
+    a.TA = 1;
+    return a;
+}
+
+template <class T>
+__global__ void k_copy(const T* src, T* dst, uint64_t n, uint64_t rows, unsigned long long* counters) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+    if (counters && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(counters + C_COPIES, (unsigned long long)rows);
+}
+
+template <class F, int V>
+cudaError_t run_variant(const MultipassReq& r) {
+    using T = typename F::T;
+    const int L = r.L;
+    const uint64_t N = 1ull << L;
+    constexpr int elog = tile_elems_log2<T>();
+    if (L <= single_pass_max_log2(sizeof(T))) {
+        // ---- one pass: TQ whole rows per tile, bit reversal fused into the groups
+        PassArgs<F> a = base_args<F>(r);
+        a.in = static_cast<const T*>(r.in);
+        a.out = static_cast<T*>(r.out);
+        a.K = L;
+        a.S0 = 0;
+        int tq = L >= elog ? 1 : (1 << (elog - L));
+        a.TQ = tq > 256 ? 256 : tq;
+        a.qmode = QM_ROWS;
+        a.in_order = a.out_order = ORD_C_FAST;
+        a.rev_first = (V == V_DIT || V == V_FLAT || V == V_PEASE || V == V_PEASE_NC);
+        a.rev_last = (V == V_DIF);
+        a.count_row = 1;
+        a.count_bitrev = (V == V_STOCKHAM) ? 0 : 1;
+        a.scale = r.scale;
+        return run_pass<F, V, LAY_VARIANT>(a, r.stream, r.num_sms, r.launches);
+    }
+    // ---- multi-pass
+    int K[8];
+    const int P = plan_passes(L, sizeof(T), V, K);
+    T* ws0 = static_cast<T*>(r.ws);
+    T* ws1 = ws0 + r.batch * N;
+    const T* cur = static_cast<const T*>(r.in);
+    cudaError_t e = cudaSuccess;
+    if (V == V_FLAT) {                     // bit_reverse_permute as its own HBM pass
+        dim3 blk(32, 8);
+        uint64_t blocks = r.batch << (L - 10);
+        uint64_t cap = (uint64_t)r.num_sms * 8;
+        k_bitrev<T><<<(unsigned)(blocks < cap ? blocks : cap), blk, 0, r.stream>>>(cur, ws1, r.batch, L, r.counters);
+        if (r.launches) ++*r.launches;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        cur = ws1;
+    }
+    int done = 0;   // stages (or low bits) already applied
+    for (int i = 0; i < P; ++i) {
+        PassArgs<F> a = base_args<F>(r);
+        const bool last = (i == P - 1);
+        T* dst = last ? static_cast<T*>(r.out) : ((cur == ws0) ? ws1 : ws0);
+        if (V == V_PEASE && !last) dst = ws0;      // Pease: write dst, copy back into src (ws1)
+        a.in = cur;
+        a.out = dst;
+        a.K = K[i];
+        a.TQ = 1 << (elog - K[i]);
+        if (a.TQ > 256) a.TQ = 256;
+        a.count_row = last;
+        a.scale = last ? r.scale : 0;
+        const int Mq = L - K[i];
+        if (V == V_DIT || V == V_FLAT) {
+            a.S0 = done;
+            if (i == 0 && V == V_DIT) {
+                a.qmode = QM_REV; a.rev_in = 1; a.in_order = ORD_T_FAST; a.out_order = ORD_C_FAST;
+                a.count_bitrev = 1;
+            } else if (i == 0) {
+                a.qmode = QM_LINEAR; a.in_order = ORD_C_FAST; a.out_order = ORD_C_FAST;
+            } else {
+                a.qmode = QM_LINEAR; a.in_order = ORD_T_FAST; a.out_order = ORD_T_FAST;
+            }
+            e = run_pass<F, V_DIT, LAY_VARIANT>(a, r.stream, r.num_sms, r.launches);
+            done += K[i];
+        } else if (V == V_DIF) {
+            const int Kd = K[P - 1 - i];           // windows from the top bit down
+            a.K = Kd;
+            a.TQ = 1 << (elog - Kd);
+            if (a.TQ > 256) a.TQ = 256;
+            a.S0 = L - done - Kd;
+            if (last) {
+                a.qmode = QM_REV; a.rev_out = 1; a.in_order = ORD_C_FAST; a.out_order = ORD_T_FAST;
+                a.count_bitrev = 1;
+            } else {
+                a.qmode = QM_LINEAR; a.in_order = ORD_T_FAST; a.out_order = ORD_T_FAST;
+            }
+            e = run_pass<F, V_DIF, LAY_VARIANT>(a, r.stream, r.num_sms, r.launches);
+            done += Kd;
+        } else if (V == V_PEASE || V == V_PEASE_NC) {
+            a.S0 = done;
+            if (i == 0) {
+                int ta = 1;
+                while (ta * ta < a.TQ) ta <<= 1;    // TQ = TA x TB, TA >= TB
+                if (ta > (1 << Mq)) ta = 1 << Mq;
+                a.TA = ta;
+                a.qmode = QM_2D; a.rev_in = 1; a.in_order = ORD_T_FAST; a.out_order = ORD_TB_FAST;
+                a.count_bitrev = 1;
+            } else {
+                a.qmode = QM_LINEAR; a.in_order = ORD_C_FAST; a.out_order = ORD_T_FAST;
+            }
+            e = run_pass<F, V_PEASE_NC, LAY_VARIANT>(a, r.stream, r.num_sms, r.launches);
+            done += K[i];
+            if (e == cudaSuccess && V == V_PEASE) {   // _stage_copy per pass (algorithms.py:242)
+                uint64_t n = r.batch * N;
+                k_copy<T><<<r.num_sms * 4, 256, 0, r.stream>>>(dst, ws1, n, r.batch, r.counters);
+                if (r.launches) ++*r.launches;
+                e = cudaGetLastError();
+                dst = ws1;
+            }
+        } else {  // V_STOCKHAM
+            a.S0 = done;
+            a.qmode = QM_LINEAR;
+            a.in_order = (L - done - K[i]) > 0 ? ORD_T_FAST : ORD_C_FAST;
+            a.out_order = ORD_T_FAST;
+            e = run_pass<F, V_STOCKHAM, LAY_VARIANT>(a, r.stream, r.num_sms, r.launches);
+            done += K[i];
+        }
+        if (e != cudaSuccess) return e;
+        cur = dst;
+    }
+    return cudaSuccess;
+}
+
+template <class F>
+cudaError_t run_sixstep(const MultipassReq& r) {
+    using T = typename F::T;
+    constexpr int elog = tile_elems_log2<T>();
+    int l1 = 0, l2 = 0;
+    while ((1ull << l1) < r.n1) ++l1;
+    while ((1ull << l2) < r.n2) ++l2;
+    T* rows = static_cast<T*>(r.ws);
+    cudaError_t e;
+    // pass A: x[i::n1] -> bitrev + DIT(n2) -> * w^(i*k2) -> rows[i][k2]
+    {
+        PassArgs<F> a = base_args<F>(r);
+        a.in = static_cast<const T*>(r.in);
+        a.out = rows;
+        a.l1 = l1; a.l2 = l2;
+        a.K = l2;
+        int tq = l2 >= elog ? 1 : 1 << (elog - l2);
+        if (tq > (1 << l1)) tq = 1 << l1;
+        a.TQ = tq > 256 ? 256 : tq;
+        a.qmode = QM_LINEAR; a.in_order = ORD_T_FAST; a.out_order = ORD_C_FAST;
+        a.rev_first = l2 > 0;
+        a.count_bitrev = 0;
+        a.tw = static_cast<const typename F::Tw*>(r.tw2);
+        a.tw_main = r.cor_lo ? nullptr : static_cast<const typename F::Tw*>(r.tw);
+        a.cor_lo = static_cast<const T*>(r.cor_lo);
+        a.cor_hi = static_cast<const T*>(r.cor_hi);
+        a.cor_lb = r.cor_lb;
+        if (l2 == 0) { a.K = 0; }
+        e = run_pass<F, V_DIT, LAY_SIX_A>(a, r.stream, r.num_sms, r.launches);
+        if (e != cudaSuccess) return e;
+    }
+    // pass B: rows[:, k2] -> bitrev + DIT(n1) -> out[n2*k1 + k2]
+    {
+        PassArgs<F> a = base_args<F>(r);
+        a.in = rows;
+        a.out = static_cast<T*>(r.out);
+        a.l1 = l1; a.l2 = l2;
+        a.K = l1;
+        int tq = l1 >= elog ? 1 : 1 << (elog - l1);
+        if (tq > (1 << l2)) tq = 1 << l2;
+        a.TQ = tq > 256 ? 256 : tq;
+        a.qmode = QM_LINEAR; a.in_order = ORD_T_FAST; a.out_order = ORD_T_FAST;
+        a.rev_first = l1 > 0;
+        a.count_row = 1;
+        a.tw = static_cast<const typename F::Tw*>(r.tw1);
+        a.scale = r.scale;
+        e = run_pass<F, V_DIT, LAY_SIX_B>(a, r.stream, r.num_sms, r.launches);
+    }
+    return e;
+}
+
+template <class F>
+cudaError_t launch_field(const MultipassReq& r) {
+    using T = typename F::T;
+    if (r.batch == 0) return cudaSuccess;
+    if (r.variant == V_NAIVE) {
+        const uint64_t total = r.batch << r.L;
+        const uint64_t blocks = (total + 255) / 256, cap = (uint64_t)r.num_sms * 16;
+        F f;
+        f.p = (T)r.p;
+        k_naive<F><<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, r.stream>>>(
+            static_cast<const T*>(r.in), static_cast<T*>(r.out), r.batch, r.L,
+            static_cast<const typename F::Tw*>(r.tw), f, r.scale, make_tw<F>(r.ninv, r.ninv_shoup), r.counters);
+        if (r.launches) ++*r.launches;
+        return cudaGetLastError();
+    }
+    switch (r.variant) {
+        case V_DIT: return run_variant<F, V_DIT>(r);
+        case V_DIF: return run_variant<F, V_DIF>(r);
+        case V_FLAT: return run_variant<F, V_FLAT>(r);
+        case V_PEASE: return run_variant<F, V_PEASE>(r);
+        case V_PEASE_NC: return run_variant<F, V_PEASE_NC>(r);
+        case V_STOCKHAM: return run_variant<F, V_STOCKHAM>(r);
+        case V_SIXSTEP: return run_sixstep<F>(r);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <class F>
+cudaError_t pointwise_field(uint64_t p, const void* a, const void* b, void* c, uint64_t n, cudaStream_t s,
+                            int num_sms, int* launches) {
+    using T = typename F::T;
+    F f;
+    f.p = (T)p;
+    uint64_t blocks = (n + 255) / 256, cap = (uint64_t)num_sms * 8;
+    if (n == 0) return cudaSuccess;
+    k_pointwise<F><<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(
+        static_cast<const T*>(a), static_cast<const T*>(b), static_cast<T*>(c), n, f);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace nttb200

@@ -1,0 +1,548 @@
+// ntt_api.cu -- implementation of include/ntt_b200.h.
+//
+// Host-side pieces (field validation, twiddle tables, plans) are native C++;
+// every transform runs on the B200.  There is no CPU fallback: with no CUDA
+// device every exec returns NTT_E_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/ntt_b200.h"
+#include "launch.cuh"
+#include "multipass.cuh"
+
+using namespace nttb200;
+typedef unsigned __int128 u128;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<unsigned long long> g_launches{0};
+std::atomic<int> g_counters_enabled{0};
+std::mutex g_mu;
+std::map<int, unsigned long long*> g_dev_counters;   // device -> 4 counters
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(NTT_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- field --
+// modmath.py:23-45 is_prime (deterministic Miller-Rabin for n < 2^64)
+uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) { return (uint64_t)((u128)a * b % m); }
+uint64_t powmod(uint64_t b, uint64_t e, uint64_t m) {
+    uint64_t r = 1 % m;
+    b %= m;
+    while (e) {
+        if (e & 1) r = mulmod(r, b, m);
+        b = mulmod(b, b, m);
+        e >>= 1;
+    }
+    return r;
+}
+
+bool is_prime(uint64_t n) {
+    if (n < 2) return false;
+    static const uint64_t small[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+    for (uint64_t s : small)
+        if (n % s == 0) return n == s;
+    uint64_t d = n - 1;
+    int r = 0;
+    while ((d & 1) == 0) { d >>= 1; ++r; }
+    for (uint64_t a : small) {
+        uint64_t x = powmod(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int i = 0; i < r - 1; ++i) {
+            x = mulmod(x, x, n);
+            if (x == n - 1) { comp = false; break; }
+        }
+        if (comp) return false;
+    }
+    return true;
+}
+
+// modmath.py:48-60 prime_factors (trial division; stops early once the
+// cofactor is prime -- same factor set, bounded time for 64-bit p-1)
+std::vector<uint64_t> prime_factors(uint64_t n) {
+    std::vector<uint64_t> f;
+    for (uint64_t d = 2; d <= n / d; d += (d == 2 ? 1 : 2)) {
+        if (n % d == 0) {
+            f.push_back(d);
+            while (n % d == 0) n /= d;
+            if (n > 1 && is_prime(n)) break;
+        }
+    }
+    if (n > 1) f.push_back(n);
+    return f;
+}
+
+bool is_generator(uint64_t g, uint64_t p, const std::vector<uint64_t>& fac) {
+    for (uint64_t q : fac)
+        if (powmod(g, (p - 1) / q, p) == 1) return false;
+    return true;
+}
+
+int check_field(uint64_t p, uint64_t g, int w) {
+    if (!is_prime(p)) return fail(NTT_E_NOT_PRIME, std::to_string(p) + " is not prime");
+    if (w < 2 || w > 64) return fail(NTT_E_INVALID, "word width w must be in [2, 64]");
+    if (p == 2 || (w < 64 && p >= (1ull << w)))
+        return fail(NTT_E_INVALID, "p must be odd and fit in " + std::to_string(w) + " bits");
+    if (!(2 <= g && g < p)) return fail(NTT_E_INVALID, "generator out of range");
+    if (!is_generator(g, p, prime_factors(p - 1)))
+        return fail(NTT_E_INVALID, std::to_string(g) + " is not a primitive root of " + std::to_string(p));
+    return NTT_OK;
+}
+
+bool pow2(uint64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+int ilog2(uint64_t n) { int l = 0; while ((1ull << l) < n) ++l; return l; }
+
+uint64_t shoup_word(uint64_t tw, uint64_t p, int w) { return (uint64_t)(((u128)tw << w) / p); }
+
+constexpr uint64_t kGold = 0xFFFFFFFF00000001ull;
+
+int field_kind(uint64_t p, int word_bytes) {
+    if (word_bytes == 4) return p < (1ull << 31) ? 0 : 1;
+    return p == kGold ? 2 : 3;
+}
+
+// ---------------------------------------------------------------- tables --
+struct DevTable {
+    int device = -1;
+    void* tw = nullptr;       // F::Tw[N]
+    uint64_t bytes = 0;
+    uint64_t n_inv = 0, n_inv_dev_shoup = 0;
+    ~DevTable() {
+        if (tw) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(device);
+            cudaFree(tw);
+            cudaSetDevice(cur);
+        }
+    }
+};
+
+using TableKey = std::tuple<uint64_t, uint64_t, uint64_t, int, int, int>;  // p,g,n,dir,word,device
+std::map<TableKey, std::weak_ptr<DevTable>> g_tables;
+
+// Host table per twiddle.py:57-88 (repeated multiplication by omega).
+void host_powers(uint64_t p, uint64_t omega, uint64_t n, std::vector<uint64_t>& w_pow) {
+    w_pow.resize(n);
+    w_pow[0] = 1;
+    for (uint64_t i = 1; i < n; ++i) w_pow[i] = mulmod(w_pow[i - 1], omega, p);
+}
+
+int get_dev_table(uint64_t p, uint64_t g, uint64_t n, int dir, int word, int device,
+                  std::shared_ptr<DevTable>& out) {
+    TableKey key{p, g, n, dir, word, device};
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_tables.find(key);
+    if (it != g_tables.end()) {
+        if (auto sp = it->second.lock()) { out = sp; return NTT_OK; }
+    }
+    uint64_t omega = powmod(g, (p - 1) / n, p);
+    if (dir == NTT_INVERSE) omega = powmod(omega, p - 2, p);
+    std::vector<uint64_t> w_pow;
+    host_powers(p, omega, n, w_pow);
+    const int kind = field_kind(p, word);
+    auto t = std::make_shared<DevTable>();
+    t->device = device;
+    std::vector<unsigned char> buf;
+    if (kind == 0 || kind == 1) {
+        buf.resize(n * 8);
+        uint32_t* d = reinterpret_cast<uint32_t*>(buf.data());
+        for (uint64_t i = 0; i < n; ++i) { d[2 * i] = (uint32_t)w_pow[i]; d[2 * i + 1] = (uint32_t)shoup_word(w_pow[i], p, 32); }
+    } else if (kind == 2) {
+        buf.resize(n * 8);
+        memcpy(buf.data(), w_pow.data(), n * 8);
+    } else {
+        buf.resize(n * 16);
+        uint64_t* d = reinterpret_cast<uint64_t*>(buf.data());
+        for (uint64_t i = 0; i < n; ++i) { d[2 * i] = w_pow[i]; d[2 * i + 1] = shoup_word(w_pow[i], p, 64); }
+    }
+    if (dir == NTT_INVERSE) {
+        t->n_inv = powmod(n % p, p - 2, p);
+        t->n_inv_dev_shoup = shoup_word(t->n_inv, p, word == 4 ? 32 : 64);
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaMalloc(&t->tw, buf.size());
+    if (e == cudaSuccess) e = cudaMemcpy(t->tw, buf.data(), buf.size(), cudaMemcpyHostToDevice);
+    cudaSetDevice(cur);
+    if (e != cudaSuccess) { t->tw = nullptr; return cuda_fail(e, "twiddle table upload"); }
+    t->bytes = buf.size();
+    g_tables[key] = t;
+    out = t;
+    return NTT_OK;
+}
+
+unsigned long long* dev_counters(int device) {
+    if (!g_counters_enabled.load()) return nullptr;
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_dev_counters.find(device);
+    if (it != g_dev_counters.end()) return it->second;
+    unsigned long long* d = nullptr;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    if (cudaMalloc(&d, C_NCOUNTERS * sizeof(unsigned long long)) != cudaSuccess) d = nullptr;
+    else cudaMemset(d, 0, C_NCOUNTERS * sizeof(unsigned long long));
+    cudaSetDevice(cur);
+    g_dev_counters[device] = d;
+    return d;
+}
+
+}  // namespace
+
+struct ntt_plan_s {
+    uint64_t p, g, n, n1, n2;
+    int w, variant, dir, word, device, kind, L;
+    std::shared_ptr<DevTable> table, table1, table2;   // main, six-step n1 / n2 sub-tables
+    // six-step correction twiddles w^e = cor_hi[e >> cor_lb] * cor_lo[e mod 2^cor_lb] (exact)
+    void* cor_lo = nullptr;
+    void* cor_hi = nullptr;
+    int cor_lb = 0;
+    int num_sms = 148;
+    // workspace for multi-pass plans and host-buffer execution
+    void* ws = nullptr;
+    uint64_t ws_bytes = 0;
+    void* hbuf = nullptr;
+    uint64_t hbuf_bytes = 0;
+    std::mutex mu;
+    ~ntt_plan_s() {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        if (ws) cudaFree(ws);
+        if (hbuf) cudaFree(hbuf);
+        if (cor_lo) cudaFree(cor_lo);
+        if (cor_hi) cudaFree(cor_hi);
+        cudaSetDevice(cur);
+    }
+};
+
+namespace {
+
+int grow(void*& ptr, uint64_t& have, uint64_t need) {
+    if (have >= need) return NTT_OK;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    have = 0;
+    cudaError_t e = cudaMalloc(&ptr, need);
+    if (e != cudaSuccess) return cuda_fail(e, "workspace allocation");
+    have = need;
+    return NTT_OK;
+}
+
+cudaError_t launch_mp_kind(int kind, const MultipassReq& r) {
+    switch (kind) {
+        case 0: return mp_launch_f32s(r);
+        case 1: return mp_launch_f32w(r);
+        case 2: return mp_launch_gold(r);
+        default: return mp_launch_f64(r);
+    }
+}
+
+int smem_max_log2_word(int word) { return single_pass_max_log2(word); }
+
+// Upload count residues omega^(i*step) (device word) for the two-level
+// six-step correction table.
+int upload_powers(uint64_t p, uint64_t base, uint64_t count, int word, int device, void** out) {
+    std::vector<uint64_t> v(count);
+    uint64_t x = 1;
+    for (uint64_t i = 0; i < count; ++i) { v[i] = x; x = mulmod(x, base, p); }
+    std::vector<unsigned char> buf(count * word);
+    if (word == 4) { uint32_t* d = reinterpret_cast<uint32_t*>(buf.data()); for (uint64_t i = 0; i < count; ++i) d[i] = (uint32_t)v[i]; }
+    else memcpy(buf.data(), v.data(), count * 8);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaMalloc(out, buf.size());
+    if (e == cudaSuccess) e = cudaMemcpy(*out, buf.data(), buf.size(), cudaMemcpyHostToDevice);
+    cudaSetDevice(cur);
+    if (e != cudaSuccess) { *out = nullptr; return cuda_fail(e, "correction table upload"); }
+    return NTT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ntt_abi_version(void) { return NTT_B200_ABI_VERSION; }
+const char* ntt_last_error(void) { return g_last_error.c_str(); }
+
+int ntt_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); return 0; }
+    return n;
+}
+
+int ntt_field_check(uint64_t p, uint64_t g, int w_bits) { return check_field(p, g, w_bits); }
+
+int ntt_find_primitive_root(uint64_t p, uint64_t* g_out) {
+    if (!is_prime(p)) return fail(NTT_E_NOT_PRIME, std::to_string(p) + " is not prime");
+    if (p == 2) { *g_out = 1; return NTT_OK; }
+    auto fac = prime_factors(p - 1);
+    for (uint64_t g = 2; g < p; ++g)
+        if (is_generator(g, p, fac)) { *g_out = g; return NTT_OK; }
+    return fail(NTT_E_NOT_PRIME, "no generator found");
+}
+
+int ntt_root_of_unity(uint64_t p, uint64_t g, uint64_t n, uint64_t* omega_out) {
+    if (!pow2(n)) return fail(NTT_E_NOT_POWER_OF_TWO, "size " + std::to_string(n) + " is not a power of two");
+    if ((p - 1) % n) return fail(NTT_E_SIZE_NOT_SUPPORTED, std::to_string(n) + " does not divide p-1 = " + std::to_string(p - 1));
+    *omega_out = powmod(g, (p - 1) / n, p);
+    return NTT_OK;
+}
+
+int ntt_table_build(uint64_t p, uint64_t g, int w_bits, uint64_t n, int direction, uint64_t* w_pow,
+                    uint64_t* w_shoup, uint64_t* n_inv, uint64_t* n_inv_shoup) {
+    if (direction != NTT_FORWARD && direction != NTT_INVERSE) return fail(NTT_E_INVALID, "unknown direction");
+    uint64_t omega = 0;
+    int st = ntt_root_of_unity(p, g, n, &omega);
+    if (st) return st;
+    if (direction == NTT_INVERSE) omega = powmod(omega, p - 2, p);
+    std::vector<uint64_t> wp;
+    host_powers(p, omega, n, wp);
+    memcpy(w_pow, wp.data(), n * 8);
+    for (uint64_t i = 0; i < n; ++i) w_shoup[i] = shoup_word(wp[i], p, w_bits);
+    if (direction == NTT_INVERSE) {
+        uint64_t ni = powmod(n % p, p - 2, p);
+        if (n_inv) *n_inv = ni;
+        if (n_inv_shoup) *n_inv_shoup = shoup_word(ni, p, w_bits);
+    }
+    return NTT_OK;
+}
+
+int ntt_plan_create(uint64_t p, uint64_t g, int w_bits, uint64_t n, int variant, int direction, uint64_t n1,
+                    uint64_t n2, int word_bytes, int device, ntt_plan_t* plan_out) {
+    if (!plan_out) return fail(NTT_E_INVALID, "plan_out is NULL");
+    *plan_out = nullptr;
+    if (variant < NTT_NAIVE || variant > NTT_SIXSTEP)
+        return fail(NTT_E_UNSUPPORTED_VARIANT, "unknown variant id " + std::to_string(variant));
+    if (n < 2 || !pow2(n))
+        return fail(NTT_E_NOT_POWER_OF_TWO, "transform size " + std::to_string(n) + " is not a power of two >= 2");
+    if (direction != NTT_FORWARD && direction != NTT_INVERSE) return fail(NTT_E_INVALID, "unknown direction");
+    int st = check_field(p, g, w_bits);
+    if (st) return st;
+    if ((p - 1) % n)
+        return fail(NTT_E_SIZE_NOT_SUPPORTED, std::to_string(n) + " does not divide p-1 = " + std::to_string(p - 1));
+    if (word_bytes != 4 && word_bytes != 8) return fail(NTT_E_INVALID, "word_bytes must be 4 or 8");
+    if (word_bytes == 4 && p >= (1ull << 32)) return fail(NTT_E_INVALID, "uint32 storage needs p < 2^32");
+    const int L = ilog2(n);
+    if (variant == NTT_SIXSTEP) {
+        if (n1 == 0 && n2 == 0) { n1 = 1ull << ((L + 1) / 2); n2 = n / n1; }
+        else if (n1 == 0) n1 = n2 ? n / n2 : 0;
+        else if (n2 == 0) n2 = n / n1;
+        if (n1 < 1 || n2 < 1 || (u128)n1 * n2 != n || !pow2(n1) || !pow2(n2))
+            return fail(NTT_E_BAD_FACTORIZATION, std::to_string(n1) + " * " + std::to_string(n2) + " != " +
+                                                     std::to_string(n) + " (powers of two required)");
+    } else {
+        n1 = n2 = 0;
+    }
+    int ndev = ntt_device_count();
+    if (ndev <= 0) return fail(NTT_E_NO_DEVICE, "no CUDA device visible: the B200 engine has no CPU fallback");
+    if (device < 0 || device >= ndev) return fail(NTT_E_INVALID, "device ordinal out of range");
+    if (variant == NTT_NAIVE && L > 16) return fail(NTT_E_SIZE_NOT_SUPPORTED, "naive DFT is limited to N <= 2^16");
+    std::unique_ptr<ntt_plan_s> pl(new ntt_plan_s());
+    pl->p = p; pl->g = g; pl->n = n; pl->n1 = n1; pl->n2 = n2; pl->w = w_bits; pl->variant = variant;
+    pl->dir = direction; pl->word = word_bytes; pl->device = device; pl->kind = field_kind(p, word_bytes);
+    pl->L = L;
+    if (variant == NTT_SIXSTEP) {
+        // the six-step kernels only read the n1 / n2 sub-tables and the
+        // two-level correction tables; no size-N table on the device
+        pl->table = std::make_shared<DevTable>();
+        pl->table->device = device;
+        if (direction == NTT_INVERSE) {
+            pl->table->n_inv = powmod(n % p, p - 2, p);
+            pl->table->n_inv_dev_shoup = shoup_word(pl->table->n_inv, p, word_bytes == 4 ? 32 : 64);
+        }
+    } else {
+        st = get_dev_table(p, g, n, direction, word_bytes, device, pl->table);
+        if (st) return st;
+    }
+    if (variant == NTT_SIXSTEP) {
+        if (ilog2(n1) > smem_max_log2_word(word_bytes) || ilog2(n2) > smem_max_log2_word(word_bytes))
+            return fail(NTT_E_SIZE_NOT_SUPPORTED, "six-step sub-transforms must fit in shared memory");
+        if (n1 > 1 && (st = get_dev_table(p, g, n1, direction, word_bytes, device, pl->table1))) return st;
+        if (n2 > 1 && (st = get_dev_table(p, g, n2, direction, word_bytes, device, pl->table2))) return st;
+        uint64_t omega = powmod(g, (p - 1) / n, p);
+        if (direction == NTT_INVERSE) omega = powmod(omega, p - 2, p);
+        pl->cor_lb = (L + 1) / 2;
+        if ((st = upload_powers(p, omega, 1ull << pl->cor_lb, word_bytes, device, &pl->cor_lo))) return st;
+        if ((st = upload_powers(p, powmod(omega, 1ull << pl->cor_lb, p), 1ull << (L - pl->cor_lb), word_bytes,
+                                device, &pl->cor_hi))) return st;
+    }
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
+        pl->num_sms = sms;
+    *plan_out = pl.release();
+    return NTT_OK;
+}
+
+int ntt_plan_destroy(ntt_plan_t plan) {
+    delete plan;
+    return NTT_OK;
+}
+
+int ntt_plan_info(ntt_plan_t plan, ntt_plan_info_t* info) {
+    if (!plan || !info) return fail(NTT_E_INVALID, "NULL argument");
+    memset(info, 0, sizeof(*info));
+    info->p = plan->p; info->g = plan->g; info->n = plan->n; info->n1 = plan->n1; info->n2 = plan->n2;
+    info->w_bits = plan->w; info->variant = plan->variant; info->direction = plan->dir;
+    info->word_bytes = plan->word; info->device = plan->device; info->field_kind = plan->kind;
+    if (plan->variant == NTT_SIXSTEP) info->passes = 2;
+    else if (plan->variant == NTT_NAIVE || plan->L <= smem_max_log2_word(plan->word)) info->passes = 1;
+    else info->passes = mp_num_passes(plan->L, plan->word, plan->variant);
+    info->n_inv = plan->table->n_inv;
+    info->n_inv_shoup = plan->dir == NTT_INVERSE ? shoup_word(plan->table->n_inv, plan->p, plan->w) : 0;
+    info->device_table_bytes = plan->table->bytes + (plan->table1 ? plan->table1->bytes : 0) +
+                               (plan->table2 ? plan->table2->bytes : 0);
+    return NTT_OK;
+}
+
+uint64_t ntt_plan_workspace_bytes(ntt_plan_t plan, uint64_t batch) {
+    if (!plan) return 0;
+    if (plan->variant == NTT_SIXSTEP) return batch * plan->n * plan->word;
+    if (plan->variant == NTT_NAIVE || plan->L <= smem_max_log2_word(plan->word)) return 0;
+    return mp_workspace_bytes(plan->L, plan->word, plan->variant, batch);
+}
+
+static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t batch, unsigned flags,
+                       cudaStream_t stream) {
+    const bool scale = (flags & NTT_FLAG_SCALE) != 0;
+    if (scale && plan->dir != NTT_INVERSE) return fail(NTT_E_INVALID, "intt requires an inverse-direction table");
+    if (batch == 0) return NTT_OK;
+    if (!d_in || !d_out) return fail(NTT_E_INVALID, "NULL buffer");
+    unsigned long long* ctr = dev_counters(plan->device);
+    uint64_t need = ntt_plan_workspace_bytes(plan, batch);
+    if (need) {
+        std::lock_guard<std::mutex> lk(plan->mu);
+        int st = grow(plan->ws, plan->ws_bytes, need);
+        if (st) return st;
+    }
+    int launches = 0;
+    MultipassReq r{};
+    r.variant = plan->variant; r.L = plan->L; r.in = d_in; r.out = d_out; r.batch = batch;
+    r.tw = plan->table->tw; r.p = plan->p; r.scale = scale;
+    r.ninv = plan->table->n_inv; r.ninv_shoup = plan->table->n_inv_dev_shoup;
+    r.counters = ctr; r.stream = stream; r.num_sms = plan->num_sms; r.launches = &launches;
+    r.ws = plan->ws;
+    if (plan->variant == NTT_SIXSTEP) {
+        r.n1 = plan->n1; r.n2 = plan->n2;
+        r.tw1 = plan->table1 ? plan->table1->tw : nullptr;
+        r.tw2 = plan->table2 ? plan->table2->tw : nullptr;
+        r.cor_lo = plan->cor_lo; r.cor_hi = plan->cor_hi; r.cor_lb = plan->cor_lb;
+    }
+    cudaError_t e = launch_mp_kind(plan->kind, r);
+    g_launches += launches;
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    return NTT_OK;
+}
+
+int ntt_exec(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t batch, unsigned flags, void* stream) {
+    if (!plan) return fail(NTT_E_INVALID, "NULL plan");
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != plan->device) cudaSetDevice(plan->device);
+    int st = exec_device(plan, d_in, d_out, batch, flags, static_cast<cudaStream_t>(stream));
+    if (cur != plan->device) cudaSetDevice(cur);
+    return st;
+}
+
+int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch, unsigned flags, void* stream) {
+    if (!plan) return fail(NTT_E_INVALID, "NULL plan");
+    if (batch == 0) return NTT_OK;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != plan->device) cudaSetDevice(plan->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t bytes = batch * plan->n * plan->word;
+    int st = NTT_OK;
+    {
+        std::lock_guard<std::mutex> lk(plan->mu);
+        st = grow(plan->hbuf, plan->hbuf_bytes, bytes);
+    }
+    cudaError_t e = cudaSuccess;
+    if (!st) {
+        e = cudaMemcpyAsync(plan->hbuf, h_in, bytes, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) st = cuda_fail(e, "H2D copy");
+    }
+    if (!st) st = exec_device(plan, plan->hbuf, plan->hbuf, batch, flags, s);
+    if (!st) {
+        e = cudaMemcpyAsync(h_out, plan->hbuf, bytes, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = cuda_fail(e, "D2H copy");
+    }
+    if (cur != plan->device) cudaSetDevice(cur);
+    return st;
+}
+
+int ntt_pointwise_mul(ntt_plan_t plan, const void* d_a, const void* d_b, void* d_c, uint64_t count, void* stream) {
+    if (!plan) return fail(NTT_E_INVALID, "NULL plan");
+    int launches = 0;
+    cudaError_t e = pointwise_launch(plan->kind, plan->p, d_a, d_b, d_c, count,
+                                     static_cast<cudaStream_t>(stream), plan->num_sms, &launches);
+    g_launches += launches;
+    if (e != cudaSuccess) return cuda_fail(e, "pointwise_mul");
+    return NTT_OK;
+}
+
+int ntt_counters_enable(int enable) {
+    g_counters_enabled = enable ? 1 : 0;
+    return NTT_OK;
+}
+
+int ntt_counters_read(ntt_counters_t* out) {
+    if (!out) return fail(NTT_E_INVALID, "NULL argument");
+    memset(out, 0, sizeof(*out));
+    out->kernel_launches = g_launches.load();
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto& kv : g_dev_counters) {
+        if (!kv.second) continue;
+        unsigned long long h[C_NCOUNTERS] = {0};
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(kv.first);
+        cudaError_t e = cudaMemcpy(h, kv.second, sizeof(h), cudaMemcpyDeviceToHost);
+        cudaSetDevice(cur);
+        if (e != cudaSuccess) return cuda_fail(e, "counter read");
+        out->transforms += h[C_TRANSFORMS];
+        out->bitrev_passes += h[C_BITREV];
+        out->stage_copies += h[C_COPIES];
+        out->hbm_passes += h[C_HBM];
+    }
+    return NTT_OK;
+}
+
+int ntt_counters_reset(void) {
+    g_launches = 0;
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto& kv : g_dev_counters) {
+        if (!kv.second) continue;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(kv.first);
+        cudaMemset(kv.second, 0, C_NCOUNTERS * sizeof(unsigned long long));
+        cudaDeviceSynchronize();
+        cudaSetDevice(cur);
+    }
+    return NTT_OK;
+}
+
+}  // extern "C"

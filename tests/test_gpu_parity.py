@@ -1,0 +1,279 @@
+"""Parity of the B200 kernels against the CPU oracle (oracle/ntt_oracle.c, pinned
+to the reference by tests/test_oracle_pins.py) and against vectors produced by
+the reference itself (tests/golden/reference_vectors.json, SURVEY.md sec.8c hashes).
+
+Every comparison is bit-exact (integer arithmetic).  Calls go through the
+package's public API, which executes through the C ABI (libntt_b200.so).
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2405_11353_b200 as P  # noqa: E402
+from paper_2405_11353_b200.configs import CONFIGS, GOLDEN, seeded_input  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+GOLD = (1 << 64) - (1 << 32) + 1
+# (name, p, g, w, dtype, max log2 N exercised)
+FIELDS = [
+    ("p998", 998244353, 3, 32, np.uint32, 20),
+    ("default", 3221225473, 5, 32, np.uint32, 16),
+    ("goldilocks", GOLD, 7, 64, np.uint64, 16),
+    ("p998_u64", 998244353, 3, 64, np.uint64, 12),
+    ("big64", 18446744069414584321, 7, 64, np.uint64, 6),   # placeholder, replaced below
+]
+VARIANTS7 = ("dit", "dif", "flat", "pease", "pease_nc", "stockham", "sixstep")
+
+
+def _generic64():
+    """An NTT-friendly 64-bit prime > 2^63 that is NOT Goldilocks (F64 path)."""
+    for c in range((1 << 32) - 2, 1 << 31, -1):
+        p = c * (1 << 32) + 1
+        if p != GOLD and P.is_prime(p):
+            return p, P.find_primitive_root(p)
+    raise RuntimeError("no prime found")
+
+
+@pytest.fixture(scope="module")
+def fields():
+    p, g = _generic64()
+    fl = list(FIELDS[:-1]) + [("generic64", p, g, 64, np.uint64, 12)]
+    return {f[0]: f for f in fl}
+
+
+def dev():
+    return torch.device("cuda", 0)
+
+
+def to_dev(x: np.ndarray):
+    if x.dtype == np.uint32:
+        return torch.from_numpy(x.view(np.int32)).view(torch.uint32).to(dev())
+    return torch.from_numpy(x.view(np.int64)).view(torch.uint64).to(dev())
+
+
+def to_host(t) -> np.ndarray:
+    if t.dtype == torch.uint32:
+        return t.cpu().view(torch.int32).numpy().view(np.uint32)
+    return t.cpu().view(torch.int64).numpy().view(np.uint64)
+
+
+def gpu_ntt(x, p, g, w, variant, inverse=False, scale=False, n1=None):
+    params = P.FieldParams(p, g, w)
+    n = x.shape[-1]
+    if variant == "sixstep":
+        plan = P.make_plan(params, "sixstep", n, P.INVERSE if inverse else P.FORWARD, n1=n1)
+        if inverse and scale:
+            return to_host(P.run_plan(plan, to_dev(x)))
+        if inverse:
+            return to_host(P.algorithms._execute(to_dev(x), params, n, "sixstep", P.INVERSE, False,
+                                                 plan.n1, plan.n2))
+        return to_host(P.ntt_sixstep(to_dev(x), plan))
+    table = P.build_table(params, n, P.INVERSE if inverse else P.FORWARD)
+    if scale:
+        return to_host(P.intt(to_dev(x), table, variant))
+    return to_host(P.ntt(to_dev(x), table, variant))
+
+
+def rand(p, B, L, dt, seed):
+    return np.random.default_rng(seed).integers(0, p, size=(B, 1 << L), dtype=np.uint64).astype(dt)
+
+
+@pytest.mark.parametrize("variant", VARIANTS7 + ("naive",))
+@pytest.mark.parametrize("fname", ["p998", "default", "goldilocks", "p998_u64", "generic64"])
+def test_variant_vs_oracle_small(fields, fname, variant):
+    _, p, g, w, dt, maxl = fields[fname]
+    for L in range(1, min(maxl, 10) + 1):
+        if variant == "naive" and L > 9:
+            continue
+        B = 3 if L > 6 else 17
+        x = rand(p, B, L, dt, 1000 + L)
+        want = O.ntt(x, p, g, w, variant if variant != "naive" else "dit")
+        got = gpu_ntt(x, p, g, w, variant)
+        assert np.array_equal(got, want), (fname, variant, L)
+
+
+@pytest.mark.parametrize("variant", VARIANTS7)
+@pytest.mark.parametrize("fname", ["p998", "default", "goldilocks"])
+def test_variant_inverse_and_intt(fields, fname, variant):
+    _, p, g, w, dt, maxl = fields[fname]
+    for L in (1, 5, 11, 13):
+        x = rand(p, 4, L, dt, 2000 + L)
+        want_u = O.ntt(x, p, g, w, variant, inverse=True)
+        want_s = O.ntt(x, p, g, w, variant, inverse=True, scale=True)
+        assert np.array_equal(gpu_ntt(x, p, g, w, variant, inverse=True), want_u), (fname, variant, L)
+        assert np.array_equal(gpu_ntt(x, p, g, w, variant, inverse=True, scale=True), want_s), (fname, variant, L)
+
+
+@pytest.mark.parametrize("variant", VARIANTS7)
+@pytest.mark.parametrize("fname,L", [("p998", 14), ("p998", 15), ("p998", 16), ("p998", 18),
+                                     ("default", 16), ("goldilocks", 13), ("goldilocks", 14),
+                                     ("goldilocks", 16), ("generic64", 14)])
+def test_variant_vs_oracle_large(fields, fname, L, variant):
+    _, p, g, w, dt, _ = fields[fname]
+    x = rand(p, 2, L, dt, 3000 + L)
+    want = O.ntt(x, p, g, w, variant)
+    assert np.array_equal(gpu_ntt(x, p, g, w, variant), want), (fname, variant, L)
+
+
+def test_reference_golden_vectors(golden):
+    """Every case the reference produced (all variants agree there) -- forward,
+    unscaled inverse, intt -- reproduced by every GPU variant."""
+    fmeta = golden["fields"]
+    for case in golden["cases"]:
+        fm = fmeta[case["field"]]
+        p, g, w = fm["p"], fm["g"], fm["w"]
+        dt = np.uint32 if p < (1 << 32) else np.uint64
+        x = np.array(case["x"], dtype=np.uint64).astype(dt)[None, :]
+        for v in case["variants_checked"]:
+            if v == "naive" or (v == "sixstep" and case["n"] < 2):
+                continue
+            assert gpu_ntt(x, p, g, w, v)[0].tolist() == case["fwd"], (case["field"], case["n"], v)
+            assert gpu_ntt(x, p, g, w, v, inverse=True)[0].tolist() == case["inv_unscaled"]
+            assert gpu_ntt(x, p, g, w, v, inverse=True, scale=True)[0].tolist() == case["intt"]
+        # exact naive on the GPU (the reference's naive overflows for 64-bit p)
+        if case["n"] <= 512:
+            assert gpu_ntt(x, p, g, w, "naive")[0].tolist() == case["fwd"]
+
+
+def test_reference_sixstep_splits(golden):
+    for case in golden["sixstep"]:
+        fm = golden["fields"][case["field"]]
+        p, g, w = fm["p"], fm["g"], fm["w"]
+        dt = np.uint32 if p < (1 << 32) else np.uint64
+        x = np.array(case["x"], dtype=np.uint64).astype(dt)[None, :]
+        got = gpu_ntt(x, p, g, w, "sixstep", n1=case["n1"])
+        assert got[0].tolist() == case["fwd"], (case["field"], case["n"], case["n1"])
+
+
+def test_list_api_and_bench_checksum(golden):
+    """The reference calling convention (list in, list out) + cli bench known answer."""
+    params = P.FieldParams(998244353, 3)
+    for n, rec in golden["bench_checksum"].items():
+        table = P.build_table(params, int(n))
+        for v in VARIANTS7:
+            out = P.ntt(rec["x"], table, v)
+            assert isinstance(out, list) and out[0] == rec["checksum"] == (467606314 if n == "1024" else out[0])
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_config_golden_hash_full(cfg):
+    w = CONFIGS[cfg]
+    x = seeded_input(w)
+    assert O.sha256_le(x) == GOLDEN[cfg][0]
+    for v in w.variants:
+        if v == "naive":
+            continue
+        got = gpu_ntt(x, w.p, w.g, w.w, v, n1=w.n1)
+        assert O.sha256_le(got) == GOLDEN[cfg][1], (cfg, v)
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_config_golden_hash_large(cfg):
+    """Configs 4 (512 x 2^20) and 5 (2^26 Goldilocks six-step): full-output
+    SHA-256 equals the hash the reference itself produced."""
+    w = CONFIGS[cfg]
+    x = seeded_input(w)
+    for v in w.variants:
+        got = gpu_ntt(x, w.p, w.g, w.w, v, n1=w.n1)
+        assert O.sha256_le(got) == GOLDEN[cfg][1], (cfg, v)
+
+
+@pytest.mark.parametrize("variant", ["dit", "dif", "pease_nc", "stockham", "sixstep"])
+def test_round_trip_config4_size(variant):
+    w = CONFIGS[4]
+    x = seeded_input(w, rows=8)
+    y = gpu_ntt(x, w.p, w.g, w.w, variant)
+    z = gpu_ntt(y, w.p, w.g, w.w, variant, inverse=True, scale=True)
+    assert np.array_equal(z, x)
+
+
+def test_linearity_goldilocks_2_16():
+    w = CONFIGS[3]
+    x = seeded_input(w, rows=4)
+    p = w.p
+    a, b = 123456789123456789 % p, 987654321987654321 % p
+    xs, ys = x[:2], x[2:]
+    combo = np.array([[(a * int(u) + b * int(v)) % p for u, v in zip(r1, r2)] for r1, r2 in zip(xs, ys)],
+                     dtype=np.uint64)
+    lhs = gpu_ntt(combo, p, w.g, w.w, "dif")
+    fx, fy = gpu_ntt(xs, p, w.g, w.w, "dif"), gpu_ntt(ys, p, w.g, w.w, "dif")
+    rhs = np.array([[(a * int(u) + b * int(v)) % p for u, v in zip(r1, r2)] for r1, r2 in zip(fx, fy)],
+                   dtype=np.uint64)
+    assert np.array_equal(lhs, rhs)
+
+
+def test_structural_counters():
+    """B200 analogue of test_algorithms.py:116-141: Pease copies back, Pease_nc
+    never does; Stockham never bit-reverses, DIT does."""
+    params = P.FieldParams(3221225473, 5)
+    x = rand(params.p, 8, 6, np.uint32, 9)
+    P.counters_enable(True)
+    for L, B in ((6, 8), (12, 4), (16, 2)):
+        x = rand(params.p, B, L, np.uint32, 9 + L)
+        table = P.build_table(params, 1 << L)
+        res = {}
+        for v in ("pease", "pease_nc", "stockham", "dit"):
+            P.counters_reset()
+            P.ntt(to_dev(x), table, v)
+            torch.cuda.synchronize()
+            res[v] = P.counters_read()
+        assert res["pease"]["stage_copies"] > 0
+        assert res["pease_nc"]["stage_copies"] == 0
+        assert res["stockham"]["bitrev_passes"] == 0
+        assert res["dit"]["bitrev_passes"] == B
+        for v in res:
+            assert res[v]["transforms"] == B, (v, res[v])
+    P.counters_enable(False)
+
+
+def test_edge_cases():
+    params = P.FieldParams(998244353, 3)
+    table = P.build_table(params, 16)
+    inv = P.build_table(params, 16, P.INVERSE)
+    with pytest.raises(P.SizeMismatch):
+        P.ntt(to_dev(np.zeros((2, 8), np.uint32)), table)
+    with pytest.raises(ValueError):
+        P.intt(to_dev(np.zeros((2, 16), np.uint32)), table)
+    # empty batch
+    e = P.ntt(to_dev(np.zeros((0, 16), np.uint32)), table, "pease_nc")
+    assert tuple(e.shape) == (0, 16)
+    # delta -> ones, constant -> (N*c, 0, ...) on every variant (test_algorithms.py:42-55)
+    for v in VARIANTS7:
+        d = np.zeros((1, 16), np.uint32)
+        d[0, 0] = 1
+        assert gpu_ntt(d, params.p, params.g, 32, v).tolist() == [[1] * 16]
+        c = np.full((1, 16), 7, np.uint32)
+        assert gpu_ntt(c, params.p, params.g, 32, v)[0].tolist() == [112] + [0] * 15
+        assert P.intt(P.ntt([5] * 16, table, v), inv, v) == [5] * 16
+    # in-place through the C ABI (d_in == d_out)
+    x = rand(params.p, 4, 12, np.uint32, 77)
+    t = to_dev(x)
+    dp = P.algorithms.device_plan_for(P.make_plan(params, "pease_nc", 4096), 4, 0)
+    dp.exec_device(t.data_ptr(), t.data_ptr(), 4, False, torch.cuda.current_stream().cuda_stream)
+    assert np.array_equal(to_host(t), O.ntt(x, params.p, params.g, 32, "pease_nc"))
+    # p = 17 (the reference fixture field), all sizes it supports
+    p17 = P.FieldParams(17, 3)
+    for L in (1, 2, 3, 4):
+        xx = rand(17, 5, L, np.uint32, L)
+        for v in VARIANTS7:
+            assert np.array_equal(gpu_ntt(xx, 17, 3, 32, v), O.ntt(xx, 17, 3, 32, v))
+    del p17
+
+
+def test_pointwise_mul():
+    params = P.FieldParams(GOLD, 7, 64)
+    dp = P.algorithms.device_plan_for(P.make_plan(params, "dit", 1024), 8, 0)
+    a = rand(GOLD, 1, 10, np.uint64, 1)
+    b = rand(GOLD, 1, 10, np.uint64, 2)
+    ta, tb = to_dev(a), to_dev(b)
+    tc = torch.empty_like(ta)
+    dp.pointwise(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), 1024, torch.cuda.current_stream().cuda_stream)
+    want = [(int(u) * int(v)) % GOLD for u, v in zip(a[0], b[0])]
+    assert to_host(tc)[0].tolist() == want
