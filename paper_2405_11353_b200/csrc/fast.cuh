@@ -1,0 +1,482 @@
+// fast.cuh -- specialised single-pass kernels (whole polynomial in shared
+// memory) for 2^9 <= N <= 2^13: DIT, DIF, Pease, Pease_nc, Stockham.
+//
+// Same stage-faithful dataflows as engine.cuh, specialised at compile time:
+//  * a TEAM of N/16 threads owns one polynomial at a time; each thread holds a
+//    closed 16-element sub-network in registers per group of <= 4 stages;
+//    several teams per CTA share one shared-memory twiddle table; teams sync
+//    with named barriers (bar.sync id, N/16);
+//  * the next polynomial is prefetched by ONE elected thread with a TMA bulk
+//    copy (cp.async.bulk ... mbarrier::complete_tx) into the team's staging
+//    buffer while the current one is being transformed;
+//  * the bit reversal of DIT / Pease is fused into the first group's gather
+//    from the staging buffer, DIF's into the last group's scatter to HBM;
+//    every global store is a coalesced 128-byte warp row;
+//  * stage twiddles come from the per-stage table T[2^(s-1) + k] = w^(k*N/2^s)
+//    (the reference's w_pow entries, reordered) in shared memory -- one
+//    8-byte LDS per DISTINCT twiddle of a thread's group, immediate offsets;
+//  * exchange buffers use a GF(2)-linear XOR swizzle, and each group's
+//    thread->sub-network map is chosen so warp accesses are bank-conflict free.
+#pragma once
+#include <cstdint>
+#include "engine.cuh"
+#include "lazy.cuh"
+
+namespace nttb200 {
+namespace fastk {
+
+NTT_D uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+NTT_D void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+NTT_D void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+NTT_D void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+NTT_D void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+NTT_D void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+NTT_D void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+NTT_D void team_sync(int id, int nthreads) {
+    if (nthreads == 32) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <class T>
+NTT_HD constexpr int lane_bits() { return sizeof(T) == 4 ? 5 : 4; }
+
+// Bit permutation of a thread id onto the free position bits of a group
+// (everything outside the 4-bit register block [B, B+4)).  The first
+// lane_bits() thread bits go to free bits with pairwise distinct residues
+// mod CW, so a warp's accesses hit distinct banks under the XOR-fold swizzle.
+struct Perm {
+    int bit[16];
+};
+NTT_HD constexpr Perm plan_lanes(int L, int B, int CW) {
+    Perm P{};
+    int fr[16] = {};
+    int nf = 0;
+    for (int b = 0; b < L; ++b)
+        if (b < B || b >= B + 4) fr[nf++] = b;
+    bool used[16] = {};
+    bool res[8] = {};
+    int k = 0;
+    for (int i = 0; i < nf && k < CW; ++i) {
+        const int r = fr[i] % CW;
+        if (!res[r]) { res[r] = true; used[i] = true; P.bit[k++] = fr[i]; }
+    }
+    for (int i = 0; i < nf; ++i)
+        if (!used[i]) P.bit[k++] = fr[i];
+    return P;
+}
+
+template <int NBITS>
+NTT_D uint32_t scatter_bits(uint32_t t, const Perm& P) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < NBITS; ++j) r |= ((t >> j) & 1u) << P.bit[j];
+    return r;
+}
+
+template <int L>
+struct Geo {
+    static constexpr int N = 1 << L;
+    static constexpr int TT = 1 << (L - 4);    // threads per team
+    static constexpr int G = (L + 3) / 4;       // register groups
+    static constexpr int K0 = L - 4 * (G - 1);  // short group (first; DIF: last)
+};
+
+template <class A>
+struct FastArgs {
+    using T = typename A::T;
+    using Tw = typename A::Tw;
+    const T* in;
+    T* out;
+    uint64_t batch;
+    const Tw* stw;         // stage table, N entries (index 0 unused)
+    uint64_t p;
+    int scale;
+    Tw ninv;
+    unsigned long long* counters;
+};
+
+// ---------------------------------------------------------------- DIT/DIF --
+// In-place window [b0, b0+kg) of a register block [B, B+4); pbase = position
+// of register 0.  DIT: stages b0+1.. ascending; DIF: descending.
+template <class A, int L, int B, int b0, int kg, bool DIF>
+NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[16], uint32_t pbase, const typename A::Tw* stw) {
+    static_assert(b0 >= B && b0 + kg <= B + 4, "window outside block");
+    constexpr int off = b0 - B;
+#pragma unroll
+    for (int jj = 0; jj < kg; ++jj) {
+        const int j = DIF ? kg - 1 - jj : jj;
+        const int s = b0 + 1 + j;
+        const uint32_t kmask = (1u << (s - 1)) - 1;
+        const typename A::Tw* row = stw + (1u << (s - 1)) + (pbase & kmask);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            if (c & (1 << (off + j))) continue;
+            const uint32_t kc = ((uint32_t)c << B) & kmask;      // compile-time part of k
+            const int hi = c | (1 << (off + j));
+            if (s == 1) {                                         // w^0 = 1
+                if (DIF) ar.dif1(v[c], v[hi]); else ar.dit1(v[c], v[hi]);
+            } else {
+                const typename A::Tw w = row[kc];
+                if (DIF) ar.dif(v[c], v[hi], w); else ar.dit(v[c], v[hi], w);
+            }
+        }
+    }
+}
+
+// -------------------------------------------------------------- Pease -----
+// Networks of 2^kg contiguous positions; a thread holds NB = 16/2^kg of them
+// (network n = registers [n*2^kg, (n+1)*2^kg)).  Constant geometry inside the
+// registers; twiddle k = (B << sg) | (q >> (L - kg - sg)) for butterfly with
+// output-bit prefix B (algorithms.py:216-217 in the rotated frame).
+template <class A, int L, int sg, int kg>
+NTT_D void pease_regs(const A& ar, typename A::T (&v)[16], uint32_t ubase, const typename A::Tw* stw) {
+    using T = typename A::T;
+    constexpr int NB = 16 >> kg;
+    constexpr int H = 1 << (kg - 1);
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+        const uint32_t q = (ubase << (4 - kg)) | n;            // network id (L-kg bits)
+        const uint32_t qtop = sg ? (q >> (L - kg - sg)) : 0u;   // top sg bits of q
+#pragma unroll
+        for (int m = 0; m < kg; ++m) {
+            const int s = sg + m + 1;
+            T nv[1 << kg];
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const uint32_t R = 2u * i;
+                const uint32_t Bp = R >> (kg - m);               // output bits so far (m bits)
+                T x = v[n * (1 << kg) + 2 * i], y = v[n * (1 << kg) + 2 * i + 1];
+                if (s == 1) ar.dit1(x, y);
+                else ar.dit(x, y, stw[(1u << (s - 1)) + ((Bp << sg) | qtop)]);
+                nv[i] = x;
+                nv[i + H] = y;
+            }
+#pragma unroll
+            for (int c = 0; c < (1 << kg); ++c) v[n * (1 << kg) + c] = nv[c];
+        }
+    }
+}
+
+// ------------------------------------------------------------ Stockham ----
+// Window of kg pair bits at [lob, lob+kg) of the position (lob = L-sg-kg);
+// registers c = (w << (4-kg)) | x, x = extra bits just below the window (first
+// group only).  Stage s = sg+m pairs the window's top remaining bit; the
+// output bit is inserted above the previous ones ([c_rest | B] layout);
+// twiddle k = j = (B << sg) | hi (algorithms.py:281-299).
+template <class A, int L, int sg, int kg>
+NTT_D void stockham_regs(const A& ar, typename A::T (&v)[16], uint32_t hi, const typename A::Tw* stw) {
+    using T = typename A::T;
+    constexpr int NB = 16 >> kg;
+    constexpr int H = 1 << (kg - 1);
+#pragma unroll
+    for (int x = 0; x < NB; ++x) {
+#pragma unroll
+        for (int m = 0; m < kg; ++m) {
+            const int s = sg + m;   // 0-based stage
+            T nv[1 << kg];
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const uint32_t Bv = i & ((1u << m) - 1), crest = (uint32_t)i >> m;
+                T a = v[(i << (4 - kg)) | x], b = v[((i + H) << (4 - kg)) | x];
+                if (s == 0) ar.dit1(a, b);
+                else ar.dit(a, b, stw[(1u << s) + ((Bv << sg) | hi)]);
+                nv[(crest << (m + 1)) | Bv] = a;
+                nv[(crest << (m + 1)) | (1u << m) | Bv] = b;
+            }
+#pragma unroll
+            for (int c = 0; c < (1 << kg); ++c) v[(c << (4 - kg)) | x] = nv[c];
+        }
+    }
+}
+
+// -------------------------------------------------------------- kernel ----
+template <class A, int V, int L, int TEAMS>
+__global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a) {
+    using T = typename A::T;
+    using Tw = typename A::Tw;
+    using GG = Geo<L>;
+    constexpr int N = GG::N, TT = GG::TT, G = GG::G, K0 = GG::K0;
+    constexpr int CW = lane_bits<T>();
+    constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);   // permuting groups
+    constexpr int NBUF = PP ? 3 : 2;       // staging + work (+ second work for ping-pong)
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ uint64_t mbar[TEAMS];
+
+    Tw* stw = reinterpret_cast<Tw*>(smem_raw);
+    const int team = threadIdx.x / TT;
+    const uint32_t t = threadIdx.x % TT;
+    T* S = reinterpret_cast<T*>(smem_raw + (size_t)N * sizeof(Tw)) + (size_t)team * NBUF * N;
+    T* W0 = S + N;
+    T* W1 = PP ? S + 2 * N : W0;
+    A ar;
+    ar.init(a.p);
+
+    // twiddle table once per CTA; barriers
+    for (int i = threadIdx.x; i < N; i += blockDim.x) stw[i] = a.stw[i];
+    if (t == 0) mbar_init(&mbar[team], 1);
+    fence_mbar_init();
+    __syncthreads();
+
+    const uint64_t stride = (uint64_t)gridDim.x * TEAMS;
+    uint64_t poly = (uint64_t)blockIdx.x * TEAMS + team;
+    const uint32_t bytes = N * sizeof(T);
+    if (t == 0 && poly < a.batch) {
+        mbar_expect_tx(&mbar[team], bytes);
+        tma_load_1d(S, a.in + poly * N, bytes, &mbar[team]);
+    }
+    uint32_t phase = 0;
+    int copies = 0;
+    const int bar_id = 1 + team;
+
+    for (; poly < a.batch; poly += stride) {
+        T v[16];
+        mbar_wait(&mbar[team], phase);
+        phase ^= 1;
+        T* gout = a.out + poly * N;
+        const uint64_t next = poly + stride;
+
+        if (V == V_DIT || V == V_DIF) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                // ---- geometry of group g (compile time after unrolling)
+                const int B = (V == V_DIT) ? (g == 0 ? 0 : K0 + 4 * (g - 1)) : (g == G - 1 ? 0 : L - 4 * (g + 1));
+                const int kg = (V == V_DIT) ? (g == 0 ? K0 : 4) : (g == G - 1 ? K0 : 4);
+                const bool first = g == 0, last = g == G - 1;
+                uint32_t pbase;
+                if ((V == V_DIT && first) || (V == V_DIF && last)) pbase = brev(t, L - 4) << 4;   // block [0,4)
+                else if ((V == V_DIT && last) || (V == V_DIF && first)) pbase = t;                 // block [L-4,L)
+                else {
+                    // middle groups: lane-planned map (compile-time permutation)
+                    pbase = 0;
+#define NTT_MID(BB)                                                           \
+    if (B == BB) {                                                            \
+        constexpr Perm PM = plan_lanes(L, BB, CW);                            \
+        pbase = scatter_bits<L - 4>(t, PM);                                   \
+    }
+                    NTT_MID(1) NTT_MID(2) NTT_MID(3) NTT_MID(4) NTT_MID(5) NTT_MID(6) NTT_MID(7)
+                    NTT_MID(8) NTT_MID(9)
+#undef NTT_MID
+                }
+                // ---- gather
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const uint32_t pos = pbase | ((uint32_t)c << B);
+                    if (first) v[c] = S[V == V_DIT ? brev(pos, L) : pos];
+                    else v[c] = W0[swz<T>(pos)];
+                }
+                if (first) {
+                    team_sync(bar_id, TT);      // staging consumed: prefetch the next row
+                    if (t == 0 && next < a.batch) {
+                        fence_proxy_async();
+                        mbar_expect_tx(&mbar[team], bytes);
+                        tma_load_1d(S, a.in + next * N, bytes, &mbar[team]);
+                    }
+                }
+                // ---- stages
+#define NTT_BW(BB, b0v, kgv)                                                                \
+    if (B == BB && kg == kgv) bitwin_regs<A, L, BB, b0v, kgv, V == V_DIF>(ar, v, pbase, stw);
+                if (V == V_DIT) {
+                    if (g == 0) {
+                        NTT_BW(0, 0, 1) NTT_BW(0, 0, 2) NTT_BW(0, 0, 3) NTT_BW(0, 0, 4)
+                    } else {
+                        NTT_BW(1, 1, 4) NTT_BW(2, 2, 4) NTT_BW(3, 3, 4) NTT_BW(4, 4, 4) NTT_BW(5, 5, 4)
+                        NTT_BW(6, 6, 4) NTT_BW(7, 7, 4) NTT_BW(8, 8, 4) NTT_BW(9, 9, 4)
+                    }
+                } else {
+                    if (g == G - 1) {
+                        NTT_BW(0, 0, 1) NTT_BW(0, 0, 2) NTT_BW(0, 0, 3) NTT_BW(0, 0, 4)
+                    } else {
+                        NTT_BW(1, 1, 4) NTT_BW(2, 2, 4) NTT_BW(3, 3, 4) NTT_BW(4, 4, 4) NTT_BW(5, 5, 4)
+                        NTT_BW(6, 6, 4) NTT_BW(7, 7, 4) NTT_BW(8, 8, 4) NTT_BW(9, 9, 4)
+                    }
+                }
+#undef NTT_BW
+                // ---- scatter
+                if (!last) {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) W0[swz<T>(pbase | ((uint32_t)c << B))] = v[c];
+                    team_sync(bar_id, TT);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const uint32_t pos = pbase | ((uint32_t)c << B);
+                        T r = ar.fin(v[c]);
+                        if (a.scale) r = ar.mulc(r, a.ninv);
+                        gout[V == V_DIF ? brev(pos, L) : pos] = r;
+                    }
+                }
+            }
+        } else {
+            // Pease / Pease_nc / Stockham: ping-pong W0 <-> W1 (Pease: + copy back)
+            T* src = W0;
+            T* dst = W1;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int sg = g == 0 ? 0 : K0 + 4 * (g - 1);
+                const int kg = g == 0 ? K0 : 4;
+                const bool first = g == 0, last = g == G - 1;
+                if (V != V_STOCKHAM) {
+                    // sub-networks: 16 contiguous positions (u << 4) | c
+                    const uint32_t u = first ? brev(t, L - 4) : t;
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const uint32_t pos = (u << 4) | c;
+                        v[c] = first ? S[brev(pos, L)] : src[swz<T>(pos)];
+                    }
+                    if (first) {
+                        team_sync(bar_id, TT);
+                        if (t == 0 && next < a.batch) {
+                            fence_proxy_async();
+                            mbar_expect_tx(&mbar[team], bytes);
+                            tma_load_1d(S, a.in + next * N, bytes, &mbar[team]);
+                        }
+                    }
+#define NTT_PE(SG, KGV) \
+    if (sg == SG && kg == KGV) pease_regs<A, L, SG, KGV>(ar, v, u, stw);
+                    if (g == 0) { NTT_PE(0, 1) NTT_PE(0, 2) NTT_PE(0, 3) NTT_PE(0, 4) }
+                    else { NTT_PE(1, 4) NTT_PE(2, 4) NTT_PE(3, 4) NTT_PE(4, 4) NTT_PE(5, 4) NTT_PE(6, 4)
+                           NTT_PE(7, 4) NTT_PE(8, 4) NTT_PE(9, 4) }
+#undef NTT_PE
+                    // outputs: network n = (u << (4-kg)) | n writes q | R << (L-kg)
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const uint32_t n = c >> kg, R = c & ((1u << kg) - 1);
+                        const uint32_t pos = (((u << (4 - kg)) | n)) | (R << (L - kg));
+                        if (last) {
+                            T r = ar.fin(v[c]);
+                            if (a.scale) r = ar.mulc(r, a.ninv);
+                            gout[pos] = r;
+                        } else dst[swz<T>(pos)] = v[c];
+                    }
+                } else {
+                    // Stockham: window [lob, lob+kg); first group: block [L-4, L)
+                    const int lob = L - sg - kg;
+                    uint32_t hi, lo;
+                    if (first) { hi = 0; lo = t; }
+                    else if (last) { hi = t; lo = 0; }
+                    else { lo = t & ((1u << lob) - 1); hi = t >> lob; }
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        // register c = (w << (4-kg)) | x; position = hi | w | x | lo
+                        const uint32_t pos = (hi << (L - sg)) | ((uint32_t)c << (lob - (4 - kg))) | lo;
+                        v[c] = first ? S[pos] : src[swz<T>(pos)];
+                    }
+                    if (first) {
+                        team_sync(bar_id, TT);
+                        if (t == 0 && next < a.batch) {
+                            fence_proxy_async();
+                            mbar_expect_tx(&mbar[team], bytes);
+                            tma_load_1d(S, a.in + next * N, bytes, &mbar[team]);
+                        }
+                    }
+#define NTT_ST(SG, KGV) \
+    if (sg == SG && kg == KGV) stockham_regs<A, L, SG, KGV>(ar, v, hi, stw);
+                    if (g == 0) { NTT_ST(0, 1) NTT_ST(0, 2) NTT_ST(0, 3) NTT_ST(0, 4) }
+                    else { NTT_ST(1, 4) NTT_ST(2, 4) NTT_ST(3, 4) NTT_ST(4, 4) NTT_ST(5, 4) NTT_ST(6, 4)
+                           NTT_ST(7, 4) NTT_ST(8, 4) NTT_ST(9, 4) }
+#undef NTT_ST
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        // output position = R << (L-kg) | hi << lob' | x | lo  with R = window bits
+                        const uint32_t R = (uint32_t)c >> (4 - kg), x = (uint32_t)c & ((1u << (4 - kg)) - 1);
+                        const uint32_t pos = (R << (L - kg)) | (hi << lob) | (x << (lob - (4 - kg))) | lo;
+                        if (last) {
+                            T r = ar.fin(v[c]);
+                            if (a.scale) r = ar.mulc(r, a.ninv);
+                            gout[pos] = r;
+                        } else dst[swz<T>(pos)] = v[c];
+                    }
+                }
+                if (!last) {
+                    team_sync(bar_id, TT);
+                    if (V == V_PEASE) {       // _stage_copy(cur, nxt)  (algorithms.py:242)
+                        for (int i = t; i < N; i += TT) src[i] = dst[i];
+                        ++copies;
+                        team_sync(bar_id, TT);
+                    } else {
+                        T* tmp = src; src = dst; dst = tmp;
+                    }
+                }
+            }
+        }
+        team_sync(bar_id, TT);    // work buffers free for the next row
+        if (a.counters && t == 0) {
+            atomicAdd(a.counters + C_TRANSFORMS, 1ull);
+            atomicAdd(a.counters + C_HBM, 1ull);
+            if (V != V_STOCKHAM) atomicAdd(a.counters + C_BITREV, 1ull);
+            if (V == V_PEASE) { atomicAdd(a.counters + C_COPIES, (unsigned long long)copies); copies = 0; }
+        }
+    }
+}
+
+// ------------------------------------------------------------- launcher --
+template <class A, int V, int L>
+struct FastCfg {
+    using T = typename A::T;
+    using Tw = typename A::Tw;
+    static constexpr int N = 1 << L;
+    static constexpr int TT = 1 << (L - 4);
+    static constexpr int NBUF = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM) ? 3 : 2;
+    static constexpr long kSmemCap = 227 * 1024 - 1024;
+    static constexpr long table = (long)N * sizeof(Tw);
+    static constexpr long team_bytes = (long)NBUF * N * sizeof(T);
+    static constexpr int by_smem = (int)((kSmemCap - table) / team_bytes);
+    static constexpr int by_thr = 1024 / TT;
+    static constexpr int t0 = by_smem < by_thr ? by_smem : by_thr;
+    static constexpr int TEAMS = t0 > 8 ? 8 : (t0 < 0 ? 0 : t0);
+    static constexpr long smem = table + (long)TEAMS * team_bytes;
+};
+
+template <class A, int V, int L>
+cudaError_t launch_fast_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int* launches, bool* ok) {
+    using C = FastCfg<A, V, L>;
+    if constexpr (C::TEAMS < 1) {
+        *ok = false;
+        return cudaSuccess;
+    } else {
+        auto kern = k_fast<A, V, L, C::TEAMS>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+        if (e != cudaSuccess) return e;
+        uint64_t ctas = (a.batch + C::TEAMS - 1) / C::TEAMS;
+        uint64_t grid = ctas < (uint64_t)num_sms ? ctas : (uint64_t)num_sms;
+        *ok = true;
+        if (grid == 0) return cudaSuccess;
+        kern<<<(unsigned)grid, C::TEAMS * C::TT, C::smem, s>>>(a);
+        if (launches) ++*launches;
+        return cudaGetLastError();
+    }
+}
+
+template <class A, int V>
+cudaError_t launch_fast(int L, const FastArgs<A>& a, cudaStream_t s, int num_sms, int* launches, bool* ok) {
+    *ok = false;
+    switch (L) {
+        case 9: return launch_fast_L<A, V, 9>(a, s, num_sms, launches, ok);
+        case 10: return launch_fast_L<A, V, 10>(a, s, num_sms, launches, ok);
+        case 11: return launch_fast_L<A, V, 11>(a, s, num_sms, launches, ok);
+        case 12: return launch_fast_L<A, V, 12>(a, s, num_sms, launches, ok);
+        case 13: return launch_fast_L<A, V, 13>(a, s, num_sms, launches, ok);
+        default: return cudaSuccess;
+    }
+}
+
+}  // namespace fastk
+}  // namespace nttb200

@@ -3,7 +3,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <type_traits>
 #include "multipass.cuh"
+#include "fast.cuh"
 
 namespace nttb200 {
 
@@ -73,6 +75,37 @@ __global__ void k_copy(const T* src, T* dst, uint64_t n, uint64_t rows, unsigned
     if (counters && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(counters + C_COPIES, (unsigned long long)rows);
 }
 
+template <class A, int V>
+cudaError_t run_fast_policy(const MultipassReq& r, bool* ok) {
+    fastk::FastArgs<A> a{};
+    a.in = static_cast<const typename A::T*>(r.in);
+    a.out = static_cast<typename A::T*>(r.out);
+    a.batch = r.batch;
+    a.stw = static_cast<const typename A::Tw*>(r.stw);
+    a.p = r.p;
+    a.scale = r.scale;
+    a.ninv = make_tw<typename A::Field>(r.ninv, r.ninv_shoup);
+    a.counters = r.counters;
+    return fastk::launch_fast<A, V>(r.L, a, r.stream, r.num_sms, r.launches, ok);
+}
+
+// Specialised single-pass kernels (fast.cuh) where they apply.
+template <class F, int V>
+cudaError_t try_fast(const MultipassReq& r, bool* ok) {
+    *ok = false;
+    if (V == V_FLAT || V == V_NAIVE || V == V_SIXSTEP) return cudaSuccess;
+    if (r.L < 9 || r.L > 13 || !r.stw) return cudaSuccess;
+    if ((reinterpret_cast<uintptr_t>(r.in) & 15) || (reinterpret_cast<uintptr_t>(r.out) & 15)) return cudaSuccess;
+    if constexpr (std::is_same<F, F32S>::value) {
+        if (r.p < (1ull << 30)) return run_fast_policy<LazyF32, V>(r, ok);
+        return run_fast_policy<Canon<F32S>, V>(r, ok);
+    } else if constexpr (std::is_same<F, FGold>::value) {
+        return run_fast_policy<Canon<FGold>, V>(r, ok);
+    } else {
+        return cudaSuccess;
+    }
+}
+
 template <class F, int V>
 cudaError_t run_variant(const MultipassReq& r) {
     using T = typename F::T;
@@ -80,6 +113,9 @@ cudaError_t run_variant(const MultipassReq& r) {
     const uint64_t N = 1ull << L;
     constexpr int elog = tile_elems_log2<T>();
     if (L <= single_pass_max_log2(sizeof(T))) {
+        bool ok = false;
+        cudaError_t fe = try_fast<F, V>(r, &ok);
+        if (fe != cudaSuccess || ok) return fe;
         // ---- one pass: TQ whole rows per tile, bit reversal fused into the groups
         PassArgs<F> a = base_args<F>(r);
         a.in = static_cast<const T*>(r.in);

@@ -1,0 +1,95 @@
+// lazy.cuh -- butterfly policies for the fast kernels.
+//
+// LazyF32 (p < 2^30): Harvey-style lazy Shoup butterflies.  DIT-type values
+// live in [0,4p) between stages and DIF-type values in [0,2p); one final
+// reduction makes them canonical, so the transform OUTPUT is bit-identical
+// to the reference (intermediate stage values are congruent mod p, not
+// canonical).  7 integer ops per DIT butterfly instead of 9.
+// Canon<F>: the canonical field ops of arith.cuh behind the same interface
+// (every stage canonical, exactly like the reference).
+#pragma once
+#include "arith.cuh"
+
+namespace nttb200 {
+
+struct LazyF32 {
+    using T = uint32_t;
+    using Tw = uint2;
+    using Field = F32S;
+    static constexpr bool lazy = true;
+    uint32_t p, p2;
+    NTT_D void init(uint64_t pp) { p = (uint32_t)pp; p2 = 2u * (uint32_t)pp; }
+    // DIT / Pease / Stockham butterfly: (x, y) -> (x + w*y, x - w*y); in/out [0,4p)
+    NTT_D void dit(T& x, T& y, Tw w) const {
+        const T xr = umin32(x, x - p2);
+        const T q = __umulhi(y, w.y);
+        const T t = y * w.x - q * p;          // [0,2p)
+        x = xr + t;
+        y = xr - t + p2;
+    }
+    // butterfly with twiddle 1: t = y mod 2p
+    NTT_D void dit1(T& x, T& y) const {
+        const T xr = umin32(x, x - p2);
+        const T t = umin32(y, y - p2);
+        x = xr + t;
+        y = xr - t + p2;
+    }
+    // DIF butterfly: (x, y) -> (x + y, w*(x - y)); in/out [0,2p)
+    NTT_D void dif(T& x, T& y, Tw w) const {
+        const T s = x + y;
+        const T d = x - y + p2;
+        x = umin32(s, s - p2);
+        const T q = __umulhi(d, w.y);
+        y = d * w.x - q * p;
+    }
+    NTT_D void dif1(T& x, T& y) const {
+        const T s = x + y;
+        const T d = x - y + p2;
+        x = umin32(s, s - p2);
+        y = umin32(d, d - p2);
+    }
+    NTT_D T fin(T x) const {
+        x = umin32(x, x - p2);
+        return umin32(x, x - p);
+    }
+    NTT_D T mulc(T x, Tw w) const {           // canonical x*w (x canonical)
+        const T q = __umulhi(x, w.y);
+        const T z = x * w.x - q * p;
+        return umin32(z, z - p);
+    }
+};
+
+template <class F>
+struct Canon {
+    using T = typename F::T;
+    using Tw = typename F::Tw;
+    using Field = F;
+    static constexpr bool lazy = false;
+    F f;
+    NTT_D void init(uint64_t pp) { f.p = (T)pp; }
+    NTT_D void dit(T& x, T& y, Tw w) const {
+        const T t = f.mul(y, w);
+        const T a = x;
+        x = f.add(a, t);
+        y = f.sub(a, t);
+    }
+    NTT_D void dit1(T& x, T& y) const {
+        const T a = x;
+        x = f.add(a, y);
+        y = f.sub(a, y);
+    }
+    NTT_D void dif(T& x, T& y, Tw w) const {
+        const T a = x, b = y;
+        x = f.add(a, b);
+        y = f.mul(f.sub(a, b), w);
+    }
+    NTT_D void dif1(T& x, T& y) const {
+        const T a = x, b = y;
+        x = f.add(a, b);
+        y = f.sub(a, b);
+    }
+    NTT_D T fin(T x) const { return x; }
+    NTT_D T mulc(T x, Tw w) const { return f.mul(x, w); }
+};
+
+}  // namespace nttb200

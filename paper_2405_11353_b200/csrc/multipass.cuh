@@ -248,6 +248,7 @@ struct MultipassReq {
     void* out;
     uint64_t batch;
     const void* tw;            // main table F::Tw[N]
+    const void* stw;           // per-stage table F::Tw[N]: T[2^(s-1)+k] = w^(k*N/2^s)
     const void* tw1;           // six-step size-n1 table
     const void* tw2;           // six-step size-n2 table
     const void* cor_lo;        // six-step two-level correction tables (F::T)

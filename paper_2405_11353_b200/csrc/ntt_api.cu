@@ -122,7 +122,8 @@ int field_kind(uint64_t p, int word_bytes) {
 // ---------------------------------------------------------------- tables --
 struct DevTable {
     int device = -1;
-    void* tw = nullptr;       // F::Tw[N]
+    void* tw = nullptr;       // F::Tw[N]: w^i (+ Shoup word)
+    void* stw = nullptr;      // F::Tw[N]: per-stage table T[2^(s-1)+k] = w^(k*N/2^s)
     uint64_t bytes = 0;
     uint64_t n_inv = 0, n_inv_dev_shoup = 0;
     ~DevTable() {
@@ -131,6 +132,7 @@ struct DevTable {
             cudaGetDevice(&cur);
             cudaSetDevice(device);
             cudaFree(tw);
+            if (stw) cudaFree(stw);
             cudaSetDevice(cur);
         }
     }
@@ -178,14 +180,28 @@ int get_dev_table(uint64_t p, uint64_t g, uint64_t n, int dir, int word, int dev
         t->n_inv = powmod(n % p, p - 2, p);
         t->n_inv_dev_shoup = shoup_word(t->n_inv, p, word == 4 ? 32 : 64);
     }
+    // per-stage reordering of the same entries: index i = 2^(s-1) + k holds
+    // w^(k * N/2^s), the twiddle of stage s for k < 2^(s-1)
+    const size_t esz = buf.size() / n;
+    std::vector<unsigned char> sbuf(buf.size());
+    memcpy(sbuf.data(), buf.data(), esz);
+    for (uint64_t i = 1; i < n; ++i) {
+        int s1 = 0;
+        while ((2ull << s1) <= i) ++s1;          // s - 1 = floor(log2 i)
+        const uint64_t k = i - (1ull << s1);
+        const uint64_t e = k * (n >> (s1 + 1));
+        memcpy(sbuf.data() + i * esz, buf.data() + e * esz, esz);
+    }
     int cur = 0;
     cudaGetDevice(&cur);
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaMalloc(&t->tw, buf.size());
     if (e == cudaSuccess) e = cudaMemcpy(t->tw, buf.data(), buf.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&t->stw, sbuf.size());
+    if (e == cudaSuccess) e = cudaMemcpy(t->stw, sbuf.data(), sbuf.size(), cudaMemcpyHostToDevice);
     cudaSetDevice(cur);
-    if (e != cudaSuccess) { t->tw = nullptr; return cuda_fail(e, "twiddle table upload"); }
-    t->bytes = buf.size();
+    if (e != cudaSuccess) { t->tw = nullptr; t->stw = nullptr; return cuda_fail(e, "twiddle table upload"); }
+    t->bytes = 2 * buf.size();
     g_tables[key] = t;
     out = t;
     return NTT_OK;
@@ -439,7 +455,7 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
     int launches = 0;
     MultipassReq r{};
     r.variant = plan->variant; r.L = plan->L; r.in = d_in; r.out = d_out; r.batch = batch;
-    r.tw = plan->table->tw; r.p = plan->p; r.scale = scale;
+    r.tw = plan->table->tw; r.stw = plan->table->stw; r.p = plan->p; r.scale = scale;
     r.ninv = plan->table->n_inv; r.ninv_shoup = plan->table->n_inv_dev_shoup;
     r.counters = ctr; r.stream = stream; r.num_sms = plan->num_sms; r.launches = &launches;
     r.ws = plan->ws;

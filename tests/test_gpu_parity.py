@@ -27,6 +27,7 @@ FIELDS = [
     ("default", 3221225473, 5, 32, np.uint32, 16),
     ("goldilocks", GOLD, 7, 64, np.uint64, 16),
     ("p998_u64", 998244353, 3, 64, np.uint64, 12),
+    ("babybear", 2013265921, 31, 32, np.uint32, 14),     # 2^30 < p < 2^31: canonical u32 path
     ("big64", 18446744069414584321, 7, 64, np.uint64, 6),   # placeholder, replaced below
 ]
 VARIANTS7 = ("dit", "dif", "flat", "pease", "pease_nc", "stockham", "sixstep")
@@ -86,10 +87,10 @@ def rand(p, B, L, dt, seed):
 
 
 @pytest.mark.parametrize("variant", VARIANTS7 + ("naive",))
-@pytest.mark.parametrize("fname", ["p998", "default", "goldilocks", "p998_u64", "generic64"])
+@pytest.mark.parametrize("fname", ["p998", "default", "goldilocks", "p998_u64", "generic64", "babybear"])
 def test_variant_vs_oracle_small(fields, fname, variant):
     _, p, g, w, dt, maxl = fields[fname]
-    for L in range(1, min(maxl, 10) + 1):
+    for L in range(1, min(maxl, 13) + 1):
         if variant == "naive" and L > 9:
             continue
         B = 3 if L > 6 else 17
@@ -100,10 +101,10 @@ def test_variant_vs_oracle_small(fields, fname, variant):
 
 
 @pytest.mark.parametrize("variant", VARIANTS7)
-@pytest.mark.parametrize("fname", ["p998", "default", "goldilocks"])
+@pytest.mark.parametrize("fname", ["p998", "default", "goldilocks", "babybear"])
 def test_variant_inverse_and_intt(fields, fname, variant):
     _, p, g, w, dt, maxl = fields[fname]
-    for L in (1, 5, 11, 13):
+    for L in (1, 5, 9, 10, 11, 12, 13):
         x = rand(p, 4, L, dt, 2000 + L)
         want_u = O.ntt(x, p, g, w, variant, inverse=True)
         want_s = O.ntt(x, p, g, w, variant, inverse=True, scale=True)
