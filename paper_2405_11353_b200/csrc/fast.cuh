@@ -58,6 +58,20 @@ NTT_D void team_sync(int id, int nthreads) {
 template <class T>
 NTT_HD constexpr int lane_bits() { return sizeof(T) == 4 ? 5 : 4; }
 
+// Additive padded layout of the exchange buffers: one pad slot per 2^CW
+// (and per 2^(2CW), ...) slots, so bit b of a position moves the bank by
+// 2^(b mod CW) -- the same conflict-freedom as an XOR fold, but ADDITIVE for
+// positions split into disjoint thread / register bits: address =
+// padpos(thread part) + padpos(register part) with the second term a
+// compile-time immediate offset.
+template <class T>
+NTT_HD constexpr uint32_t padpos(uint32_t pos) {
+    return sizeof(T) == 4 ? pos + (pos >> 5) + (pos >> 10)
+                          : pos + (pos >> 4) + (pos >> 8) + (pos >> 12);
+}
+template <class T, int L>
+NTT_HD constexpr int padded_len() { return ((int)padpos<T>((1u << L) - 1) + 1 + 3) & ~3; }
+
 // Bit permutation of a thread id onto the free position bits of a group
 // (everything outside the 4-bit register block [B, B+4)).  The first
 // lane_bits() thread bits go to free bits with pairwise distinct residues
@@ -223,9 +237,10 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
     Tw* stw = reinterpret_cast<Tw*>(smem_raw);
     const int team = threadIdx.x / TT;
     const uint32_t t = threadIdx.x % TT;
-    T* S = reinterpret_cast<T*>(smem_raw + (size_t)N * sizeof(Tw)) + (size_t)team * NBUF * N;
+    constexpr int NP = padded_len<T, L>();
+    T* S = reinterpret_cast<T*>(smem_raw + (size_t)N * sizeof(Tw)) + (size_t)team * (N + (NBUF - 1) * NP);
     T* W0 = S + N;
-    T* W1 = PP ? S + 2 * N : W0;
+    T* W1 = PP ? W0 + NP : W0;
     A ar;
     ar.init(a.p);
 
@@ -276,11 +291,12 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
 #undef NTT_MID
                 }
                 // ---- gather
+                T* wb = W0 + padpos<T>(pbase);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
                     const uint32_t pos = pbase | ((uint32_t)c << B);
                     if (first) v[c] = S[V == V_DIT ? brev(pos, L) : pos];
-                    else v[c] = W0[swz<T>(pos)];
+                    else v[c] = wb[padpos<T>((uint32_t)c << B)];
                 }
                 if (first) {
                     team_sync(bar_id, TT);      // staging consumed: prefetch the next row
@@ -312,7 +328,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                 // ---- scatter
                 if (!last) {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) W0[swz<T>(pbase | ((uint32_t)c << B))] = v[c];
+                    for (int c = 0; c < 16; ++c) wb[padpos<T>((uint32_t)c << B)] = v[c];
                     team_sync(bar_id, TT);
                 } else {
 #pragma unroll
@@ -336,10 +352,11 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                 if (V != V_STOCKHAM) {
                     // sub-networks: 16 contiguous positions (u << 4) | c
                     const uint32_t u = first ? brev(t, L - 4) : t;
+                    const T* sb = src + padpos<T>(u << 4);
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
                         const uint32_t pos = (u << 4) | c;
-                        v[c] = first ? S[brev(pos, L)] : src[swz<T>(pos)];
+                        v[c] = first ? S[brev(pos, L)] : sb[padpos<T>((uint32_t)c)];
                     }
                     if (first) {
                         team_sync(bar_id, TT);
@@ -356,6 +373,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                            NTT_PE(7, 4) NTT_PE(8, 4) NTT_PE(9, 4) }
 #undef NTT_PE
                     // outputs: network n = (u << (4-kg)) | n writes q | R << (L-kg)
+                    T* db = dst + padpos<T>(u << (4 - kg));
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
                         const uint32_t n = c >> kg, R = c & ((1u << kg) - 1);
@@ -364,7 +382,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                             T r = ar.fin(v[c]);
                             if (a.scale) r = ar.mulc(r, a.ninv);
                             gout[pos] = r;
-                        } else dst[swz<T>(pos)] = v[c];
+                        } else db[padpos<T>(n | (R << (L - kg)))] = v[c];
                     }
                 } else {
                     // Stockham: window [lob, lob+kg); first group: block [L-4, L)
@@ -373,11 +391,12 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                     if (first) { hi = 0; lo = t; }
                     else if (last) { hi = t; lo = 0; }
                     else { lo = t & ((1u << lob) - 1); hi = t >> lob; }
+                    const T* sb = src + padpos<T>((hi << (L - sg)) | lo);
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
                         // register c = (w << (4-kg)) | x; position = hi | w | x | lo
                         const uint32_t pos = (hi << (L - sg)) | ((uint32_t)c << (lob - (4 - kg))) | lo;
-                        v[c] = first ? S[pos] : src[swz<T>(pos)];
+                        v[c] = first ? S[pos] : sb[padpos<T>((uint32_t)c << (lob - (4 - kg)))];
                     }
                     if (first) {
                         team_sync(bar_id, TT);
@@ -393,22 +412,23 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                     else { NTT_ST(1, 4) NTT_ST(2, 4) NTT_ST(3, 4) NTT_ST(4, 4) NTT_ST(5, 4) NTT_ST(6, 4)
                            NTT_ST(7, 4) NTT_ST(8, 4) NTT_ST(9, 4) }
 #undef NTT_ST
+                    T* db = dst + padpos<T>((hi << lob) | lo);
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
-                        // output position = R << (L-kg) | hi << lob' | x | lo  with R = window bits
+                        // output position = R << (L-kg) | hi << lob | x | lo  with R = window bits
                         const uint32_t R = (uint32_t)c >> (4 - kg), x = (uint32_t)c & ((1u << (4 - kg)) - 1);
                         const uint32_t pos = (R << (L - kg)) | (hi << lob) | (x << (lob - (4 - kg))) | lo;
                         if (last) {
                             T r = ar.fin(v[c]);
                             if (a.scale) r = ar.mulc(r, a.ninv);
                             gout[pos] = r;
-                        } else dst[swz<T>(pos)] = v[c];
+                        } else db[padpos<T>((R << (L - kg)) | (x << (lob - (4 - kg))))] = v[c];
                     }
                 }
                 if (!last) {
                     team_sync(bar_id, TT);
                     if (V == V_PEASE) {       // _stage_copy(cur, nxt)  (algorithms.py:242)
-                        for (int i = t; i < N; i += TT) src[i] = dst[i];
+                        for (int i = t; i < NP; i += TT) src[i] = dst[i];
                         ++copies;
                         team_sync(bar_id, TT);
                     } else {
@@ -428,6 +448,11 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
 }
 
 // ------------------------------------------------------------- launcher --
+#ifndef NTT_FAST_MAX_THREADS
+#define NTT_FAST_MAX_THREADS 768
+#endif
+constexpr int kFastMaxThreads = NTT_FAST_MAX_THREADS;
+
 template <class A, int V, int L>
 struct FastCfg {
     using T = typename A::T;
@@ -437,9 +462,9 @@ struct FastCfg {
     static constexpr int NBUF = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM) ? 3 : 2;
     static constexpr long kSmemCap = 227 * 1024 - 1024;
     static constexpr long table = (long)N * sizeof(Tw);
-    static constexpr long team_bytes = (long)NBUF * N * sizeof(T);
+    static constexpr long team_bytes = ((long)N + (long)(NBUF - 1) * padded_len<T, L>()) * sizeof(T);
     static constexpr int by_smem = (int)((kSmemCap - table) / team_bytes);
-    static constexpr int by_thr = 1024 / TT;
+    static constexpr int by_thr = kFastMaxThreads / TT;
     static constexpr int t0 = by_smem < by_thr ? by_smem : by_thr;
     static constexpr int TEAMS = t0 > 8 ? 8 : (t0 < 0 ? 0 : t0);
     static constexpr long smem = table + (long)TEAMS * team_bytes;

@@ -1,0 +1,491 @@
+// fasttile.cuh -- compile-time specialised HBM pass kernel for large N.
+//
+// One pass = K consecutive stages of the variant (index algebra in
+// docs/PASS_ALGEBRA.md).  A CTA owns a TILE of TQ networks (2^K residues
+// each) in a padded shared-memory layout:
+//   1. coalesced 16-byte-vector gather of the tile from HBM (bit reversal of
+//      the first DIT / Pease pass fused into the gather addresses),
+//   2. ceil(K/4) register groups (16 residues per thread, <= 4 stages each,
+//      conflict-free lane maps), twiddles from the per-stage table
+//      T[2^(s-1)+k]: the first 2^SMB entries staged in shared memory once per
+//      CTA, later stages read through the read-only path (L2-resident table),
+//      one 8-byte load per DISTINCT twiddle of a thread's group,
+//   3. coalesced 16-byte-vector scatter (final reduction, n_inv scaling,
+//      six-step correction twiddles fused).
+// Tiles are persistent over the grid.  Stage-faithful: the HBM buffer after a
+// pass holds the reference's state after the same stage (congruent; exact
+// when the policy is canonical).
+#pragma once
+#include <cstdint>
+#include "fast.cuh"
+
+namespace nttb200 {
+namespace ftile {
+
+using fastk::padded_len;
+using fastk::padpos;
+using fastk::Perm;
+using fastk::plan_lanes;
+using fastk::scatter_bits;
+
+enum TileLayout { TL_VARIANT = 0, TL_SIX_A = 1, TL_SIX_B = 2 };
+enum TileQ { TQM_LINEAR = 1, TQM_REV = 2, TQM_2D = 3 };
+enum TileOrder { TO_C_FAST = 0, TO_T_FAST = 1, TO_TB_FAST = 2 };
+
+template <class A>
+struct TileArgs {
+    using T = typename A::T;
+    using Tw = typename A::Tw;
+    const T* in;
+    T* out;
+    uint64_t batch;
+    int L, S0;
+    int qmode, TA, la;         // TQM_2D: TQ = TA x TB, la = log2 TA
+    int in_order, out_order;
+    int vec_in, vec_out;       // 16-byte vector copies valid for this pass
+    int rev_in, rev_out;
+    int rev_local;             // six-step: bit-reverse the K local bits on the gather (sub-DIT input)
+    int count_row, count_bitrev;
+    const Tw* gstw;            // global per-stage table of the (sub-)transform
+    int smb;                   // entries [0, 2^smb) are staged in shared memory
+    uint64_t p;
+    int scale;
+    Tw ninv;
+    int l1, l2;                // six-step split
+    const T* cor_lo;
+    const T* cor_hi;
+    int cor_lb;
+    unsigned long long* counters;
+};
+
+template <class A, int V, int K, int LAY>
+NTT_D uint64_t t_gpos_in(const TileArgs<A>& a, uint32_t Q, uint32_t x) {
+    if (LAY == TL_SIX_A) return ((uint64_t)x << a.l1) | Q;
+    if (LAY == TL_SIX_B) return ((uint64_t)x << a.l2) | Q;
+    const int L = a.L, S0 = a.S0;
+    uint64_t g;
+    if (V == V_PEASE || V == V_PEASE_NC) g = ((uint64_t)Q << K) | x;
+    else if (V == V_STOCKHAM) {
+        const int glob = L - S0 - K;
+        g = ((uint64_t)(Q >> glob) << (L - S0)) | ((uint64_t)x << glob) | (Q & ((1u << glob) - 1));
+    } else g = (Q & ((1u << S0) - 1)) | ((uint64_t)x << S0) | ((uint64_t)(Q >> S0) << (S0 + K));
+    return a.rev_in ? (uint64_t)brev((uint32_t)g, L) : g;
+}
+
+template <class A, int V, int K, int LAY>
+NTT_D uint64_t t_gpos_out(const TileArgs<A>& a, uint32_t Q, uint32_t x) {
+    if (LAY == TL_SIX_A) return ((uint64_t)Q << a.l2) | x;
+    if (LAY == TL_SIX_B) return ((uint64_t)x << a.l2) | Q;
+    const int L = a.L, S0 = a.S0;
+    uint64_t g;
+    if (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM) g = Q | ((uint64_t)x << (L - K));
+    else g = (Q & ((1u << S0) - 1)) | ((uint64_t)x << S0) | ((uint64_t)(Q >> S0) << (S0 + K));
+    return a.rev_out ? (uint64_t)brev((uint32_t)g, L) : g;
+}
+
+// twiddle T[idx]: the group decides (uniformly) whether all its stages are
+// covered by the shared-memory copy or must use the read-only path, so the
+// loads are unconditional and the compiler can hoist them.
+template <class Tw>
+struct TwSrc {
+    const Tw* p;
+    bool global;
+};
+// explicit shared-space loads (a generic pointer would compile to LD, not LDS)
+NTT_D uint2 lds_tw(const uint2* p) {
+    uint2 r;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(fastk::smem_u32(p)));
+    return r;
+}
+NTT_D uint64_t lds_tw(const uint64_t* p) {
+    uint64_t r;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(r) : "r"(fastk::smem_u32(p)));
+    return r;
+}
+NTT_D ulonglong2 lds_tw(const ulonglong2* p) {
+    ulonglong2 r;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "r"(fastk::smem_u32(p)));
+    return r;
+}
+template <bool GL, class Tw>
+NTT_D Tw twld(const Tw* p, uint32_t idx) {
+    if (GL) return __ldg(p + idx);
+    return lds_tw(p + idx);
+}
+
+// ---------------------------------------------------------------- DIT/DIF --
+template <class A, int K, int B, int b0, int kg, bool DIF, bool GL>
+NTT_D void t_bitwin(const A& ar, typename A::T (&v)[16], uint32_t pbase, uint32_t qlow, int S0,
+                    const typename A::Tw* tw) {
+    constexpr int off = b0 - B;
+#pragma unroll
+    for (int jj = 0; jj < kg; ++jj) {
+        const int j = DIF ? kg - 1 - jj : jj;
+        const int sl = b0 + j;                         // local bit = local stage - 1
+        const int s = S0 + sl + 1;                     // global stage
+        const bool triv = (sl == 0) && (S0 == 0);      // s == 1: every twiddle is w^0
+        const uint32_t lmask = (1u << sl) - 1;
+        const uint32_t kthr = qlow | ((pbase & lmask) << S0);
+        const uint32_t rowi = (1u << (s - 1)) + kthr;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            if (c & (1 << (off + j))) continue;
+            const uint32_t kc = ((uint32_t)c << B) & lmask;
+            const int hi = c | (1 << (off + j));
+            if (triv) {
+                if (DIF) ar.dif1(v[c], v[hi]); else ar.dit1(v[c], v[hi]);
+            } else {
+                const typename A::Tw w = twld<GL>(tw, rowi + (kc << S0));
+                if (DIF) ar.dif(v[c], v[hi], w); else ar.dit(v[c], v[hi], w);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ Pease --
+template <class A, int K, int sg, int kg, bool GL>
+NTT_D void t_pease(const A& ar, typename A::T (&v)[16], uint32_t u, uint32_t qtop, int S0,
+                   const typename A::Tw* tw) {
+    using T = typename A::T;
+    constexpr int NB = 16 >> kg;
+    constexpr int H = 1 << (kg - 1);
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+        const uint32_t q = (u << (4 - kg)) | n;                   // local network id (K-kg bits)
+        const uint32_t bprev = sg ? (q >> (K - kg - sg)) : 0u;     // output bits of earlier groups
+#pragma unroll
+        for (int m = 0; m < kg; ++m) {
+            const int s = S0 + sg + m + 1;
+            const bool triv = (sg + m == 0) && (S0 == 0);
+            const uint32_t rowi = (1u << (s - 1)) + ((bprev << S0) | qtop);
+            T nv[1 << kg];
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const uint32_t Bg = (2u * i) >> (kg - m);
+                T x = v[n * (1 << kg) + 2 * i], y = v[n * (1 << kg) + 2 * i + 1];
+                if (triv) ar.dit1(x, y);
+                else ar.dit(x, y, twld<GL>(tw, rowi + (Bg << (sg + S0))));
+                nv[i] = x;
+                nv[i + H] = y;
+            }
+#pragma unroll
+            for (int c = 0; c < (1 << kg); ++c) v[n * (1 << kg) + c] = nv[c];
+        }
+    }
+}
+
+// --------------------------------------------------------------- Stockham --
+template <class A, int K, int sg, int kg, bool GL>
+NTT_D void t_stockham(const A& ar, typename A::T (&v)[16], uint32_t hi, uint32_t ghi, int S0,
+                      const typename A::Tw* tw) {
+    using T = typename A::T;
+    constexpr int NB = 16 >> kg;
+    constexpr int H = 1 << (kg - 1);
+#pragma unroll
+    for (int x = 0; x < NB; ++x) {
+#pragma unroll
+        for (int m = 0; m < kg; ++m) {
+            const int s = S0 + sg + m;     // 0-based
+            const bool triv = (sg + m == 0) && (S0 == 0);
+            const uint32_t rowi = (1u << s) + ((hi << S0) | ghi);
+            T nv[1 << kg];
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const uint32_t Bv = i & ((1u << m) - 1), crest = (uint32_t)i >> m;
+                T a = v[(i << (4 - kg)) | x], b = v[((i + H) << (4 - kg)) | x];
+                if (triv) ar.dit1(a, b);
+                else ar.dit(a, b, twld<GL>(tw, rowi + (Bv << (sg + S0))));
+                nv[(crest << (m + 1)) | Bv] = a;
+                nv[(crest << (m + 1)) | (1u << m) | Bv] = b;
+            }
+#pragma unroll
+            for (int c = 0; c < (1 << kg); ++c) v[(c << (4 - kg)) | x] = nv[c];
+        }
+    }
+}
+
+// Network stride in shared memory: the padded length, skewed so that the
+// TQ networks of a tile land in different banks for t-fast copies
+// (stride = max(1, 32/TQ) mod 32 for u32; max(1, 16/TQ) mod 16 for u64).
+template <class T, int K, int TQ>
+NTT_HD constexpr int tile_stride() {
+    constexpr int NB = sizeof(T) == 4 ? 32 : 16;
+    constexpr int want = TQ >= NB ? 1 : NB / TQ;
+    int n = padded_len<T, K>();
+    while (n % NB != want) ++n;
+    return n;
+}
+
+template <int K, int TQ>
+struct TileGeo {
+    static constexpr int TT = 1 << (K - 4);       // threads per network
+    static constexpr int G = (K + 3) / 4;
+    static constexpr int K0 = K - 4 * (G - 1);
+};
+
+// ----------------------------------------------------------------- kernel --
+template <class A, int V, int K, int TQ, int NT, int LAY, int SMB>
+__global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 2))) k_tile(TileArgs<A> a) {
+    using T = typename A::T;
+    using Tw = typename A::Tw;
+    using GG = TileGeo<K, TQ>;
+    constexpr int TT = GG::TT, G = GG::G, K0 = GG::K0;
+    constexpr int CW = fastk::lane_bits<T>();
+    constexpr int NP = tile_stride<T, K, TQ>();
+    constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);
+    constexpr int REP = (TQ * TT) / NT;             // sub-networks per thread per group
+    constexpr int VE = 16 / sizeof(T);              // residues per 16-byte vector
+    static_assert(REP >= 1 && REP * NT == TQ * TT, "thread count must divide the tile");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ uint32_t Qs[TQ];
+    __shared__ uint64_t Rb[TQ];
+    Tw* tws = reinterpret_cast<Tw*>(smem_raw);
+    T* bufA = reinterpret_cast<T*>(smem_raw + ((size_t)sizeof(Tw) << SMB));
+    T* bufB = PP ? bufA + TQ * NP : bufA;
+    A ar;
+    ar.init(a.p);
+    const int L = a.L, S0 = a.S0;
+    const int M = (LAY == TL_VARIANT) ? L - K : (LAY == TL_SIX_A ? a.l1 : a.l2);
+    const uint64_t N = 1ull << L;
+    constexpr int LTQ = TQ == 1 ? 0 : (TQ == 2 ? 1 : (TQ == 4 ? 2 : (TQ == 8 ? 3 : (TQ == 16 ? 4 : (TQ == 32 ? 5 : 6)))));
+    const int ltpr = M - LTQ;                          // log2 tiles per row
+    const uint64_t tiles_per_row = 1ull << ltpr;
+    const uint64_t ntiles = a.batch << ltpr;
+    const int smb = a.smb < SMB ? a.smb : SMB;
+    const uint32_t smlim = 1u << smb;
+    for (uint32_t i = threadIdx.x; i < smlim; i += NT) tws[i] = a.gstw[i];
+    // twiddle source per register group: smem when every stage of the group is < 2^smb
+    auto twsrc = [&](int last_stage) -> TwSrc<Tw> {
+        return last_stage <= smb ? TwSrc<Tw>{tws, false} : TwSrc<Tw>{a.gstw, true};
+    };
+    const int Lt = (LAY == TL_VARIANT) ? L : K;      // twiddle frame (six-step: sub-transform)
+    const int S0t = (LAY == TL_VARIANT) ? S0 : 0;
+    (void)Lt;
+
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();
+        if (threadIdx.x < TQ) {
+            const int t = threadIdx.x;
+            const uint64_t row = tile >> ltpr;
+            const uint32_t tr = (uint32_t)(tile & (tiles_per_row - 1));
+            uint32_t Q;
+            if (a.qmode == TQM_LINEAR) Q = tr * TQ + t;
+            else if (a.qmode == TQM_REV) Q = brev(tr * TQ + t, M);
+            else {
+                const int hb = LTQ - a.la;
+                Q = (brev(tr * a.TA + (t & (a.TA - 1)), M - hb) << hb) | (t >> a.la);
+            }
+            Qs[t] = Q;
+            Rb[t] = row * N;
+        }
+        __syncthreads();
+        // ---- gather (16-byte vectors along the contiguous run when valid)
+        if (a.vec_in && a.in_order == TO_T_FAST) {
+#pragma unroll 4
+            for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
+                const uint32_t t0 = (i % (TQ / VE)) * VE, x = i / (TQ / VE);
+                const T* src = a.in + Rb[t0] + t_gpos_in<A, V, K, LAY>(a, Qs[t0], x);
+                T tmp[VE];
+                *reinterpret_cast<uint4*>(tmp) = __ldg(reinterpret_cast<const uint4*>(src));
+#pragma unroll
+                for (int e = 0; e < VE; ++e) bufA[(t0 + e) * NP + padpos<T>(a.rev_local ? brev(x, K) : x)] = tmp[e];
+            }
+        } else if (a.vec_in && a.in_order == TO_C_FAST) {
+#pragma unroll 4
+            for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
+                const uint32_t t = i / ((1u << K) / VE), x0 = (i % ((1u << K) / VE)) * VE;
+                const T* src = a.in + Rb[t] + t_gpos_in<A, V, K, LAY>(a, Qs[t], x0);
+                T tmp[VE];
+                *reinterpret_cast<uint4*>(tmp) = __ldg(reinterpret_cast<const uint4*>(src));
+#pragma unroll
+                for (int e = 0; e < VE; ++e)
+                    bufA[t * NP + padpos<T>(a.rev_local ? brev(x0 + e, K) : x0 + e)] = tmp[e];
+            }
+        } else {
+#pragma unroll 4
+            for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K); i += NT) {
+                uint32_t t, x;
+                if (a.in_order == TO_C_FAST) { t = i >> K; x = i & ((1u << K) - 1); }
+                else if (a.in_order == TO_T_FAST) { t = i % TQ; x = i / TQ; }
+                else { const int lb = LTQ - a.la; const uint32_t tb = i & ((1u << lb) - 1), ta = (i >> lb) & (a.TA - 1); t = ta + (tb << a.la); x = i / TQ; }
+                bufA[t * NP + padpos<T>(a.rev_local ? brev(x, K) : x)] =
+                    __ldg(a.in + Rb[t] + t_gpos_in<A, V, K, LAY>(a, Qs[t], x));
+            }
+        }
+        __syncthreads();
+
+        // ---- register groups
+        T* src = bufA;
+        T* dst = bufB;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            T v[16];
+#pragma unroll
+            for (int r = 0; r < REP; ++r) {
+                const uint32_t tid = threadIdx.x + r * NT;
+                const uint32_t t = tid / TT, u = tid % TT;
+                const uint32_t Q = (LAY == TL_VARIANT) ? Qs[t] : 0u;
+                T* sb = src + t * NP;
+                T* db = dst + t * NP;
+                if (V == V_DIT || V == V_DIF) {
+                    const int B = (V == V_DIT) ? (g == 0 ? 0 : K0 + 4 * (g - 1)) : (g == G - 1 ? 0 : K - 4 * (g + 1));
+                    const int kg = (V == V_DIT) ? (g == 0 ? K0 : 4) : (g == G - 1 ? K0 : 4);
+                    uint32_t pbase = 0;
+#define NTT_TMAP(BB)                                                   \
+    if (B == BB) {                                                     \
+        constexpr Perm PM = plan_lanes(K, BB, CW);                     \
+        pbase = scatter_bits<K - 4>(u, PM);                            \
+    }
+                    NTT_TMAP(0) NTT_TMAP(1) NTT_TMAP(2) NTT_TMAP(3) NTT_TMAP(4) NTT_TMAP(5) NTT_TMAP(6)
+                    NTT_TMAP(7) NTT_TMAP(8) NTT_TMAP(9)
+#undef NTT_TMAP
+                    const uint32_t qlow = (LAY == TL_VARIANT) ? (Q & ((1u << S0t) - 1)) : 0u;
+                    const int b0g = (V == V_DIT) ? (g == 0 ? 0 : B) : (g == G - 1 ? 0 : B);
+                    const TwSrc<Tw> tw = twsrc(S0t + b0g + kg);
+                    T* wb = sb + padpos<T>(pbase);
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) v[c] = wb[padpos<T>((uint32_t)c << B)];
+#define NTT_TBW(BB, b0v, kgv)                                                                        \
+    if (B == BB && kg == kgv) {                                                                        \
+        if (tw.global) t_bitwin<A, K, BB, b0v, kgv, V == V_DIF, true>(ar, v, pbase, qlow, S0t, tw.p);  \
+        else t_bitwin<A, K, BB, b0v, kgv, V == V_DIF, false>(ar, v, pbase, qlow, S0t, tw.p);           \
+    }
+                    if ((V == V_DIT && g == 0) || (V == V_DIF && g == G - 1)) {
+                        NTT_TBW(0, 0, 1) NTT_TBW(0, 0, 2) NTT_TBW(0, 0, 3) NTT_TBW(0, 0, 4)
+                    } else {
+                        NTT_TBW(1, 1, 4) NTT_TBW(2, 2, 4) NTT_TBW(3, 3, 4) NTT_TBW(4, 4, 4) NTT_TBW(5, 5, 4)
+                        NTT_TBW(6, 6, 4) NTT_TBW(7, 7, 4) NTT_TBW(8, 8, 4) NTT_TBW(9, 9, 4)
+                    }
+#undef NTT_TBW
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) wb[padpos<T>((uint32_t)c << B)] = v[c];
+                } else if (V != V_STOCKHAM) {
+                    const int sg = g == 0 ? 0 : K0 + 4 * (g - 1);
+                    const int kg = g == 0 ? K0 : 4;
+                    const uint32_t qtop = S0t ? (Q >> (L - K - S0t)) : 0u;
+                    const TwSrc<Tw> tw = twsrc(S0t + sg + kg);
+                    const T* rb = sb + padpos<T>(u << 4);
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) v[c] = rb[padpos<T>((uint32_t)c)];
+#define NTT_TPE(SG, KGV) \
+    if (sg == SG && kg == KGV) {                                                 \
+        if (tw.global) t_pease<A, K, SG, KGV, true>(ar, v, u, qtop, S0t, tw.p);    \
+        else t_pease<A, K, SG, KGV, false>(ar, v, u, qtop, S0t, tw.p);             \
+    }
+                    if (g == 0) { NTT_TPE(0, 1) NTT_TPE(0, 2) NTT_TPE(0, 3) NTT_TPE(0, 4) }
+                    else { NTT_TPE(1, 4) NTT_TPE(2, 4) NTT_TPE(3, 4) NTT_TPE(4, 4) NTT_TPE(5, 4) NTT_TPE(6, 4)
+                           NTT_TPE(7, 4) NTT_TPE(8, 4) NTT_TPE(9, 4) }
+#undef NTT_TPE
+                    T* wbo = db + padpos<T>(u << (4 - kg));
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const uint32_t n = c >> kg, R = c & ((1u << kg) - 1);
+                        wbo[padpos<T>(n | (R << (K - kg)))] = v[c];
+                    }
+                } else {
+                    const int sg = g == 0 ? 0 : K0 + 4 * (g - 1);
+                    const int kg = g == 0 ? K0 : 4;
+                    const int lob = K - sg - kg;
+                    const int glob = L - S0t - K;
+                    const uint32_t ghi = (LAY == TL_VARIANT && S0t) ? (Q >> glob) : 0u;
+                    const TwSrc<Tw> tw = twsrc(S0t + sg + kg);
+                    uint32_t hi, lo;
+                    if (g == 0) { hi = 0; lo = u; }
+                    else if (g == G - 1) { hi = u; lo = 0; }
+                    else { lo = u & ((1u << lob) - 1); hi = u >> lob; }
+                    const T* rb = sb + padpos<T>((hi << (K - sg)) | lo);
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) v[c] = rb[padpos<T>((uint32_t)c << (lob - (4 - kg)))];
+#define NTT_TST(SG, KGV) \
+    if (sg == SG && kg == KGV) {                                                  \
+        if (tw.global) t_stockham<A, K, SG, KGV, true>(ar, v, hi, ghi, S0t, tw.p);  \
+        else t_stockham<A, K, SG, KGV, false>(ar, v, hi, ghi, S0t, tw.p);           \
+    }
+                    if (g == 0) { NTT_TST(0, 1) NTT_TST(0, 2) NTT_TST(0, 3) NTT_TST(0, 4) }
+                    else { NTT_TST(1, 4) NTT_TST(2, 4) NTT_TST(3, 4) NTT_TST(4, 4) NTT_TST(5, 4) NTT_TST(6, 4)
+                           NTT_TST(7, 4) NTT_TST(8, 4) NTT_TST(9, 4) }
+#undef NTT_TST
+                    T* wbo = db + padpos<T>((hi << lob) | lo);
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const uint32_t R = (uint32_t)c >> (4 - kg), x = (uint32_t)c & ((1u << (4 - kg)) - 1);
+                        wbo[padpos<T>((R << (K - kg)) | (x << (lob - (4 - kg))))] = v[c];
+                    }
+                }
+            }
+            __syncthreads();
+            if (PP) { T* tmp = src; src = dst; dst = tmp; }
+        }
+        const T* res = src;   // DIT/DIF: in place (bufA); ping-pong: last written buffer
+
+        // ---- scatter (final reduction, n_inv, six-step correction twiddles)
+        auto finish = [&](uint32_t t, uint32_t x, T v) -> T {
+            T r = ar.fin(v);
+            if (LAY == TL_SIX_A) {
+                const uint64_t e = ((uint64_t)Qs[t] * x) & (N - 1);
+                const T w = ar.mulfull(__ldg(a.cor_hi + (e >> a.cor_lb)), __ldg(a.cor_lo + (e & ((1ull << a.cor_lb) - 1))));
+                r = ar.mulfull(r, w);
+            }
+            if (a.scale) r = ar.mulc(r, a.ninv);
+            return r;
+        };
+        if (a.vec_out && a.out_order == TO_T_FAST) {
+            for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
+                const uint32_t t0 = (i % (TQ / VE)) * VE, x = i / (TQ / VE);
+                T tmp[VE];
+#pragma unroll
+                for (int e = 0; e < VE; ++e) tmp[e] = finish(t0 + e, x, res[(t0 + e) * NP + padpos<T>(x)]);
+                *reinterpret_cast<uint4*>(a.out + Rb[t0] + t_gpos_out<A, V, K, LAY>(a, Qs[t0], x)) =
+                    *reinterpret_cast<uint4*>(tmp);
+            }
+        } else if (a.vec_out && a.out_order == TO_C_FAST) {
+            for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
+                const uint32_t t = i / ((1u << K) / VE), x0 = (i % ((1u << K) / VE)) * VE;
+                T tmp[VE];
+#pragma unroll
+                for (int e = 0; e < VE; ++e) tmp[e] = finish(t, x0 + e, res[t * NP + padpos<T>(x0 + e)]);
+                *reinterpret_cast<uint4*>(a.out + Rb[t] + t_gpos_out<A, V, K, LAY>(a, Qs[t], x0)) =
+                    *reinterpret_cast<uint4*>(tmp);
+            }
+        } else {
+            for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K); i += NT) {
+                uint32_t t, x;
+                if (a.out_order == TO_C_FAST) { t = i >> K; x = i & ((1u << K) - 1); }
+                else if (a.out_order == TO_T_FAST) { t = i % TQ; x = i / TQ; }
+                else { const int lb = LTQ - a.la; const uint32_t tb = i & ((1u << lb) - 1), ta = (i >> lb) & (a.TA - 1); t = ta + (tb << a.la); x = i / TQ; }
+                a.out[Rb[t] + t_gpos_out<A, V, K, LAY>(a, Qs[t], x)] = finish(t, x, res[t * NP + padpos<T>(x)]);
+            }
+        }
+        if (a.counters && threadIdx.x == 0 && tile % tiles_per_row == 0) {
+            atomicAdd(a.counters + C_HBM, 1ull);
+            if (a.count_row) atomicAdd(a.counters + C_TRANSFORMS, 1ull);
+            if (a.count_bitrev) atomicAdd(a.counters + C_BITREV, (unsigned long long)a.count_bitrev);
+        }
+    }
+}
+
+template <class A, int V, int K, int TQ, int NT, int LAY, int SMB>
+cudaError_t launch_tile(const TileArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {
+    using T = typename A::T;
+    using Tw = typename A::Tw;
+    constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);
+    constexpr size_t smem = ((size_t)sizeof(Tw) << SMB) + (PP ? 2 : 1) * (size_t)TQ * tile_stride<T, K, TQ>() * sizeof(T);
+    auto kern = k_tile<A, V, K, TQ, NT, LAY, SMB>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    const int M = LAY == TL_VARIANT ? a.L - K : (LAY == TL_SIX_A ? a.l1 : a.l2);
+    const uint64_t ntiles = a.batch * ((1ull << M) / TQ);
+    uint64_t grid = (uint64_t)num_sms * occ;
+    if (grid > ntiles) grid = ntiles;
+    if (grid == 0) return cudaSuccess;
+    kern<<<(unsigned)grid, NT, smem, s>>>(a);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace ftile
+}  // namespace nttb200

@@ -6,6 +6,7 @@
 #include <type_traits>
 #include "multipass.cuh"
 #include "fast.cuh"
+#include "tiles.cuh"
 
 namespace nttb200 {
 
@@ -133,7 +134,14 @@ cudaError_t run_variant(const MultipassReq& r) {
         a.scale = r.scale;
         return run_pass<F, V, LAY_VARIANT>(a, r.stream, r.num_sms, r.launches);
     }
-    // ---- multi-pass
+    // ---- multi-pass: compile-time tile kernels where a tile shape exists
+    {
+        bool ok = false;
+        cudaError_t te = cudaSuccess;
+        if constexpr (std::is_same<F, F32S>::value) te = tile_passes_f32(V, r.p < (1ull << 30), r, &ok);
+        else if constexpr (std::is_same<F, FGold>::value) te = tile_passes_gold(V, r, &ok);
+        if (te != cudaSuccess || ok) return te;
+    }
     int K[8];
     const int P = plan_passes(L, sizeof(T), V, K);
     T* ws0 = static_cast<T*>(r.ws);
@@ -227,6 +235,11 @@ cudaError_t run_variant(const MultipassReq& r) {
 template <class F>
 cudaError_t run_sixstep(const MultipassReq& r) {
     using T = typename F::T;
+    if constexpr (std::is_same<F, FGold>::value) {
+        bool ok = false;
+        cudaError_t te = tile_sixstep_gold(r, &ok);
+        if (te != cudaSuccess || ok) return te;
+    }
     constexpr int elog = tile_elems_log2<T>();
     int l1 = 0, l2 = 0;
     while ((1ull << l1) < r.n1) ++l1;

@@ -57,6 +57,7 @@ struct LazyF32 {
         const T z = x * w.x - q * p;
         return umin32(z, z - p);
     }
+    NTT_D T mulfull(T a, T b) const { return (T)(((uint64_t)a * b) % p); }
 };
 
 template <class F>
@@ -90,6 +91,7 @@ struct Canon {
     }
     NTT_D T fin(T x) const { return x; }
     NTT_D T mulc(T x, Tw w) const { return f.mul(x, w); }
+    NTT_D T mulfull(T a, T b) const { return f.mul_full(a, b); }
 };
 
 }  // namespace nttb200

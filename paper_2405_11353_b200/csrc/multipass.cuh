@@ -251,6 +251,8 @@ struct MultipassReq {
     const void* stw;           // per-stage table F::Tw[N]: T[2^(s-1)+k] = w^(k*N/2^s)
     const void* tw1;           // six-step size-n1 table
     const void* tw2;           // six-step size-n2 table
+    const void* stw1;          // six-step size-n1 / n2 per-stage tables
+    const void* stw2;
     const void* cor_lo;        // six-step two-level correction tables (F::T)
     const void* cor_hi;
     int cor_lb;

@@ -463,6 +463,8 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
         r.n1 = plan->n1; r.n2 = plan->n2;
         r.tw1 = plan->table1 ? plan->table1->tw : nullptr;
         r.tw2 = plan->table2 ? plan->table2->tw : nullptr;
+        r.stw1 = plan->table1 ? plan->table1->stw : nullptr;
+        r.stw2 = plan->table2 ? plan->table2->stw : nullptr;
         r.cor_lo = plan->cor_lo; r.cor_hi = plan->cor_hi; r.cor_lb = plan->cor_lb;
     }
     cudaError_t e = launch_mp_kind(plan->kind, r);

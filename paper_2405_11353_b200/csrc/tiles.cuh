@@ -1,0 +1,243 @@
+// tiles.cuh -- host planner chaining fasttile.cuh passes (multi-pass N and
+// the six-step split).  Instantiated in kt_f32.cu / kt_gold.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "fasttile.cuh"
+#include "multipass.cuh"
+
+namespace nttb200 {
+
+template <class F>
+inline typename F::Tw make_tw2(uint64_t w, uint64_t ws);
+template <> inline uint2 make_tw2<F32S>(uint64_t w, uint64_t ws) { return make_uint2((uint32_t)w, (uint32_t)ws); }
+template <> inline uint64_t make_tw2<FGold>(uint64_t w, uint64_t) { return w; }
+
+template <class T>
+__global__ void k_copy_rows(const T* src, T* dst, uint64_t n, uint64_t rows, unsigned long long* counters) {
+    const uint64_t n4 = n * sizeof(T) / 16;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += (uint64_t)gridDim.x * blockDim.x)
+        reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+    if (counters && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(counters + C_COPIES, (unsigned long long)rows);
+}
+
+namespace ftile {
+
+// Compile-time tile shapes: residues per tile = 2^TE (u32: 2^13, u64: 2^12).
+template <class T>
+constexpr int tile_e() { return sizeof(T) == 4 ? 13 : 12; }
+template <class T, int K>
+constexpr int tile_tq() { return 1 << (tile_e<T>() - K); }
+template <class T, int K>
+constexpr int tile_nt() { return (tile_tq<T, K>() << (K - 4)) < 512 ? (tile_tq<T, K>() << (K - 4)) : 512; }
+constexpr int kSmb = 11;
+
+template <class A, int V, int K>
+cudaError_t pass_k(const TileArgs<A>& a, cudaStream_t s, int sms, int* launches) {
+    using T = typename A::T;
+    return launch_tile<A, V, K, tile_tq<T, K>(), tile_nt<T, K>(), TL_VARIANT, kSmb>(a, s, sms, launches);
+}
+
+template <class A, int V>
+cudaError_t pass_any(int K, const TileArgs<A>& a, cudaStream_t s, int sms, int* launches, bool* ok) {
+    using T = typename A::T;
+    *ok = true;
+    if (sizeof(T) == 4) {
+        switch (K) {
+            case 7: return pass_k<A, V, 7>(a, s, sms, launches);
+            case 8: return pass_k<A, V, 8>(a, s, sms, launches);
+            case 9: return pass_k<A, V, 9>(a, s, sms, launches);
+            case 10: return pass_k<A, V, 10>(a, s, sms, launches);
+        }
+    } else {
+        switch (K) {
+            case 7: return pass_k<A, V, 7>(a, s, sms, launches);
+            case 8: return pass_k<A, V, 8>(a, s, sms, launches);
+            case 9: return pass_k<A, V, 9>(a, s, sms, launches);
+        }
+    }
+    *ok = false;
+    return cudaSuccess;
+}
+
+inline int tile_plan(int L, int word, int* K) {
+    const int kmax = word == 4 ? 10 : 9, kmin = 7;
+    int P = (L + kmax - 1) / kmax;
+    if (P < 2) P = 2;
+    for (int i = 0; i < P; ++i) K[i] = L / P + (i < L % P ? 1 : 0);
+    for (int i = 0; i < P; ++i)
+        if (K[i] < kmin || K[i] > kmax) return 0;
+    return P;
+}
+
+template <class A>
+TileArgs<A> tile_base(const MultipassReq& r) {
+    TileArgs<A> a{};
+    a.batch = r.batch;
+    a.L = r.L;
+    a.gstw = static_cast<const typename A::Tw*>(r.stw);
+    a.smb = kSmb;
+    a.p = r.p;
+    a.ninv = make_tw2<typename A::Field>(r.ninv, r.ninv_shoup);
+    a.counters = r.counters;
+    a.TA = 1;
+    return a;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Multi-pass transform by compile-time tile kernels.  *ok = false when no
+// tile shape covers this (L, word): the caller uses the generic engine.
+template <class A, int V>
+cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
+    using T = typename A::T;
+    *ok = false;
+    if (!r.stw || V == V_NAIVE || V == V_SIXSTEP) return cudaSuccess;
+    int K[8];
+    const int P = tile_plan(r.L, sizeof(T), K);
+    if (!P) return cudaSuccess;
+    const int L = r.L;
+    const uint64_t N = 1ull << L;
+    constexpr int VE = 16 / sizeof(T);
+    T* ws0 = static_cast<T*>(r.ws);
+    T* ws1 = ws0 + r.batch * N;
+    const T* cur = static_cast<const T*>(r.in);
+    const bool al = aligned16(r.in) && aligned16(r.out) && aligned16(r.ws);
+    cudaError_t e = cudaSuccess;
+    if (V == V_FLAT) {                     // bit_reverse_permute as its own HBM pass
+        dim3 blk(32, 8);
+        uint64_t blocks = r.batch << (L - 10);
+        uint64_t cap = (uint64_t)r.num_sms * 8;
+        k_bitrev<T><<<(unsigned)(blocks < cap ? blocks : cap), blk, 0, r.stream>>>(cur, ws1, r.batch, L, r.counters);
+        if (r.launches) ++*r.launches;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        cur = ws1;
+    }
+    int done = 0;
+    for (int i = 0; i < P; ++i) {
+        const bool last = (i == P - 1);
+        T* dst = last ? static_cast<T*>(r.out) : ((cur == ws0) ? ws1 : ws0);
+        if (V == V_PEASE && !last) dst = ws0;
+        TileArgs<A> a = tile_base<A>(r);
+        a.in = cur;
+        a.out = dst;
+        a.count_row = last;
+        a.scale = last ? r.scale : 0;
+        int k = K[i];
+        const int tq = 1 << (tile_e<T>() - k);
+        bool okp = false;
+        if (V == V_DIT || V == V_FLAT) {
+            a.S0 = done;
+            if (i == 0 && V == V_DIT) {
+                a.qmode = TQM_REV; a.rev_in = 1; a.in_order = TO_T_FAST; a.out_order = TO_C_FAST; a.count_bitrev = 1;
+            } else if (i == 0) {
+                a.qmode = TQM_LINEAR; a.in_order = TO_C_FAST; a.out_order = TO_C_FAST;
+            } else {
+                a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_T_FAST;
+            }
+            a.vec_in = a.vec_out = al && tq >= VE;
+            e = pass_any<A, V_DIT>(k, a, r.stream, r.num_sms, r.launches, &okp);
+            done += k;
+        } else if (V == V_DIF) {
+            k = K[P - 1 - i];
+            a.S0 = L - done - k;
+            if (last) {
+                a.qmode = TQM_REV; a.rev_out = 1; a.in_order = TO_C_FAST; a.out_order = TO_T_FAST; a.count_bitrev = 1;
+            } else {
+                a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_T_FAST;
+            }
+            a.vec_in = a.vec_out = al && (1 << (tile_e<T>() - k)) >= VE;
+            e = pass_any<A, V_DIF>(k, a, r.stream, r.num_sms, r.launches, &okp);
+            done += k;
+        } else if (V == V_PEASE || V == V_PEASE_NC) {
+            a.S0 = done;
+            if (i == 0) {
+                int ta = 1;
+                while (ta * ta < tq) ta <<= 1;
+                a.TA = ta;
+                a.la = __builtin_ctz(ta);
+                a.qmode = TQM_2D; a.rev_in = 1; a.in_order = TO_T_FAST; a.out_order = TO_TB_FAST; a.count_bitrev = 1;
+                a.vec_in = al && ta >= VE;
+                a.vec_out = 0;
+            } else {
+                a.qmode = TQM_LINEAR; a.in_order = TO_C_FAST; a.out_order = TO_T_FAST;
+                a.vec_in = al;
+                a.vec_out = al && tq >= VE;
+            }
+            e = pass_any<A, V_PEASE_NC>(k, a, r.stream, r.num_sms, r.launches, &okp);
+            done += k;
+        } else {  // Stockham
+            a.S0 = done;
+            a.qmode = TQM_LINEAR;
+            const int glob = L - done - k;
+            a.in_order = glob > 0 ? TO_T_FAST : TO_C_FAST;
+            a.out_order = TO_T_FAST;
+            a.vec_in = al && (glob == 0 || (1 << glob) >= VE) && tq >= VE;
+            a.vec_out = al && tq >= VE;
+            e = pass_any<A, V_STOCKHAM>(k, a, r.stream, r.num_sms, r.launches, &okp);
+            done += k;
+        }
+        if (e != cudaSuccess) return e;
+        if (!okp) return cudaErrorInvalidValue;      // tile_plan guarantees coverage
+        if (V == V_PEASE) {                          // _stage_copy per pass (algorithms.py:242)
+            k_copy_rows<T><<<r.num_sms * 4, 256, 0, r.stream>>>(dst, ws1, r.batch * N, r.batch, r.counters);
+            if (r.launches) ++*r.launches;
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            dst = ws1;
+        }
+        cur = dst;
+    }
+    *ok = true;
+    return cudaSuccess;
+}
+
+// Six-step with 2^13 x 2^13 Goldilocks sub-transforms (config 5 shape) and
+// any split whose sub-sizes have a compiled tile shape.
+template <class A, int K1, int K2>
+cudaError_t run_sixstep_tiles_k(const MultipassReq& r) {
+    using T = typename A::T;
+    T* rows = static_cast<T*>(r.ws);
+    const bool al = aligned16(r.in) && aligned16(r.out) && aligned16(r.ws);
+    cudaError_t e;
+    {
+        TileArgs<A> a = tile_base<A>(r);
+        a.in = static_cast<const T*>(r.in);
+        a.out = rows;
+        a.l1 = K1; a.l2 = K2; a.S0 = 0;
+        a.gstw = static_cast<const typename A::Tw*>(r.stw2);
+        a.smb = K2;
+        a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_C_FAST;
+        a.rev_local = 1;                                // bit_reverse_permute(row) (algorithms.py:374)
+        a.vec_in = 0;                                   // runs of TQ=2 residues (16 B): scalar gather
+        a.vec_out = al;
+        a.cor_lo = static_cast<const T*>(r.cor_lo);
+        a.cor_hi = static_cast<const T*>(r.cor_hi);
+        a.cor_lb = r.cor_lb;
+        e = launch_tile<A, V_DIT, K2, 2, 512, TL_SIX_A, K2>(a, r.stream, r.num_sms, r.launches);
+        if (e != cudaSuccess) return e;
+    }
+    {
+        TileArgs<A> a = tile_base<A>(r);
+        a.in = rows;
+        a.out = static_cast<T*>(r.out);
+        a.l1 = K1; a.l2 = K2; a.S0 = 0;
+        a.gstw = static_cast<const typename A::Tw*>(r.stw1);
+        a.smb = K1;
+        a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_T_FAST;
+        a.rev_local = 1;                                // bit_reverse_permute(col) (algorithms.py:385)
+        a.vec_in = a.vec_out = 0;
+        a.count_row = 1;
+        a.scale = r.scale;
+        e = launch_tile<A, V_DIT, K1, 2, 512, TL_SIX_B, K1>(a, r.stream, r.num_sms, r.launches);
+    }
+    return e;
+}
+
+}  // namespace ftile
+
+// entry points compiled in kt_f32.cu / kt_gold.cu
+cudaError_t tile_passes_f32(int variant, bool lazy, const MultipassReq& r, bool* ok);
+cudaError_t tile_passes_gold(int variant, const MultipassReq& r, bool* ok);
+cudaError_t tile_sixstep_gold(const MultipassReq& r, bool* ok);
+
+}  // namespace nttb200
