@@ -133,3 +133,95 @@ struct F64 {
 };
 
 }  // namespace nttb200
+
+namespace nttb200 {
+
+// Goldilocks with explicit 32-bit carry chains (PTX add.cc / addc / mad.wide).
+// Same canonical results as FGold (every op returns a value in [0,p)), but
+// the compiler's 64-bit compare+select sequences are replaced by carry flags:
+//   add: s = a+b; t = s + EPS; result = (carry(s) | carry(t)) ? t : s
+//        (a,b < p: s >= p  <=>  s + EPS overflows)
+//   sub: d = a-b; result = borrow ? d - EPS : d
+//   mul: 128-bit product from 4 mul.wide.u32, reduction 2^64 = EPS, 2^96 = -1.
+struct FGoldC {
+    using T = uint64_t;
+    using Tw = uint64_t;
+    static constexpr int kind = 2;
+    static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
+    uint64_t p;
+    NTT_D static uint32_t lo(uint64_t x) { return (uint32_t)x; }
+    NTT_D static uint32_t hi(uint64_t x) { return (uint32_t)(x >> 32); }
+    NTT_D static uint64_t mk(uint32_t l, uint32_t h) { return ((uint64_t)h << 32) | l; }
+    NTT_D static T add_c(T a, T b) {
+        uint32_t s0, s1, t0, t1, c;
+        asm("add.cc.u32 %0, %5, %7;\n\t"
+            "addc.cc.u32 %1, %6, %8;\n\t"
+            "addc.u32 %4, 0, 0;\n\t"
+            "add.cc.u32 %2, %0, 0xffffffff;\n\t"
+            "addc.cc.u32 %3, %1, 0;\n\t"
+            "addc.u32 %4, %4, 0;"
+            : "=r"(s0), "=r"(s1), "=r"(t0), "=r"(t1), "=r"(c)
+            : "r"(lo(a)), "r"(hi(a)), "r"(lo(b)), "r"(hi(b)));
+        return c ? mk(t0, t1) : mk(s0, s1);
+    }
+    NTT_D static T sub_c(T a, T b) {
+        uint32_t d0, d1, m;
+        (void)m;
+        asm("sub.cc.u32 %0, %3, %5;\n\t"
+            "subc.cc.u32 %1, %4, %6;\n\t"
+            "subc.u32 %2, 0, 0;\n\t"          // m = 0 or 0xffffffff (= EPS on borrow)
+            "sub.cc.u32 %0, %0, %2;\n\t"
+            "subc.u32 %1, %1, 0;"
+            : "=r"(d0), "=r"(d1), "=r"(m)
+            : "r"(lo(a)), "r"(hi(a)), "r"(lo(b)), "r"(hi(b)));
+        return mk(d0, d1);
+    }
+    NTT_D static T mul_c(T a, T b) {
+        uint32_t r0 = lo((uint64_t)lo(a) * lo(b)), r1 = hi((uint64_t)lo(a) * lo(b));
+        uint32_t r2 = lo((uint64_t)hi(a) * hi(b)), r3 = hi((uint64_t)hi(a) * hi(b));
+        // 128-bit product r3:r2:r1:r0 from four 32x32->64 partial products
+        const uint64_t p01 = (uint64_t)lo(a) * hi(b), p10 = (uint64_t)hi(a) * lo(b);
+        asm("add.cc.u32 %1, %1, %4;\n\t"
+            "addc.cc.u32 %2, %2, %5;\n\t"
+            "addc.u32 %3, %3, 0;\n\t"
+            "add.cc.u32 %1, %1, %6;\n\t"
+            "addc.cc.u32 %2, %2, %7;\n\t"
+            "addc.u32 %3, %3, 0;"
+            : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3)
+            : "r"(lo(p01)), "r"(hi(p01)), "r"(lo(p10)), "r"(hi(p10)));
+        // x = r1:r0 + r2 * 2^64 + r3 * 2^96 == (r1:r0) - r3 + r2 * (2^32 - 1)
+        uint32_t t0, t1, m, u0, u1, c;
+        asm("sub.cc.u32 %0, %6, %9;\n\t"          // t = lo64 - r3
+            "subc.cc.u32 %1, %7, 0;\n\t"
+            "subc.u32 %2, 0, 0;\n\t"              // m = borrow ? EPS : 0
+            "sub.cc.u32 %0, %0, %2;\n\t"          // t -= EPS on borrow (cannot underflow)
+            "subc.u32 %1, %1, 0;\n\t"
+            "sub.cc.u32 %3, 0, %8;\n\t"           // u = r2 * EPS = (r2 << 32) - r2
+            "subc.u32 %4, %8, 0;\n\t"
+            "add.cc.u32 %0, %0, %3;\n\t"          // t += u, carry c
+            "addc.cc.u32 %1, %1, %4;\n\t"
+            "addc.u32 %5, 0, 0;"
+            : "=r"(t0), "=r"(t1), "=r"(m), "=r"(u0), "=r"(u1), "=r"(c)
+            : "r"(r0), "r"(r1), "r"(r2), "r"(r3));
+        // on carry add EPS (2^64 = EPS, cannot overflow again); then canonicalise
+        // with the +EPS overflow test (s >= p  <=>  s + EPS >= 2^64)
+        uint32_t s0, s1, q0, q1, c2, mneg;
+        asm("neg.s32 %5, %6;\n\t"                  // 0 / 0xffffffff
+            "add.cc.u32 %0, %7, %5;\n\t"
+            "addc.u32 %1, %8, 0;\n\t"
+            "add.cc.u32 %2, %0, 0xffffffff;\n\t"
+            "addc.cc.u32 %3, %1, 0;\n\t"
+            "addc.u32 %4, 0, 0;"
+            : "=r"(s0), "=r"(s1), "=r"(q0), "=r"(q1), "=r"(c2), "=r"(mneg)
+            : "r"(c), "r"(t0), "r"(t1));
+        (void)m; (void)u0; (void)u1;
+        return c2 ? mk(q0, q1) : mk(s0, s1);
+    }
+    NTT_D T add(T a, T b) const { return add_c(a, b); }
+    NTT_D T sub(T a, T b) const { return sub_c(a, b); }
+    NTT_D T mul(T x, Tw w) const { return mul_c(x, w); }
+    NTT_D T mul_full(T a, T b) const { return mul_c(a, b); }
+    NTT_D static T tw_value(Tw w) { return w; }
+};
+
+}  // namespace nttb200

@@ -44,13 +44,21 @@ struct TileArgs {
     int in_order, out_order;
     int vec_in, vec_out;       // 16-byte vector copies valid for this pass
     int rev_in, rev_out;
-    int rev_local;             // six-step: bit-reverse the K local bits on the gather (sub-DIT input)
+    int rev_local;             // bit-reverse the K local bits on the gather (six-step sub-DIT input;
+                               // Pease pass 1 reading the row-bit-reversed intermediate)
+    int out_trb;               // Pease pass 0: write position (x << (L-K)) | rev_{L-K}(Q) (row-bit-reversed
+                               // transpose of the stage state) so both HBM sides are 32-byte runs
     int count_row, count_bitrev;
     const Tw* gstw;            // global per-stage table of the (sub-)transform
     int smb;                   // entries [0, 2^smb) are staged in shared memory
     uint64_t p;
     int scale;
     Tw ninv;
+    int twist;                 // four-step factorisation of a late pass (docs/PASS_ALGEBRA.md):
+                               // 0 none, 1 pre w^(Q*rev(x)), 2 pre w^(Q*x), 3 post w^(Q*rev(x))
+    const Tw* tw_lo;           // w^j, j < 2^th          (the plan's main table prefix)
+    const Tw* tw_hi;           // w^(j*2^th), j < 2^(L-th)
+    int th;
     int l1, l2;                // six-step split
     const T* cor_lo;
     const T* cor_hi;
@@ -78,8 +86,10 @@ NTT_D uint64_t t_gpos_out(const TileArgs<A>& a, uint32_t Q, uint32_t x) {
     if (LAY == TL_SIX_B) return ((uint64_t)x << a.l2) | Q;
     const int L = a.L, S0 = a.S0;
     uint64_t g;
-    if (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM) g = Q | ((uint64_t)x << (L - K));
-    else g = (Q & ((1u << S0) - 1)) | ((uint64_t)x << S0) | ((uint64_t)(Q >> S0) << (S0 + K));
+    if (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM) {
+        if (a.out_trb) return ((uint64_t)x << (L - K)) | brev(Q, L - K);
+        g = Q | ((uint64_t)x << (L - K));
+    } else g = (Q & ((1u << S0) - 1)) | ((uint64_t)x << S0) | ((uint64_t)(Q >> S0) << (S0 + K));
     return a.rev_out ? (uint64_t)brev((uint32_t)g, L) : g;
 }
 
@@ -224,7 +234,7 @@ struct TileGeo {
 };
 
 // ----------------------------------------------------------------- kernel --
-template <class A, int V, int K, int TQ, int NT, int LAY, int SMB>
+template <class A, int V, int K, int TQ, int NT, int LAY, int SMB, int TWB>
 __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 2))) k_tile(TileArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
@@ -240,7 +250,11 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
     __shared__ uint32_t Qs[TQ];
     __shared__ uint64_t Rb[TQ];
     Tw* tws = reinterpret_cast<Tw*>(smem_raw);
-    T* bufA = reinterpret_cast<T*>(smem_raw + ((size_t)sizeof(Tw) << SMB));
+    // per-tile twist tables (only when a.twist): network t, j < 32:
+    //   twl[t][j] = w^(Q_t * j), twh[t][j] = w^(Q_t * 32 * j)  (rows padded to 33)
+    Tw* twl = tws + (1 << SMB);
+    Tw* twh = twl + TQ * 33;
+    T* bufA = reinterpret_cast<T*>(smem_raw + ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * 66 : 0));
     T* bufB = PP ? bufA + TQ * NP : bufA;
     A ar;
     ar.init(a.p);
@@ -258,9 +272,16 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
     auto twsrc = [&](int last_stage) -> TwSrc<Tw> {
         return last_stage <= smb ? TwSrc<Tw>{tws, false} : TwSrc<Tw>{a.gstw, true};
     };
-    const int Lt = (LAY == TL_VARIANT) ? L : K;      // twiddle frame (six-step: sub-transform)
-    const int S0t = (LAY == TL_VARIANT) ? S0 : 0;
-    (void)Lt;
+    // local mode: six-step sub-transforms, or a late pass factorised into
+    // twist + local transform -- stage twiddles from the local table prefix only
+    const bool loc = (LAY != TL_VARIANT) || a.twist;
+    const int S0t = loc ? 0 : S0;
+    const int Lg = loc ? K : L;
+    // twist factor w^(Q_t * xr) = twl[t][xr mod 32] * twh[t][xr >> 5] applied to v
+    auto twistv = [&](T v, uint32_t t, uint32_t x) -> T {
+        const uint32_t xr = (a.twist == 2) ? x : brev(x, K);
+        return ar.mulc(ar.mulc(v, twl[t * 33 + (xr & 31)]), twh[t * 33 + (xr >> 5)]);
+    };
 
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         __syncthreads();
@@ -279,6 +300,15 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
             Rb[t] = row * N;
         }
         __syncthreads();
+        if (TWB && a.twist) {                 // per-network twist tables from the main table w^i
+            const uint64_t nm = N - 1;
+            for (uint32_t i = threadIdx.x; i < TQ * 64u; i += NT) {
+                const uint32_t t = i >> 6, j = i & 31;
+                const uint64_t e = (i & 32) ? ((uint64_t)Qs[t] * 32u * j) & nm : ((uint64_t)Qs[t] * j) & nm;
+                ((i & 32) ? twh : twl)[t * 33 + j] = __ldg(a.tw_lo + e);
+            }
+            __syncthreads();
+        }
         // ---- gather (16-byte vectors along the contiguous run when valid)
         if (a.vec_in && a.in_order == TO_T_FAST) {
 #pragma unroll 4
@@ -288,7 +318,11 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
                 T tmp[VE];
                 *reinterpret_cast<uint4*>(tmp) = __ldg(reinterpret_cast<const uint4*>(src));
 #pragma unroll
-                for (int e = 0; e < VE; ++e) bufA[(t0 + e) * NP + padpos<T>(a.rev_local ? brev(x, K) : x)] = tmp[e];
+                for (int e = 0; e < VE; ++e) {
+                    T v = tmp[e];
+                    if (TWB && a.twist && a.twist < 3) v = twistv(v, t0 + e, a.rev_local ? brev(x, K) : x);
+                    bufA[(t0 + e) * NP + padpos<T>(a.rev_local ? brev(x, K) : x)] = v;
+                }
             }
         } else if (a.vec_in && a.in_order == TO_C_FAST) {
 #pragma unroll 4
@@ -298,8 +332,11 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
                 T tmp[VE];
                 *reinterpret_cast<uint4*>(tmp) = __ldg(reinterpret_cast<const uint4*>(src));
 #pragma unroll
-                for (int e = 0; e < VE; ++e)
-                    bufA[t * NP + padpos<T>(a.rev_local ? brev(x0 + e, K) : x0 + e)] = tmp[e];
+                for (int e = 0; e < VE; ++e) {
+                    T v = tmp[e];
+                    if (TWB && a.twist && a.twist < 3) v = twistv(v, t, a.rev_local ? brev(x0 + e, K) : x0 + e);
+                    bufA[t * NP + padpos<T>(a.rev_local ? brev(x0 + e, K) : x0 + e)] = v;
+                }
             }
         } else {
 #pragma unroll 4
@@ -308,8 +345,9 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
                 if (a.in_order == TO_C_FAST) { t = i >> K; x = i & ((1u << K) - 1); }
                 else if (a.in_order == TO_T_FAST) { t = i % TQ; x = i / TQ; }
                 else { const int lb = LTQ - a.la; const uint32_t tb = i & ((1u << lb) - 1), ta = (i >> lb) & (a.TA - 1); t = ta + (tb << a.la); x = i / TQ; }
-                bufA[t * NP + padpos<T>(a.rev_local ? brev(x, K) : x)] =
-                    __ldg(a.in + Rb[t] + t_gpos_in<A, V, K, LAY>(a, Qs[t], x));
+                T v = __ldg(a.in + Rb[t] + t_gpos_in<A, V, K, LAY>(a, Qs[t], x));
+                if (TWB && a.twist && a.twist < 3) v = twistv(v, t, a.rev_local ? brev(x, K) : x);
+                bufA[t * NP + padpos<T>(a.rev_local ? brev(x, K) : x)] = v;
             }
         }
         __syncthreads();
@@ -324,7 +362,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
             for (int r = 0; r < REP; ++r) {
                 const uint32_t tid = threadIdx.x + r * NT;
                 const uint32_t t = tid / TT, u = tid % TT;
-                const uint32_t Q = (LAY == TL_VARIANT) ? Qs[t] : 0u;
+                const uint32_t Q = loc ? 0u : Qs[t];
                 T* sb = src + t * NP;
                 T* db = dst + t * NP;
                 if (V == V_DIT || V == V_DIF) {
@@ -339,7 +377,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
                     NTT_TMAP(0) NTT_TMAP(1) NTT_TMAP(2) NTT_TMAP(3) NTT_TMAP(4) NTT_TMAP(5) NTT_TMAP(6)
                     NTT_TMAP(7) NTT_TMAP(8) NTT_TMAP(9)
 #undef NTT_TMAP
-                    const uint32_t qlow = (LAY == TL_VARIANT) ? (Q & ((1u << S0t) - 1)) : 0u;
+                    const uint32_t qlow = loc ? 0u : (Q & ((1u << S0t) - 1));
                     const int b0g = (V == V_DIT) ? (g == 0 ? 0 : B) : (g == G - 1 ? 0 : B);
                     const TwSrc<Tw> tw = twsrc(S0t + b0g + kg);
                     T* wb = sb + padpos<T>(pbase);
@@ -362,7 +400,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
                 } else if (V != V_STOCKHAM) {
                     const int sg = g == 0 ? 0 : K0 + 4 * (g - 1);
                     const int kg = g == 0 ? K0 : 4;
-                    const uint32_t qtop = S0t ? (Q >> (L - K - S0t)) : 0u;
+                    const uint32_t qtop = S0t ? (Q >> (Lg - K - S0t)) : 0u;
                     const TwSrc<Tw> tw = twsrc(S0t + sg + kg);
                     const T* rb = sb + padpos<T>(u << 4);
 #pragma unroll
@@ -386,8 +424,8 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
                     const int sg = g == 0 ? 0 : K0 + 4 * (g - 1);
                     const int kg = g == 0 ? K0 : 4;
                     const int lob = K - sg - kg;
-                    const int glob = L - S0t - K;
-                    const uint32_t ghi = (LAY == TL_VARIANT && S0t) ? (Q >> glob) : 0u;
+                    const int glob = Lg - S0t - K;
+                    const uint32_t ghi = (!loc && S0t) ? (Q >> glob) : 0u;
                     const TwSrc<Tw> tw = twsrc(S0t + sg + kg);
                     uint32_t hi, lo;
                     if (g == 0) { hi = 0; lo = u; }
@@ -420,6 +458,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
 
         // ---- scatter (final reduction, n_inv, six-step correction twiddles)
         auto finish = [&](uint32_t t, uint32_t x, T v) -> T {
+            if (TWB && a.twist == 3) v = twistv(v, t, x);
             T r = ar.fin(v);
             if (LAY == TL_SIX_A) {
                 const uint64_t e = ((uint64_t)Qs[t] * x) & (N - 1);
@@ -464,13 +503,15 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
     }
 }
 
-template <class A, int V, int K, int TQ, int NT, int LAY, int SMB>
+template <class A, int V, int K, int TQ, int NT, int LAY, int SMB, int TWB = 0>
 cudaError_t launch_tile(const TileArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {
     using T = typename A::T;
     using Tw = typename A::Tw;
     constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);
-    constexpr size_t smem = ((size_t)sizeof(Tw) << SMB) + (PP ? 2 : 1) * (size_t)TQ * tile_stride<T, K, TQ>() * sizeof(T);
-    auto kern = k_tile<A, V, K, TQ, NT, LAY, SMB>;
+    constexpr size_t smem = ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * 66 : 0) +
+                            (PP ? 2 : 1) * (size_t)TQ * tile_stride<T, K, TQ>() * sizeof(T);
+    if (a.twist && K > 10) return cudaErrorInvalidValue;   // twist tables cover xr < 2^10
+    auto kern = k_tile<A, V, K, TQ, NT, LAY, SMB, TWB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0;

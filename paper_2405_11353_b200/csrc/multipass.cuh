@@ -253,6 +253,8 @@ struct MultipassReq {
     const void* tw2;           // six-step size-n2 table
     const void* stw1;          // six-step size-n1 / n2 per-stage tables
     const void* stw2;
+    const void* twh;           // four-step twist hi table F::Tw[2^(L-twh_bits)]: w^(j*2^twh_bits)
+    int twh_bits;
     const void* cor_lo;        // six-step two-level correction tables (F::T)
     const void* cor_hi;
     int cor_lb;

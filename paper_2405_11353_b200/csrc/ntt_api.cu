@@ -233,6 +233,9 @@ struct ntt_plan_s {
     void* cor_lo = nullptr;
     void* cor_hi = nullptr;
     int cor_lb = 0;
+    // four-step twist hi table (u32 multi-pass): w^(j * 2^twh_bits) + Shoup word
+    void* twh = nullptr;
+    int twh_bits = 0;
     int num_sms = 148;
     // workspace for multi-pass plans and host-buffer execution
     void* ws = nullptr;
@@ -248,6 +251,7 @@ struct ntt_plan_s {
         if (hbuf) cudaFree(hbuf);
         if (cor_lo) cudaFree(cor_lo);
         if (cor_hi) cudaFree(cor_hi);
+        if (twh) cudaFree(twh);
         cudaSetDevice(cur);
     }
 };
@@ -404,6 +408,29 @@ int ntt_plan_create(uint64_t p, uint64_t g, int w_bits, uint64_t n, int variant,
         if ((st = upload_powers(p, powmod(omega, 1ull << pl->cor_lb, p), 1ull << (L - pl->cor_lb), word_bytes,
                                 device, &pl->cor_hi))) return st;
     }
+    if (word_bytes == 4 && variant != NTT_NAIVE && variant != NTT_SIXSTEP && L > smem_max_log2_word(4) && L <= 20) {
+        // twist hi table for the four-step factorisation of the late pass
+        const int th = (L + 1) / 2;
+        uint64_t omega = powmod(g, (p - 1) / n, p);
+        if (direction == NTT_INVERSE) omega = powmod(omega, p - 2, p);
+        const uint64_t step = powmod(omega, 1ull << th, p);
+        const uint64_t cnt = 1ull << (L - th);
+        std::vector<uint32_t> buf(2 * cnt);
+        uint64_t x = 1;
+        for (uint64_t j = 0; j < cnt; ++j) {
+            buf[2 * j] = (uint32_t)x;
+            buf[2 * j + 1] = (uint32_t)shoup_word(x, p, 32);
+            x = mulmod(x, step, p);
+        }
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        cudaError_t e = cudaMalloc(&pl->twh, buf.size() * 4);
+        if (e == cudaSuccess) e = cudaMemcpy(pl->twh, buf.data(), buf.size() * 4, cudaMemcpyHostToDevice);
+        cudaSetDevice(cur);
+        if (e != cudaSuccess) { pl->twh = nullptr; return cuda_fail(e, "twist table upload"); }
+        pl->twh_bits = th;
+    }
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
         pl->num_sms = sms;
@@ -459,6 +486,8 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
     r.ninv = plan->table->n_inv; r.ninv_shoup = plan->table->n_inv_dev_shoup;
     r.counters = ctr; r.stream = stream; r.num_sms = plan->num_sms; r.launches = &launches;
     r.ws = plan->ws;
+    r.twh = plan->twh;
+    r.twh_bits = plan->twh_bits;
     if (plan->variant == NTT_SIXSTEP) {
         r.n1 = plan->n1; r.n2 = plan->n2;
         r.tw1 = plan->table1 ? plan->table1->tw : nullptr;

@@ -35,7 +35,8 @@ constexpr int kSmb = 11;
 template <class A, int V, int K>
 cudaError_t pass_k(const TileArgs<A>& a, cudaStream_t s, int sms, int* launches) {
     using T = typename A::T;
-    return launch_tile<A, V, K, tile_tq<T, K>(), tile_nt<T, K>(), TL_VARIANT, kSmb>(a, s, sms, launches);
+    constexpr int TWB = sizeof(T) == 4 ? 10 : 0;    // twist tables for the u32 late pass
+    return launch_tile<A, V, K, tile_tq<T, K>(), tile_nt<T, K>(), TL_VARIANT, kSmb, TWB>(a, s, sms, launches);
 }
 
 template <class A, int V>
@@ -103,6 +104,9 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
     T* ws1 = ws0 + r.batch * N;
     const T* cur = static_cast<const T*>(r.in);
     const bool al = aligned16(r.in) && aligned16(r.out) && aligned16(r.ws);
+    // four-step factorisation of the late pass (u32 fields, 2-pass plans): the
+    // network-dependent stage twiddles become one per-element twist
+    const bool fac = sizeof(T) == 4 && P == 2 && K[0] <= 10 && K[1] <= 10;
     cudaError_t e = cudaSuccess;
     if (V == V_FLAT) {                     // bit_reverse_permute as its own HBM pass
         dim3 blk(32, 8);
@@ -126,6 +130,7 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
         int k = K[i];
         const int tq = 1 << (tile_e<T>() - k);
         bool okp = false;
+        if (fac) a.tw_lo = static_cast<const typename A::Tw*>(r.tw);     // main table w^i
         if (V == V_DIT || V == V_FLAT) {
             a.S0 = done;
             if (i == 0 && V == V_DIT) {
@@ -136,6 +141,7 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
                 a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_T_FAST;
             }
             a.vec_in = a.vec_out = al && tq >= VE;
+            if (fac && i == 1) a.twist = 1;
             e = pass_any<A, V_DIT>(k, a, r.stream, r.num_sms, r.launches, &okp);
             done += k;
         } else if (V == V_DIF) {
@@ -147,11 +153,19 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
                 a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_T_FAST;
             }
             a.vec_in = a.vec_out = al && (1 << (tile_e<T>() - k)) >= VE;
+            if (fac && i == 0) a.twist = 3;
             e = pass_any<A, V_DIF>(k, a, r.stream, r.num_sms, r.launches, &okp);
             done += k;
         } else if (V == V_PEASE || V == V_PEASE_NC) {
             a.S0 = done;
-            if (i == 0) {
+            if (i == 0 && P == 2) {
+                // networks with consecutive rev(Q): natural-order gather runs; the
+                // stage state is written row-bit-reversed-transposed (out_trb) so the
+                // scatter runs are contiguous too; pass 1 undoes it (rev_local)
+                a.qmode = TQM_REV; a.rev_in = 1; a.out_trb = 1;
+                a.in_order = TO_T_FAST; a.out_order = TO_T_FAST; a.count_bitrev = 1;
+                a.vec_in = a.vec_out = al && tq >= VE;
+            } else if (i == 0) {
                 int ta = 1;
                 while (ta * ta < tq) ta <<= 1;
                 a.TA = ta;
@@ -161,9 +175,11 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
                 a.vec_out = 0;
             } else {
                 a.qmode = TQM_LINEAR; a.in_order = TO_C_FAST; a.out_order = TO_T_FAST;
+                a.rev_local = (P == 2);
                 a.vec_in = al;
                 a.vec_out = al && tq >= VE;
             }
+            if (fac && i == 1) a.twist = 1;
             e = pass_any<A, V_PEASE_NC>(k, a, r.stream, r.num_sms, r.launches, &okp);
             done += k;
         } else {  // Stockham
@@ -174,6 +190,7 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
             a.out_order = TO_T_FAST;
             a.vec_in = al && (glob == 0 || (1 << glob) >= VE) && tq >= VE;
             a.vec_out = al && tq >= VE;
+            if (fac && i == 1) a.twist = 2;
             e = pass_any<A, V_STOCKHAM>(k, a, r.stream, r.num_sms, r.launches, &okp);
             done += k;
         }

@@ -1,0 +1,147 @@
+"""Prototype (pure Python, small N) of the four-step factorisation of a late
+pass: K consecutive stages of DIT / Pease / Stockham (second pass) or DIF
+(first pass) == per-element twist + a LOCAL size-2^K transform of the same
+variant using only local twiddles.  Verifies the twist exponents used by
+csrc/fasttile.cuh against the oracle's per-stage replay.
+"""
+import random
+
+P = 998244353
+G = 3
+
+
+def rev(x, b):
+    return int(format(x, f"0{b}b")[::-1], 2) if b else 0
+
+
+def tables(L):
+    n = 1 << L
+    w = pow(G, (P - 1) // n, P)
+    return n, w, [pow(w, i, P) for i in range(n)]
+
+
+def dit_stage(a, s, L, wp):
+    n = 1 << L
+    m, half, stride = 1 << s, 1 << (s - 1), n >> s
+    for j in range(0, n, m):
+        for k in range(half):
+            lo, hi = j + k, j + k + half
+            t = a[hi] * wp[k * stride] % P
+            a[lo], a[hi] = (a[lo] + t) % P, (a[lo] - t) % P
+
+
+def dif_stage(a, s, L, wp):
+    n = 1 << L
+    m, half, stride = 1 << s, 1 << (s - 1), n >> s
+    for j in range(0, n, m):
+        for k in range(half):
+            lo, hi = j + k, j + k + half
+            f1, f2 = a[lo], a[hi]
+            a[lo] = (f1 + f2) % P
+            a[hi] = (f1 - f2) * wp[k * stride] % P
+
+
+def pease_stage(src, s, L, wp):
+    n = 1 << L
+    dst = [0] * n
+    low = L - s
+    for r in range(n // 2):
+        e = (r >> low) << low
+        t = src[2 * r + 1] * wp[e] % P
+        dst[r] = (src[2 * r] + t) % P
+        dst[r + n // 2] = (src[2 * r] - t) % P
+    return dst
+
+
+def stockham_stage(cur, s, L, wp):
+    n = 1 << L
+    nxt = [0] * n
+    span, stride = 1 << s, n >> (s + 1)
+    for j in range(span):
+        e = j * stride
+        for i in range(stride):
+            a, b = cur[2 * j * stride + i], cur[2 * j * stride + stride + i] * wp[e] % P
+            nxt[j * stride + i] = (a + b) % P
+            nxt[j * stride + i + n // 2] = (a - b) % P
+    return nxt
+
+
+def check(L, K0):
+    """2-pass split L = K0 + K1 for each variant."""
+    n, w, wp = tables(L)
+    K1 = L - K0
+    x = [random.randrange(P) for _ in range(n)]
+    ok = {}
+    # ---------------- DIT: pass 2 (window [K0, L)) = twist + local DIT (size 2^K1)
+    a = [x[rev(i, L)] for i in range(n)]
+    for s in range(1, K0 + 1):
+        dit_stage(a, s, L, wp)
+    ref = list(a)
+    for s in range(K0 + 1, L + 1):
+        dit_stage(ref, s, L, wp)
+    M = 1 << K1
+    _, wl, wpl = tables(K1)            # local table (size-2^K1 root = w^(N/M))
+    assert wl == pow(w, n // M, P)
+    out = [0] * n
+    for r in range(1 << K0):           # network = low K0 bits
+        v = [a[r + (xx << K0)] for xx in range(M)]               # local position xx = block
+        v = [v[xx] * pow(w, r * rev(xx, K1), P) % P for xx in range(M)]   # twist W^(r*rev(x)), W = w
+        for s in range(1, K1 + 1):
+            dit_stage(v, s, K1, wpl)
+        for xx in range(M):
+            out[r + (xx << K0)] = v[xx]
+    ok["dit"] = out == ref
+    # ---------------- Pease: pass 2 = twist + local Pease
+    b = [x[rev(i, L)] for i in range(n)]
+    for s in range(1, K0 + 1):
+        b = pease_stage(b, s, L, wp)
+    ref = list(b)
+    for s in range(K0 + 1, L + 1):
+        ref = pease_stage(ref, s, L, wp)
+    out = [0] * n
+    for Q in range(1 << K0):           # network Q reads Q*2^K1 + x, writes Q | R << K0
+        v = [b[(Q << K1) + xx] for xx in range(M)]
+        v = [v[xx] * pow(w, Q * rev(xx, K1), P) % P for xx in range(M)]
+        for s in range(1, K1 + 1):
+            v = pease_stage(v, s, K1, wpl)
+        for R in range(M):
+            out[Q | (R << K0)] = v[R]
+    ok["pease"] = out == ref
+    # ---------------- Stockham: pass 2 = twist + local Stockham
+    c = list(x)
+    for s in range(K0):
+        c = stockham_stage(c, s, L, wp)
+    ref = list(c)
+    for s in range(K0, L):
+        ref = stockham_stage(ref, s, L, wp)
+    out = [0] * n
+    glob = L - K0 - K1                # = 0 here: Q = ghi (top K0 bits)
+    for Q in range(1 << K0):
+        v = [c[(Q << K1) + xx] for xx in range(M)]      # position ghi << (L-S0) | x
+        v = [v[xx] * pow(w, Q * xx, P) % P for xx in range(M)]   # Stockham twist: natural x
+        for s in range(K1):
+            v = stockham_stage(v, s, K1, wpl)
+        for R in range(M):
+            out[(R << K0) | Q] = v[R]
+    ok["stockham"] = out == ref
+    # ---------------- DIF: pass 1 (window [K0, L), top) = local DIF + post-twist
+    d = list(x)
+    ref = list(d)
+    for s in range(L, K0, -1):
+        dif_stage(ref, s, L, wp)
+    out = [0] * n
+    for r in range(1 << K0):           # network = low K0 bits, local x at bits [K0, L)
+        v = [d[r + (xx << K0)] for xx in range(M)]
+        for s in range(K1, 0, -1):
+            dif_stage(v, s, K1, wpl)
+        v = [v[xx] * pow(w, r * rev(xx, K1), P) % P for xx in range(M)]   # post-twist
+        for xx in range(M):
+            out[r + (xx << K0)] = v[xx]
+    ok["dif"] = out == ref
+    return ok
+
+
+if __name__ == "__main__":
+    random.seed(1)
+    for L, K0 in ((6, 3), (7, 3), (7, 4), (8, 4), (9, 5)):
+        print(L, K0, check(L, K0))

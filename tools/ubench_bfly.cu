@@ -1,0 +1,105 @@
+// Micro-benchmark: butterfly throughput of each arithmetic policy with no
+// memory traffic (register-resident, 16 independent values per thread), to
+// measure the integer-pipe ceiling that bounds the NTT kernels on B200.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr
+//      -I paper_2405_11353_b200/csrc tools/ubench_bfly.cu -o build/ubench_bfly
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "lazy.cuh"
+
+using namespace nttb200;
+
+template <class A>
+__global__ void k_bfly(typename A::T* out, uint64_t p, int iters, typename A::Tw w0, typename A::Tw w1) {
+    using T = typename A::T;
+    A ar;
+    ar.init(p);
+    T v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = (T)(threadIdx.x * 16 + i + blockIdx.x);
+    typename A::Tw w = w0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                if (c & (1 << j)) continue;
+                ar.dit(v[c], v[c | (1 << j)], w);
+            }
+        }
+        w = (it & 1) ? w0 : w1;
+    }
+    T acc = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc ^= v[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+template <class A>
+void run(const char* name, uint64_t p, typename A::Tw w0, typename A::Tw w1, int threads) {
+    using T = typename A::T;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    T* out;
+    cudaMalloc(&out, (size_t)sms * 8 * threads * sizeof(T));
+    const int iters = 2000;
+    const int blocks = sms * (2048 / threads);
+    k_bfly<A><<<blocks, threads>>>(out, p, 10, w0, w1);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    k_bfly<A><<<blocks, threads>>>(out, p, iters, w0, w1);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    double bfly = (double)blocks * threads * iters * 32;   // 4 stages x 8 butterflies
+    printf("%-12s threads/blk=%4d  %.3f ms  %.2f Tbfly/s  (%.2f warp-bfly/clk/SM at 1.9GHz)\n", name, threads, ms,
+           bfly / ms / 1e9, bfly / 32 / (ms * 1e-3) / sms / 1.9e9);
+    cudaFree(out);
+}
+
+__global__ void k_goldcheck(const uint64_t* a, const uint64_t* b, int n, int* bad) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    FGold f; f.p = FGold::P;
+    uint64_t x = a[i], y = b[i];
+    if (FGoldC::mul_c(x, y) != f.mul_full(x, y)) atomicAdd(bad, 1);
+    if (FGoldC::add_c(x, y) != f.add(x, y)) atomicAdd(bad + 1, 1);
+    if (FGoldC::sub_c(x, y) != f.sub(x, y)) atomicAdd(bad + 2, 1);
+}
+void check_gold() {
+    const int n = 1 << 22;
+    uint64_t *a, *b; int* bad;
+    cudaMallocManaged(&a, n * 8); cudaMallocManaged(&b, n * 8); cudaMallocManaged(&bad, 12);
+    uint64_t s = 88172645463325252ull;
+    const uint64_t P = FGold::P;
+    for (int i = 0; i < n; ++i) {
+        s ^= s << 13; s ^= s >> 7; s ^= s << 17; a[i] = s % P;
+        s ^= s << 13; s ^= s >> 7; s ^= s << 17; b[i] = s % P;
+        if (i < 64) { a[i] = P - 1 - i; b[i] = (i & 1) ? P - 1 : i; }
+    }
+    bad[0] = bad[1] = bad[2] = 0;
+    k_goldcheck<<<(n + 255) / 256, 256>>>(a, b, n, bad);
+    cudaDeviceSynchronize();
+    printf("goldcheck mismatches: mul %d add %d sub %d (of %d)\n", bad[0], bad[1], bad[2], n);
+}
+
+int main() {
+    const uint32_t p = 998244353u;
+    uint2 w0 = make_uint2(3, (uint32_t)(((uint64_t)3 << 32) / p));
+    uint2 w1 = make_uint2(5, (uint32_t)(((uint64_t)5 << 32) / p));
+    run<LazyF32>("lazy-u32", p, w0, w1, 256);
+    run<LazyF32>("lazy-u32", p, w0, w1, 512);
+    run<Canon<F32S>>("canon-u32", p, w0, w1, 256);
+    const uint64_t G = 0xFFFFFFFF00000001ull;
+    run<Canon<FGold>>("goldilocks", G, 7ull, 49ull, 256);
+    run<Canon<FGold>>("goldilocks", G, 7ull, 49ull, 512);
+    run<Canon<FGoldC>>("gold-carry", G, 7ull, 49ull, 256);
+    run<Canon<FGoldC>>("gold-carry", G, 7ull, 49ull, 512);
+    // exactness check of FGoldC vs FGold on random operands
+    check_gold();
+    return 0;
+}
