@@ -301,6 +301,37 @@ def main() -> None:
             except Exception as exc:  # report, do not hide
                 extra[f"config{cfg}_{var}"] = {"error": repr(exc)[:300]}
 
+    if world > 1 and not args.no_extra:
+        # config 5 as ONE transform split four-step across the ranks (strong
+        # scaling, one NCCL all-to-all per step); slab layout per distributed.py
+        try:
+            from paper_2405_11353_b200.distributed import DistributedSixStep, column_slab
+            wc = CONFIGS[5]
+            params = P.FieldParams(wc.p, wc.g, wc.w)
+            ds = DistributedSixStep(params, wc.n, n1=wc.n1, n2=wc.n // wc.n1)
+            xh = seeded_input(wc)[0]
+            slab = torch.from_numpy(column_slab(xh, rank, world, ds.n1, ds.n2).view(np.int64)).view(torch.uint64).to(dev)
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    ds.run(slab)
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                nst = max(3, min(args.steps, 10))
+                e0.record(stream)
+                for _ in range(nst):
+                    ds.run(slab)
+                e1.record(stream)
+                stream.synchronize()
+            barrier()
+            t = max_over_ranks(e0.elapsed_time(e1)) / 1e3 / nst
+            extra["config5_sixstep_distributed"] = {
+                "ntt_per_s": 1.0 / t, "ms_per_step": 1e3 * t, "scaling": "strong", "ranks": world,
+                "gbfly_per_s": wc.butterflies() / t / 1e9,
+                "alltoall_bytes_per_rank": (world - 1) * (wc.n // world // world) * 8,
+                "workload": "1 x 2^26 Goldilocks, four-step 2^13 x 2^13, one NCCL all_to_all_single"}
+        except Exception as exc:
+            extra["config5_sixstep_distributed"] = {"error": repr(exc)[:300]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, cores, sample = cpu_oracle_rate(w, args.variant, 10.0)

@@ -107,6 +107,19 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
  * shared-memory-resident plans); the library allocates and caches it. */
 uint64_t ntt_plan_workspace_bytes(ntt_plan_t plan, uint64_t batch);
 
+/* Distributed four-step of a six-step plan (algorithms.py:355-389 split
+ * across `world` ranks).  Rank g owns input columns
+ * i in [g*n1/G, (g+1)*n1/G) as the slab x_local[j][i_local] (n2 x n1/G) and
+ * produces output columns k2 in [g*n2/G, ...) as out_local[k1][k2_local]
+ * (n1 x n2/G), i.e. out[k1*n2 + k2].  step 0 (A): strided size-n2 DITs +
+ * correction twiddles, written packed for the exchange as
+ * send[h][i_local][k2_local] (h = destination rank); the caller then runs ONE
+ * equal-split all-to-all (NCCL) of n1*n2/G^2 residues per peer; step 1 (B):
+ * size-n1 DITs of the received recv[i][k2_local].  world must be a power of
+ * two dividing n1 and n2. */
+int ntt_sixstep_dist_step(ntt_plan_t plan, int step, int rank, int world, const void* d_in, void* d_out,
+                          void* stream);
+
 /* polymul.pointwise_mul -- polymul.py:45-49: c[i] = a[i]*b[i] mod p over
  * `count` residues (device pointers, plan's field/word). */
 int ntt_pointwise_mul(ntt_plan_t plan, const void* d_a, const void* d_b, void* d_c,

@@ -40,7 +40,7 @@ NTT_FLAG_SCALE = 1
 EXPORTS = (
     "ntt_field_check", "ntt_find_primitive_root", "ntt_root_of_unity", "ntt_table_build",
     "ntt_plan_create", "ntt_plan_destroy", "ntt_plan_info", "ntt_exec", "ntt_exec_host",
-    "ntt_plan_workspace_bytes", "ntt_pointwise_mul", "ntt_counters_enable", "ntt_counters_read",
+    "ntt_plan_workspace_bytes", "ntt_pointwise_mul", "ntt_sixstep_dist_step", "ntt_counters_enable", "ntt_counters_read",
     "ntt_counters_reset", "ntt_last_error", "ntt_abi_version", "ntt_device_count",
 )
 
@@ -95,6 +95,7 @@ def load():
         L.ntt_plan_workspace_bytes.argtypes = [_vp, _u64]
         L.ntt_plan_workspace_bytes.restype = _u64
         L.ntt_pointwise_mul.argtypes = [_vp, _vp, _vp, _vp, _u64, _vp]
+        L.ntt_sixstep_dist_step.argtypes = [_vp, _int, _int, _int, _vp, _vp, _vp]
         L.ntt_counters_enable.argtypes = [_int]
         L.ntt_counters_read.argtypes = [ctypes.POINTER(Counters)]
         L.ntt_counters_reset.argtypes = []
@@ -148,6 +149,9 @@ class DevicePlan:
 
     def pointwise(self, a_ptr: int, b_ptr: int, c_ptr: int, count: int, stream: int) -> None:
         check(load().ntt_pointwise_mul(self._h, a_ptr, b_ptr, c_ptr, count, stream))
+
+    def sixstep_dist_step(self, step: int, rank: int, world: int, in_ptr: int, out_ptr: int, stream: int) -> None:
+        check(load().ntt_sixstep_dist_step(self._h, step, rank, world, in_ptr, out_ptr, stream))
 
     def workspace_bytes(self, batch: int) -> int:
         return int(load().ntt_plan_workspace_bytes(self._h, batch))

@@ -134,6 +134,8 @@ template <class A, int L, int B, int b0, int kg, bool DIF>
 NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[16], uint32_t pbase, const typename A::Tw* stw) {
     static_assert(b0 >= B && b0 + kg <= B + 4, "window outside block");
     constexpr int off = b0 - B;
+    // block [0,4): pbase has zero low bits, so k = kc is a compile-time constant
+    // and every w^0 butterfly skips its multiply
 #pragma unroll
     for (int jj = 0; jj < kg; ++jj) {
         const int j = DIF ? kg - 1 - jj : jj;
@@ -145,7 +147,7 @@ NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[16], uint32_t pbase, cons
             if (c & (1 << (off + j))) continue;
             const uint32_t kc = ((uint32_t)c << B) & kmask;      // compile-time part of k
             const int hi = c | (1 << (off + j));
-            if (s == 1) {                                         // w^0 = 1
+            if (s == 1 || (B == 0 && kc == 0)) {                  // w^0 = 1
                 if (DIF) ar.dif1(v[c], v[hi]); else ar.dit1(v[c], v[hi]);
             } else {
                 const typename A::Tw w = row[kc];
@@ -178,7 +180,7 @@ NTT_D void pease_regs(const A& ar, typename A::T (&v)[16], uint32_t ubase, const
                 const uint32_t R = 2u * i;
                 const uint32_t Bp = R >> (kg - m);               // output bits so far (m bits)
                 T x = v[n * (1 << kg) + 2 * i], y = v[n * (1 << kg) + 2 * i + 1];
-                if (s == 1) ar.dit1(x, y);
+                if (s == 1 || (sg == 0 && Bp == 0)) ar.dit1(x, y);     // w^0 (k = Bp when sg == 0)
                 else ar.dit(x, y, stw[(1u << (s - 1)) + ((Bp << sg) | qtop)]);
                 nv[i] = x;
                 nv[i + H] = y;
@@ -210,7 +212,7 @@ NTT_D void stockham_regs(const A& ar, typename A::T (&v)[16], uint32_t hi, const
             for (int i = 0; i < H; ++i) {
                 const uint32_t Bv = i & ((1u << m) - 1), crest = (uint32_t)i >> m;
                 T a = v[(i << (4 - kg)) | x], b = v[((i + H) << (4 - kg)) | x];
-                if (s == 0) ar.dit1(a, b);
+                if (s == 0 || (sg == 0 && Bv == 0)) ar.dit1(a, b);     // w^0 (j = Bv when sg == 0)
                 else ar.dit(a, b, stw[(1u << s) + ((Bv << sg) | hi)]);
                 nv[(crest << (m + 1)) | Bv] = a;
                 nv[(crest << (m + 1)) | (1u << m) | Bv] = b;

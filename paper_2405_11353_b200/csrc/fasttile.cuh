@@ -59,7 +59,10 @@ struct TileArgs {
     const Tw* tw_lo;           // w^j, j < 2^th          (the plan's main table prefix)
     const Tw* tw_hi;           // w^(j*2^th), j < 2^(L-th)
     int th;
-    int l1, l2;                // six-step split
+    int l1, l2;                // six-step: gather stride bits (A: local columns n1/G), row bits (B)
+    int qoff;                  // six-step A: global index of local column 0 (distributed: rank*n1/G)
+    int pb;                    // six-step A: log2 of the row slice per destination (n2/G); = l2 when G = 1
+    uint64_t pblk;             // six-step A: elements per destination block (n1/G * n2/G)
     const T* cor_lo;
     const T* cor_hi;
     int cor_lb;
@@ -82,7 +85,8 @@ NTT_D uint64_t t_gpos_in(const TileArgs<A>& a, uint32_t Q, uint32_t x) {
 
 template <class A, int V, int K, int LAY>
 NTT_D uint64_t t_gpos_out(const TileArgs<A>& a, uint32_t Q, uint32_t x) {
-    if (LAY == TL_SIX_A) return ((uint64_t)Q << a.l2) | x;
+    if (LAY == TL_SIX_A)      // packed for the all-to-all: [dest h][i_local][k2 mod n2/G]
+        return (uint64_t)(x >> a.pb) * a.pblk + ((uint64_t)Q << a.pb) + (x & ((1u << a.pb) - 1));
     if (LAY == TL_SIX_B) return ((uint64_t)x << a.l2) | Q;
     const int L = a.L, S0 = a.S0;
     uint64_t g;
@@ -461,7 +465,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
             if (TWB && a.twist == 3) v = twistv(v, t, x);
             T r = ar.fin(v);
             if (LAY == TL_SIX_A) {
-                const uint64_t e = ((uint64_t)Qs[t] * x) & (N - 1);
+                const uint64_t e = ((uint64_t)(Qs[t] + a.qoff) * x) & (N - 1);
                 const T w = ar.mulfull(__ldg(a.cor_hi + (e >> a.cor_lb)), __ldg(a.cor_lo + (e & ((1ull << a.cor_lb) - 1))));
                 r = ar.mulfull(r, w);
             }

@@ -14,12 +14,33 @@ cudaError_t tile_passes_gold(int variant, const MultipassReq& r, bool* ok) {
         default: *ok = false; return cudaSuccess;
     }
 }
+template <int K1, int K2>
+static bool six_match(const MultipassReq& r) {
+    return r.n1 == (1ull << K1) && r.n2 == (1ull << K2);
+}
 cudaError_t tile_sixstep_gold(const MultipassReq& r, bool* ok) {
+    using A = Canon<FGold>;
     *ok = false;
-    if (r.n1 == (1ull << 13) && r.n2 == (1ull << 13) && r.stw1 && r.stw2 && r.cor_lo) {
-        *ok = true;
-        return ftile::run_sixstep_tiles_k<Canon<FGold>, 13, 13>(r);
-    }
+    if (!r.stw1 || !r.stw2 || !r.cor_lo) return cudaSuccess;
+    *ok = true;
+    if (six_match<13, 13>(r)) return ftile::run_sixstep_tiles_k<A, 13, 13>(r);
+    if (six_match<7, 7>(r)) return ftile::run_sixstep_tiles_k<A, 7, 7>(r);
+    *ok = false;
+    return cudaSuccess;
+}
+cudaError_t tile_sixstep_dist_gold(const MultipassReq& r, int step, int rank, int world, const void* in, void* out,
+                                   bool* ok) {
+    using A = Canon<FGold>;
+    *ok = false;
+    if (!r.stw1 || !r.stw2 || !r.cor_lo) return cudaSuccess;
+    *ok = true;
+    if (six_match<13, 13>(r))
+        return step == 0 ? ftile::sixstep_step_a<A, 13, 13>(r, rank, world, in, out)
+                         : ftile::sixstep_step_b<A, 13, 13>(r, world, in, out);
+    if (six_match<7, 7>(r))
+        return step == 0 ? ftile::sixstep_step_a<A, 7, 7>(r, rank, world, in, out)
+                         : ftile::sixstep_step_b<A, 7, 7>(r, world, in, out);
+    *ok = false;
     return cudaSuccess;
 }
 }  // namespace nttb200

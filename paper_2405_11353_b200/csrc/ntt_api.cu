@@ -540,6 +540,40 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     return st;
 }
 
+int ntt_sixstep_dist_step(ntt_plan_t plan, int step, int rank, int world, const void* d_in, void* d_out,
+                          void* stream) {
+    if (!plan) return fail(NTT_E_INVALID, "NULL plan");
+    if (plan->variant != NTT_SIXSTEP) return fail(NTT_E_BAD_FACTORIZATION, "plan is not a six-step plan");
+    if (step != 0 && step != 1) return fail(NTT_E_INVALID, "step must be 0 (A) or 1 (B)");
+    if (world < 1 || (world & (world - 1)) || (uint64_t)world > plan->n1 || (uint64_t)world > plan->n2 ||
+        rank < 0 || rank >= world)
+        return fail(NTT_E_INVALID, "world must be a power of two dividing n1 and n2; 0 <= rank < world");
+    if (!d_in || !d_out) return fail(NTT_E_INVALID, "NULL buffer");
+    if (plan->kind != 2)
+        return fail(NTT_E_SIZE_NOT_SUPPORTED, "distributed four-step is implemented for the Goldilocks field");
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != plan->device) cudaSetDevice(plan->device);
+    int launches = 0;
+    MultipassReq r{};
+    r.variant = plan->variant; r.L = plan->L; r.batch = 1; r.p = plan->p;
+    r.n1 = plan->n1; r.n2 = plan->n2;
+    r.tw1 = plan->table1 ? plan->table1->tw : nullptr;
+    r.tw2 = plan->table2 ? plan->table2->tw : nullptr;
+    r.stw1 = plan->table1 ? plan->table1->stw : nullptr;
+    r.stw2 = plan->table2 ? plan->table2->stw : nullptr;
+    r.cor_lo = plan->cor_lo; r.cor_hi = plan->cor_hi; r.cor_lb = plan->cor_lb;
+    r.counters = dev_counters(plan->device);
+    r.stream = static_cast<cudaStream_t>(stream); r.num_sms = plan->num_sms; r.launches = &launches;
+    bool ok = false;
+    cudaError_t e = tile_sixstep_dist_gold(r, step, rank, world, d_in, d_out, &ok);
+    g_launches += launches;
+    if (cur != plan->device) cudaSetDevice(cur);
+    if (e != cudaSuccess) return cuda_fail(e, "distributed six-step");
+    if (!ok) return fail(NTT_E_SIZE_NOT_SUPPORTED, "no compiled tile shape for this (n1, n2) split");
+    return NTT_OK;
+}
+
 int ntt_pointwise_mul(ntt_plan_t plan, const void* d_a, const void* d_b, void* d_c, uint64_t count, void* stream) {
     if (!plan) return fail(NTT_E_INVALID, "NULL plan");
     int launches = 0;

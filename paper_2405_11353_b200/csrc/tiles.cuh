@@ -208,46 +208,67 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
     return cudaSuccess;
 }
 
-// Six-step with 2^13 x 2^13 Goldilocks sub-transforms (config 5 shape) and
-// any split whose sub-sizes have a compiled tile shape.
+// Six-step split by tile kernels (Goldilocks; algorithms.py:355-389), also
+// the rank-local steps of the distributed four-step: rank g of G owns input
+// columns i in [g*n1/G, (g+1)*n1/G) as a slab x_local[j][i_local] and, after
+// the all-to-all, output columns k2 in [g*n2/G, ...) as out_local[k1][k2_local].
+template <int K>
+constexpr int six_tq() { return K >= 10 ? 2 : 4; }
+template <int K>
+constexpr int six_nt() { return (six_tq<K>() << (K - 4)) < 512 ? (six_tq<K>() << (K - 4)) : 512; }
+
+template <class A, int K1, int K2>
+cudaError_t sixstep_step_a(const MultipassReq& r, int rank, int world, const void* in, void* out) {
+    using T = typename A::T;
+    int lg = 0;
+    while ((1 << lg) < world) ++lg;
+    TileArgs<A> a = tile_base<A>(r);
+    a.in = static_cast<const T*>(in);
+    a.out = static_cast<T*>(out);
+    a.l1 = K1 - lg;                     // local columns n1/G
+    a.l2 = K2;
+    a.pb = K2 - lg;                     // n2/G per destination
+    a.pblk = 1ull << (K1 - lg + K2 - lg);
+    a.qoff = (uint32_t)rank << (K1 - lg);
+    a.S0 = 0;
+    a.gstw = static_cast<const typename A::Tw*>(r.stw2);
+    a.smb = K2;
+    a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_C_FAST;
+    a.rev_local = 1;                    // bit_reverse_permute(row) (algorithms.py:374)
+    a.vec_in = 0;
+    a.vec_out = aligned16(out) && lg == 0;
+    a.cor_lo = static_cast<const T*>(r.cor_lo);
+    a.cor_hi = static_cast<const T*>(r.cor_hi);
+    a.cor_lb = r.cor_lb;
+    return launch_tile<A, V_DIT, K2, six_tq<K2>(), six_nt<K2>(), TL_SIX_A, K2>(a, r.stream, r.num_sms, r.launches);
+}
+
+template <class A, int K1, int K2>
+cudaError_t sixstep_step_b(const MultipassReq& r, int world, const void* in, void* out) {
+    using T = typename A::T;
+    int lg = 0;
+    while ((1 << lg) < world) ++lg;
+    TileArgs<A> a = tile_base<A>(r);
+    a.in = static_cast<const T*>(in);
+    a.out = static_cast<T*>(out);
+    a.l1 = K1;
+    a.l2 = K2 - lg;                     // rows of n2/G columns
+    a.S0 = 0;
+    a.gstw = static_cast<const typename A::Tw*>(r.stw1);
+    a.smb = K1;
+    a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_T_FAST;
+    a.rev_local = 1;                    // bit_reverse_permute(col) (algorithms.py:385)
+    a.vec_in = a.vec_out = 0;
+    a.count_row = 1;
+    a.scale = r.scale;
+    return launch_tile<A, V_DIT, K1, six_tq<K1>(), six_nt<K1>(), TL_SIX_B, K1>(a, r.stream, r.num_sms, r.launches);
+}
+
 template <class A, int K1, int K2>
 cudaError_t run_sixstep_tiles_k(const MultipassReq& r) {
-    using T = typename A::T;
-    T* rows = static_cast<T*>(r.ws);
-    const bool al = aligned16(r.in) && aligned16(r.out) && aligned16(r.ws);
-    cudaError_t e;
-    {
-        TileArgs<A> a = tile_base<A>(r);
-        a.in = static_cast<const T*>(r.in);
-        a.out = rows;
-        a.l1 = K1; a.l2 = K2; a.S0 = 0;
-        a.gstw = static_cast<const typename A::Tw*>(r.stw2);
-        a.smb = K2;
-        a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_C_FAST;
-        a.rev_local = 1;                                // bit_reverse_permute(row) (algorithms.py:374)
-        a.vec_in = 0;                                   // runs of TQ=2 residues (16 B): scalar gather
-        a.vec_out = al;
-        a.cor_lo = static_cast<const T*>(r.cor_lo);
-        a.cor_hi = static_cast<const T*>(r.cor_hi);
-        a.cor_lb = r.cor_lb;
-        e = launch_tile<A, V_DIT, K2, 2, 512, TL_SIX_A, K2>(a, r.stream, r.num_sms, r.launches);
-        if (e != cudaSuccess) return e;
-    }
-    {
-        TileArgs<A> a = tile_base<A>(r);
-        a.in = rows;
-        a.out = static_cast<T*>(r.out);
-        a.l1 = K1; a.l2 = K2; a.S0 = 0;
-        a.gstw = static_cast<const typename A::Tw*>(r.stw1);
-        a.smb = K1;
-        a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_T_FAST;
-        a.rev_local = 1;                                // bit_reverse_permute(col) (algorithms.py:385)
-        a.vec_in = a.vec_out = 0;
-        a.count_row = 1;
-        a.scale = r.scale;
-        e = launch_tile<A, V_DIT, K1, 2, 512, TL_SIX_B, K1>(a, r.stream, r.num_sms, r.launches);
-    }
-    return e;
+    cudaError_t e = sixstep_step_a<A, K1, K2>(r, 0, 1, r.in, r.ws);
+    if (e != cudaSuccess) return e;
+    return sixstep_step_b<A, K1, K2>(r, 1, r.ws, r.out);
 }
 
 }  // namespace ftile
@@ -256,5 +277,8 @@ cudaError_t run_sixstep_tiles_k(const MultipassReq& r) {
 cudaError_t tile_passes_f32(int variant, bool lazy, const MultipassReq& r, bool* ok);
 cudaError_t tile_passes_gold(int variant, const MultipassReq& r, bool* ok);
 cudaError_t tile_sixstep_gold(const MultipassReq& r, bool* ok);
+// distributed four-step, rank-local steps (step = 0: A, 1: B)
+cudaError_t tile_sixstep_dist_gold(const MultipassReq& r, int step, int rank, int world, const void* in, void* out,
+                                   bool* ok);
 
 }  // namespace nttb200

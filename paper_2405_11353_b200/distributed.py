@@ -1,0 +1,115 @@
+"""Multi-GPU execution.
+
+* Batches (independent polynomials) shard by rows with NO collective:
+  :func:`shard_rows` gives each rank its contiguous row block; every rank runs
+  the ordinary batched transform on its own GPU.
+* One giant transform (config 5: 2^26 Goldilocks) is split four-step across
+  ranks with exactly ONE exchange: :class:`DistributedSixStep`.  The reference's
+  six-step indexing (algorithms.py:355-389) is kept: the input is the n2 x n1
+  matrix X[j][i] = x[j*n1 + i]; rank g owns the column slab i in
+  [g*n1/G, (g+1)*n1/G) as ``x_local[j][i_local]``, runs the size-n2 DITs of its
+  columns and the correction twiddles w^(i*k2) (step A, the pack for the
+  all-to-all fused into the kernel's store), then ONE equal-split
+  ``all_to_all_single`` (NCCL over NVLink) moves block [g -> h] = rows of rank g,
+  columns k2 of rank h; step B runs the size-n1 DITs and leaves
+  ``out_local[k1][k2_local]`` = out[k1*n2 + k2] for k2 in rank g's column slab.
+
+The rank-local steps are ``ntt_sixstep_dist_step`` of the C ABI; they are
+injectable (``step_fns``) so the orchestration itself -- slab layout, pack
+layout, exchange, unpack -- is tested on CPU ranks with the gloo backend.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .algorithms import device_plan_for, make_plan
+from .twiddle import FORWARD
+
+try:
+    import torch
+    import torch.distributed as dist
+except Exception:  # pragma: no cover
+    torch = None
+    dist = None
+
+
+def shard_rows(batch: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous row block [lo, hi) of rank `rank` (no collective needed)."""
+    lo = batch * rank // world
+    hi = batch * (rank + 1) // world
+    return lo, hi
+
+
+def column_slab(x: np.ndarray, rank: int, world: int, n1: int, n2: int) -> np.ndarray:
+    """Rank's input slab x_local[j][i_local] = x[j*n1 + rank*n1/G + i_local]."""
+    c = n1 // world
+    return np.ascontiguousarray(x.reshape(n2, n1)[:, rank * c:(rank + 1) * c])
+
+
+def assemble_output(out_locals, n1: int, n2: int) -> np.ndarray:
+    """Inverse of the output distribution: out[k1*n2 + k2] from every rank's slab."""
+    return np.ascontiguousarray(np.concatenate([np.asarray(o).reshape(n1, -1) for o in out_locals], axis=1)).reshape(-1)
+
+
+class DistributedSixStep:
+    """Four-step of ONE transform across the ranks of a process group."""
+
+    def __init__(self, params, n: int, direction: str = FORWARD, n1: int | None = None, n2: int | None = None,
+                 group=None, step_fns=None, device: int | None = None):
+        if dist is None or not dist.is_initialized():
+            raise RuntimeError("torch.distributed must be initialised (one process per GPU)")
+        self.plan = make_plan(params, "sixstep", n, direction, n1, n2)
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n1, self.n2, self.n = self.plan.n1, self.plan.n2, n
+        G = self.world
+        if G & (G - 1) or self.n1 % G or self.n2 % G:
+            raise ValueError("world size must be a power of two dividing n1 and n2")
+        self.cols = self.n1 // G              # input columns per rank
+        self.kcols = self.n2 // G             # output columns per rank
+        self.block = self.cols * self.kcols   # residues per peer in the all-to-all
+        self.word = 4 if params.p < (1 << 32) else 8
+        if step_fns is None:
+            dev = torch.cuda.current_device() if device is None else device
+            self._dp = device_plan_for(self.plan, self.word, dev)
+            self.step_a, self.step_b = self._gpu_step_a, self._gpu_step_b
+        else:
+            self.step_a, self.step_b = step_fns
+
+    # ---- default: the B200 kernels through the C ABI
+    def _gpu_step_a(self, x_local, send, rank, world):
+        self._dp.sixstep_dist_step(0, rank, world, x_local.data_ptr(), send.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream)
+
+    def _gpu_step_b(self, recv, out_local, rank, world):
+        self._dp.sixstep_dist_step(1, rank, world, recv.data_ptr(), out_local.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream)
+
+    def local_input_shape(self) -> tuple[int, int]:
+        return (self.n2, self.cols)
+
+    def run(self, x_local, timings: dict | None = None):
+        """x_local: this rank's slab [n2, n1/G] (device tensor for the GPU
+        path).  Returns out_local [n1, n2/G]."""
+        if tuple(x_local.shape) != (self.n2, self.cols):
+            raise ValueError(f"local slab must be {(self.n2, self.cols)}, got {tuple(x_local.shape)}")
+        send = torch.empty(self.world * self.block, dtype=x_local.dtype, device=x_local.device)
+        recv = torch.empty_like(send)
+        out_local = torch.empty((self.n1, self.kcols), dtype=x_local.dtype, device=x_local.device)
+        self.step_a(x_local, send, self.rank, self.world)
+        # ONE exchange: block h of `send` goes to rank h (equal splits)
+        self._exchange(recv, send)
+        self.step_b(recv, out_local, self.rank, self.world)
+        return out_local
+
+    def _exchange(self, recv, send):
+        if self.world == 1:
+            recv.copy_(send)
+            return
+        # NCCL has no uint64 all-to-all dtype in torch: move the raw bytes
+        view = {torch.uint64: torch.int64, torch.uint32: torch.int32}.get(send.dtype)
+        s = send.view(view) if view is not None else send
+        r = recv.view(view) if view is not None else recv
+        dist.all_to_all_single(r, s, group=self.group)

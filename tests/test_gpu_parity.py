@@ -278,3 +278,48 @@ def test_pointwise_mul():
     dp.pointwise(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), 1024, torch.cuda.current_stream().cuda_stream)
     want = [(int(u) * int(v)) % GOLD for u, v in zip(a[0], b[0])]
     assert to_host(tc)[0].tolist() == want
+
+
+def _emulate_distributed(x, p, g, n, n1, world):
+    """Run the rank-local steps of the distributed four-step for every rank on
+    ONE device through the C ABI, with the all-to-all done as a local block
+    permutation (never launching mutually-waiting ranks on one GPU)."""
+    from paper_2405_11353_b200.distributed import assemble_output, column_slab
+    n2 = n // n1
+    params = P.FieldParams(p, g, 64)
+    plan = P.make_plan(params, "sixstep", n, n1=n1)
+    dp = P.algorithms.device_plan_for(plan, 8, 0)
+    c, r = n1 // world, n2 // world
+    block = c * r
+    s = torch.cuda.current_stream().cuda_stream
+    sends = []
+    for rank in range(world):
+        slab = to_dev(column_slab(x, rank, world, n1, n2))
+        send = torch.empty(world * block, dtype=torch.uint64, device=dev())
+        dp.sixstep_dist_step(0, rank, world, slab.data_ptr(), send.data_ptr(), s)
+        sends.append(send)
+    outs = []
+    for rank in range(world):
+        recv = torch.cat([sends[src][rank * block:(rank + 1) * block] for src in range(world)])
+        out = torch.empty(n1 * r, dtype=torch.uint64, device=dev())
+        dp.sixstep_dist_step(1, rank, world, recv.data_ptr(), out.data_ptr(), s)
+        outs.append(to_host(out))
+    return assemble_output(outs, n1, n2)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_distributed_sixstep_emulated_small(world):
+    n, n1 = 1 << 14, 1 << 7
+    x = rand(GOLD, 1, 14, np.uint64, 55)[0]
+    got = _emulate_distributed(x, GOLD, 7, n, n1, world)
+    assert np.array_equal(got, O.ntt(x, GOLD, 7, 64, "sixstep", n1=n1))
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_distributed_sixstep_emulated_config5(world):
+    """Config 5 (2^26 Goldilocks, 2^13 x 2^13) split over `world` ranks:
+    output hash equals the reference's."""
+    w = CONFIGS[5]
+    x = seeded_input(w)[0]
+    got = _emulate_distributed(x, w.p, w.g, w.n, w.n1, world)
+    assert O.sha256_le(got) == GOLDEN[5][1]
