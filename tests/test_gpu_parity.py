@@ -323,3 +323,50 @@ def test_distributed_sixstep_emulated_config5(world):
     x = seeded_input(w)[0]
     got = _emulate_distributed(x, w.p, w.g, w.n, w.n1, world)
     assert O.sha256_le(got) == GOLDEN[5][1]
+
+
+@pytest.mark.parametrize("variant", VARIANTS7)
+def test_cyclic_mul_ntt_vs_schoolbook(variant):
+    """Convolution theorem (test_polymul.py:46-53) on the device, 32- and 64-bit fields."""
+    for p, g, w, L in ((998244353, 3, 32, 8), (3221225473, 5, 32, 5), (GOLD, 7, 64, 6)):
+        params = P.FieldParams(p, g, w)
+        rng = np.random.default_rng(L)
+        a = [int(v) for v in rng.integers(0, p, size=1 << L, dtype=np.uint64)]
+        b = [int(v) for v in rng.integers(0, p, size=1 << L, dtype=np.uint64)]
+        assert P.cyclic_mul_ntt(a, b, params, variant) == P.schoolbook_cyclic(a, b, p)
+    # batched device operands: every row multiplied in one set of launches
+    params = P.FieldParams(998244353, 3)
+    A = rand(998244353, 8, 10, np.uint32, 1)
+    B = rand(998244353, 8, 10, np.uint32, 2)
+    C = to_host(P.cyclic_mul_ntt(to_dev(A), to_dev(B), params, variant))
+    for r in (0, 7):
+        assert C[r].tolist() == P.schoolbook_cyclic(A[r].tolist(), B[r].tolist(), 998244353)
+
+
+def test_estimator_batched_device_path():
+    from sklearn.pipeline import Pipeline
+    from paper_2405_11353_b200.estimator import NttTransform
+    X = rand(998244353, 64, 10, np.uint32, 3).astype(np.int64)
+    for v in ("dit", "pease_nc", "stockham", "sixstep"):
+        t = NttTransform(variant=v, prime=998244353).fit(X)
+        Y = t.transform(X)
+        assert np.array_equal(Y.astype(np.uint64), O.ntt(X.astype(np.uint64), 998244353, 3, 32, "dit"))
+        assert np.array_equal(t.inverse_transform(Y), X)
+    pipe = Pipeline([("ntt", NttTransform(variant="dif", prime=998244353))])
+    assert pipe.fit_transform(X).shape == X.shape
+    Xg = rand(GOLD, 4, 8, np.uint64, 4)
+    tg = NttTransform(variant="dif", prime=GOLD).fit(Xg)
+    assert np.array_equal(tg.transform(Xg), O.ntt(Xg, GOLD, 7, 64, "dif"))
+    assert np.array_equal(tg.inverse_transform(tg.transform(Xg)), Xg)
+
+
+def test_cli_verify_and_bench(tmp_path):
+    from paper_2405_11353_b200 import cli
+    assert cli.main(["verify", "--max-log", "6", "--prime", "998244353", "--vectors", "2"]) == 0
+    assert cli.main(["verify", "--max-log", "5", "--vectors", "2"]) == 0        # reference DEFAULT_PRIME
+    out = tmp_path / "b.csv"
+    assert cli.main(["bench", "--algo", "pease_nc", "--size", "1024", "--reps", "2", "--batch", "64",
+                     "--prime", "998244353", "--csv", str(out)]) == 0
+    rows = out.read_text().splitlines()
+    assert rows[0].startswith("algo,n,prime,reps,mean_ns,median_ns,min_ns,checksum")
+    assert rows[1].split(",")[7] == "467606314"       # cli.py bench known answer

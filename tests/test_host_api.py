@@ -168,3 +168,40 @@ def test_table_build_native_equals_python_definition():
         assert t.w_pow == wp
         assert t.w_shoup == [(v << w) // p for v in wp]
         assert t.n_inv == pow(n, p - 2, p)
+
+
+def test_schoolbook_and_host_polymul_helpers():
+    # test_polymul.py:14-18 examples (re-parametrised), exact for 64-bit p too
+    assert P.schoolbook_cyclic([1, 2, 0, 0], [3, 4, 0, 0], 17) == [3, 10, 8, 0]
+    assert P.schoolbook_cyclic([0, 0, 0, 1], [0, 1, 0, 0], 17) == [1, 0, 0, 0]
+    a, b = [GOLD - 1, 2, 3, 4], [GOLD - 2, 5, 0, 7]
+    want = [sum(a[i] * b[(k - i) % 4] for i in range(4)) % GOLD for k in range(4)]
+    assert P.schoolbook_cyclic(a, b, GOLD) == want
+    assert P.pointwise_mul([3, 4], [5, 6], 17) == [15, 7]
+    with pytest.raises(P.SizeMismatch):
+        P.schoolbook_cyclic([1, 2], [1], 17)
+
+
+def test_estimator_validation_without_device():
+    from paper_2405_11353_b200.estimator import NttTransform
+    est = NttTransform(variant="bogus")
+    with pytest.raises(P.UnsupportedVariant):
+        est.fit(np.zeros((2, 8), np.int64))
+    with pytest.raises(ValueError):
+        NttTransform().fit(np.zeros((2, 6), np.int64))
+    with pytest.raises(ValueError):
+        NttTransform().fit(-np.ones((2, 8), np.int64))
+    with pytest.raises(ValueError):
+        NttTransform(prime=17).fit(np.full((2, 8), 17, np.int64))
+    t = NttTransform(prime=998244353).fit(np.zeros((3, 16), np.int64))
+    assert t.n_features_in_ == 16 and t.params_.g == 3
+    tg = NttTransform(prime=GOLD).fit(np.zeros((1, 8), np.uint64))
+    assert tg.params_.w == 64
+    from sklearn.base import clone
+    assert clone(t).get_params() == {"variant": "dit", "prime": 998244353, "generator": None}
+
+
+def test_cli_usage_errors():
+    from paper_2405_11353_b200 import cli
+    assert cli.main(["nonsense"]) == 2
+    assert cli.bench_input(1024, 998244353, 42)[:2] == cli.bench_input(1024, 998244353, 42)[:2]
