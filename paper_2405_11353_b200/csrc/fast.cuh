@@ -232,7 +232,12 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
     constexpr int N = GG::N, TT = GG::TT, G = GG::G, K0 = GG::K0;
     constexpr int CW = lane_bits<T>();
     constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);   // permuting groups
-    constexpr int NBUF = PP ? 3 : 2;       // staging + work (+ second work for ping-pong)
+    // Pease keeps two work buffers + the copy-back (algorithms.py:242); Pease_nc
+    // and Stockham swap "buffers" through the registers: every thread holds its
+    // whole sub-network, so after a team barrier the group writes the same
+    // buffer (no copy, one buffer less => one more team per CTA)
+    constexpr bool TWO = (V == V_PEASE);
+    constexpr int NBUF = TWO ? 3 : 2;      // staging + work (+ second work buffer for Pease)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint64_t mbar[TEAMS];
 
@@ -242,7 +247,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
     constexpr int NP = padded_len<T, L>();
     T* S = reinterpret_cast<T*>(smem_raw + (size_t)N * sizeof(Tw)) + (size_t)team * (N + (NBUF - 1) * NP);
     T* W0 = S + N;
-    T* W1 = PP ? W0 + NP : W0;
+    T* W1 = TWO ? W0 + NP : W0;
     A ar;
     ar.init(a.p);
 
@@ -374,6 +379,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                     else { NTT_PE(1, 4) NTT_PE(2, 4) NTT_PE(3, 4) NTT_PE(4, 4) NTT_PE(5, 4) NTT_PE(6, 4)
                            NTT_PE(7, 4) NTT_PE(8, 4) NTT_PE(9, 4) }
 #undef NTT_PE
+                    if (!TWO && !first && !last) team_sync(bar_id, TT);   // all reads of W0 done
                     // outputs: network n = (u << (4-kg)) | n writes q | R << (L-kg)
                     T* db = dst + padpos<T>(u << (4 - kg));
 #pragma unroll
@@ -414,6 +420,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                     else { NTT_ST(1, 4) NTT_ST(2, 4) NTT_ST(3, 4) NTT_ST(4, 4) NTT_ST(5, 4) NTT_ST(6, 4)
                            NTT_ST(7, 4) NTT_ST(8, 4) NTT_ST(9, 4) }
 #undef NTT_ST
+                    if (!TWO && !first && !last) team_sync(bar_id, TT);   // all reads of W0 done
                     T* db = dst + padpos<T>((hi << lob) | lo);
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
@@ -433,9 +440,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                         for (int i = t; i < NP; i += TT) src[i] = dst[i];
                         ++copies;
                         team_sync(bar_id, TT);
-                    } else {
-                        T* tmp = src; src = dst; dst = tmp;
-                    }
+                    }                         // Pease_nc / Stockham: roles swap in place
                 }
             }
         }
@@ -451,7 +456,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
 
 // ------------------------------------------------------------- launcher --
 #ifndef NTT_FAST_MAX_THREADS
-#define NTT_FAST_MAX_THREADS 768
+#define NTT_FAST_MAX_THREADS 1024
 #endif
 constexpr int kFastMaxThreads = NTT_FAST_MAX_THREADS;
 
@@ -461,7 +466,7 @@ struct FastCfg {
     using Tw = typename A::Tw;
     static constexpr int N = 1 << L;
     static constexpr int TT = 1 << (L - 4);
-    static constexpr int NBUF = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM) ? 3 : 2;
+    static constexpr int NBUF = (V == V_PEASE) ? 3 : 2;
     static constexpr long kSmemCap = 227 * 1024 - 1024;
     static constexpr long table = (long)N * sizeof(Tw);
     static constexpr long team_bytes = ((long)N + (long)(NBUF - 1) * padded_len<T, L>()) * sizeof(T);

@@ -59,6 +59,7 @@ struct TileArgs {
     const Tw* tw_lo;           // w^j, j < 2^th          (the plan's main table prefix)
     const Tw* tw_hi;           // w^(j*2^th), j < 2^(L-th)
     int th;
+    int diag;                  // diagnostics only: 1 = skip the register groups, 2 = skip gather+scatter
     int l1, l2;                // six-step: gather stride bits (A: local columns n1/G), row bits (B)
     int qoff;                  // six-step A: global index of local column 0 (distributed: rank*n1/G)
     int pb;                    // six-step A: log2 of the row slice per destination (n2/G); = l2 when G = 1
@@ -253,6 +254,8 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint32_t Qs[TQ];
     __shared__ uint64_t Rb[TQ];
+    // every layout is additive over disjoint bits: gpos(Q, x) = gpos(Q, 0) + gpos(0, x)
+    __shared__ uint64_t Gin[TQ], Gout[TQ];
     Tw* tws = reinterpret_cast<Tw*>(smem_raw);
     // per-tile twist tables (only when a.twist): network t, j < 32:
     //   twl[t][j] = w^(Q_t * j), twh[t][j] = w^(Q_t * 32 * j)  (rows padded to 33)
@@ -302,6 +305,8 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
             }
             Qs[t] = Q;
             Rb[t] = row * N;
+            Gin[t] = row * N + t_gpos_in<A, V, K, LAY>(a, Q, 0);
+            Gout[t] = row * N + t_gpos_out<A, V, K, LAY>(a, Q, 0);
         }
         __syncthreads();
         if (TWB && a.twist) {                 // per-network twist tables from the main table w^i
@@ -314,11 +319,13 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
             __syncthreads();
         }
         // ---- gather (16-byte vectors along the contiguous run when valid)
-        if (a.vec_in && a.in_order == TO_T_FAST) {
+        if (a.diag == 2) {
+        } else if (a.vec_in && a.in_order == TO_T_FAST) {
+            const uint64_t gb = Gin[(threadIdx.x % (TQ / VE)) * VE];
 #pragma unroll 4
             for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
                 const uint32_t t0 = (i % (TQ / VE)) * VE, x = i / (TQ / VE);
-                const T* src = a.in + Rb[t0] + t_gpos_in<A, V, K, LAY>(a, Qs[t0], x);
+                const T* src = a.in + gb + t_gpos_in<A, V, K, LAY>(a, 0u, x);
                 T tmp[VE];
                 *reinterpret_cast<uint4*>(tmp) = __ldg(reinterpret_cast<const uint4*>(src));
 #pragma unroll
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
 #pragma unroll 4
             for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
                 const uint32_t t = i / ((1u << K) / VE), x0 = (i % ((1u << K) / VE)) * VE;
-                const T* src = a.in + Rb[t] + t_gpos_in<A, V, K, LAY>(a, Qs[t], x0);
+                const T* src = a.in + Gin[t] + t_gpos_in<A, V, K, LAY>(a, 0u, x0);
                 T tmp[VE];
                 *reinterpret_cast<uint4*>(tmp) = __ldg(reinterpret_cast<const uint4*>(src));
 #pragma unroll
@@ -349,7 +356,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
                 if (a.in_order == TO_C_FAST) { t = i >> K; x = i & ((1u << K) - 1); }
                 else if (a.in_order == TO_T_FAST) { t = i % TQ; x = i / TQ; }
                 else { const int lb = LTQ - a.la; const uint32_t tb = i & ((1u << lb) - 1), ta = (i >> lb) & (a.TA - 1); t = ta + (tb << a.la); x = i / TQ; }
-                T v = __ldg(a.in + Rb[t] + t_gpos_in<A, V, K, LAY>(a, Qs[t], x));
+                T v = __ldg(a.in + Gin[t] + t_gpos_in<A, V, K, LAY>(a, 0u, x));
                 if (TWB && a.twist && a.twist < 3) v = twistv(v, t, a.rev_local ? brev(x, K) : x);
                 bufA[t * NP + padpos<T>(a.rev_local ? brev(x, K) : x)] = v;
             }
@@ -361,6 +368,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
         T* dst = bufB;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
+            if (a.diag == 1) break;
             T v[16];
 #pragma unroll
             for (int r = 0; r < REP; ++r) {
@@ -472,22 +480,26 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
             if (a.scale) r = ar.mulc(r, a.ninv);
             return r;
         };
-        if (a.vec_out && a.out_order == TO_T_FAST) {
+        if (a.diag == 2) {
+        } else if (a.vec_out && a.out_order == TO_T_FAST) {
+            const uint64_t gb = Gout[(threadIdx.x % (TQ / VE)) * VE];
+#pragma unroll 4
             for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
                 const uint32_t t0 = (i % (TQ / VE)) * VE, x = i / (TQ / VE);
                 T tmp[VE];
 #pragma unroll
                 for (int e = 0; e < VE; ++e) tmp[e] = finish(t0 + e, x, res[(t0 + e) * NP + padpos<T>(x)]);
-                *reinterpret_cast<uint4*>(a.out + Rb[t0] + t_gpos_out<A, V, K, LAY>(a, Qs[t0], x)) =
+                *reinterpret_cast<uint4*>(a.out + gb + t_gpos_out<A, V, K, LAY>(a, 0u, x)) =
                     *reinterpret_cast<uint4*>(tmp);
             }
         } else if (a.vec_out && a.out_order == TO_C_FAST) {
+#pragma unroll 4
             for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
                 const uint32_t t = i / ((1u << K) / VE), x0 = (i % ((1u << K) / VE)) * VE;
                 T tmp[VE];
 #pragma unroll
                 for (int e = 0; e < VE; ++e) tmp[e] = finish(t, x0 + e, res[t * NP + padpos<T>(x0 + e)]);
-                *reinterpret_cast<uint4*>(a.out + Rb[t] + t_gpos_out<A, V, K, LAY>(a, Qs[t], x0)) =
+                *reinterpret_cast<uint4*>(a.out + Gout[t] + t_gpos_out<A, V, K, LAY>(a, 0u, x0)) =
                     *reinterpret_cast<uint4*>(tmp);
             }
         } else {
@@ -496,7 +508,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
                 if (a.out_order == TO_C_FAST) { t = i >> K; x = i & ((1u << K) - 1); }
                 else if (a.out_order == TO_T_FAST) { t = i % TQ; x = i / TQ; }
                 else { const int lb = LTQ - a.la; const uint32_t tb = i & ((1u << lb) - 1), ta = (i >> lb) & (a.TA - 1); t = ta + (tb << a.la); x = i / TQ; }
-                a.out[Rb[t] + t_gpos_out<A, V, K, LAY>(a, Qs[t], x)] = finish(t, x, res[t * NP + padpos<T>(x)]);
+                a.out[Gout[t] + t_gpos_out<A, V, K, LAY>(a, 0u, x)] = finish(t, x, res[t * NP + padpos<T>(x)]);
             }
         }
         if (a.counters && threadIdx.x == 0 && tile % tiles_per_row == 0) {

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include "fasttile.cuh"
 #include "multipass.cuh"
 
@@ -71,6 +72,12 @@ inline int tile_plan(int L, int word, int* K) {
     return P;
 }
 
+// NTT_TILE_DIAG=1|2: diagnostics (skip compute | skip data movement); never set in production
+inline int tile_diag() {
+    static int d = [] { const char* e = getenv("NTT_TILE_DIAG"); return e ? atoi(e) : 0; }();
+    return d;
+}
+
 template <class A>
 TileArgs<A> tile_base(const MultipassReq& r) {
     TileArgs<A> a{};
@@ -82,6 +89,7 @@ TileArgs<A> tile_base(const MultipassReq& r) {
     a.ninv = make_tw2<typename A::Field>(r.ninv, r.ninv_shoup);
     a.counters = r.counters;
     a.TA = 1;
+    a.diag = tile_diag();
     return a;
 }
 

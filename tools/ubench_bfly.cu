@@ -10,6 +10,32 @@
 
 using namespace nttb200;
 
+// variant of LazyF32 with the two output additions written as 3-input PTX
+// adds (IADD3-able) and the quotient product via mul.wide
+struct LazyF32b : LazyF32 {
+    NTT_D void dit(T& x, T& y, Tw w) const {
+        const T xr = umin32(x, x - p2);
+        const T q = __umulhi(y, w.y);
+        const T t = y * w.x - q * p;
+        uint32_t X, Y;
+        asm("vadd.u32.u32.u32.add %0, %2, %3, %4;\n\t"
+            "sub.u32 %1, %2, %3;\n\t"
+            : "=r"(X), "=r"(Y) : "r"(xr), "r"(t), "r"(0u));
+        x = X;
+        y = Y + p2;
+    }
+};
+struct LazyF32c : LazyF32 {      // q*p folded: t = y*w - q*p via mad with negated p
+    NTT_D void dit(T& x, T& y, Tw w) const {
+        const T xr = umin32(x, x - p2);
+        const T q = __umulhi(y, w.y);
+        T t;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(q), "r"(0u - p), "r"(y * w.x));
+        x = xr + t;
+        y = xr - t + p2;
+    }
+};
+
 template <class A>
 __global__ void k_bfly(typename A::T* out, uint64_t p, int iters, typename A::Tw w0, typename A::Tw w1) {
     using T = typename A::T;
@@ -64,11 +90,10 @@ void run(const char* name, uint64_t p, typename A::Tw w0, typename A::Tw w1, int
 __global__ void k_goldcheck(const uint64_t* a, const uint64_t* b, int n, int* bad) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    FGold f; f.p = FGold::P;
     uint64_t x = a[i], y = b[i];
-    if (FGoldC::mul_c(x, y) != f.mul_full(x, y)) atomicAdd(bad, 1);
-    if (FGoldC::add_c(x, y) != f.add(x, y)) atomicAdd(bad + 1, 1);
-    if (FGoldC::sub_c(x, y) != f.sub(x, y)) atomicAdd(bad + 2, 1);
+    if (FGoldC::mul_c(x, y) != FGold::reduce128(x * y, __umul64hi(x, y))) atomicAdd(bad, 1);
+    { uint64_t s_ = x + y; if (s_ < x) s_ += FGold::EPS; if (FGoldC::add_c(x, y) != FGold::canon(s_)) atomicAdd(bad + 1, 1); }
+    if (FGoldC::sub_c(x, y) != (x < y ? x - y - FGold::EPS : x - y)) atomicAdd(bad + 2, 1);
 }
 void check_gold() {
     const int n = 1 << 22;
@@ -93,6 +118,8 @@ int main() {
     uint2 w1 = make_uint2(5, (uint32_t)(((uint64_t)5 << 32) / p));
     run<LazyF32>("lazy-u32", p, w0, w1, 256);
     run<LazyF32>("lazy-u32", p, w0, w1, 512);
+    run<LazyF32b>("lazy-vadd", p, w0, w1, 256);
+    run<LazyF32c>("lazy-mad", p, w0, w1, 256);
     run<Canon<F32S>>("canon-u32", p, w0, w1, 256);
     const uint64_t G = 0xFFFFFFFF00000001ull;
     run<Canon<FGold>>("goldilocks", G, 7ull, 49ull, 256);
