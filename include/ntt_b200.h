@@ -98,8 +98,11 @@ int ntt_plan_info(ntt_plan_t plan, ntt_plan_info_t* info);
 int ntt_exec(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t batch, unsigned flags,
              void* stream);
 
-/* Same with HOST buffers: H2D copy, transform, D2H copy, synchronise.
- * The path a list[int] / numpy caller takes (end-to-end timing). */
+/* Same with HOST buffers: H2D copy, transform, D2H copy, synchronise (the
+ * path a list[int] / numpy caller takes; `stream` is unused -- the call is
+ * synchronous).  Large batches of shared-memory-resident plans are cut into
+ * chunks pipelined over three internal streams so the copies in both
+ * directions overlap the transforms (use pinned host memory for overlap). */
 int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch, unsigned flags,
                   void* stream);
 

@@ -242,6 +242,7 @@ struct ntt_plan_s {
     uint64_t ws_bytes = 0;
     void* hbuf = nullptr;
     uint64_t hbuf_bytes = 0;
+    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};   // host-exec pipeline streams
     std::mutex mu;
     ~ntt_plan_s() {
         int cur = 0;
@@ -249,6 +250,8 @@ struct ntt_plan_s {
         cudaSetDevice(device);
         if (ws) cudaFree(ws);
         if (hbuf) cudaFree(hbuf);
+        for (auto st : hs)
+            if (st) cudaStreamDestroy(st);
         if (cor_lo) cudaFree(cor_lo);
         if (cor_hi) cudaFree(cor_hi);
         if (twh) cudaFree(twh);
@@ -518,23 +521,41 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     int cur = 0;
     cudaGetDevice(&cur);
     if (cur != plan->device) cudaSetDevice(plan->device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const uint64_t bytes = batch * plan->n * plan->word;
+    const uint64_t row_bytes = plan->n * plan->word;
+    const uint64_t bytes = batch * row_bytes;
     int st = NTT_OK;
     {
         std::lock_guard<std::mutex> lk(plan->mu);
         st = grow(plan->hbuf, plan->hbuf_bytes, bytes);
+        for (auto& hs : plan->hs)
+            if (!st && !hs && cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking) != cudaSuccess)
+                st = fail(NTT_E_CUDA, "stream creation failed");
     }
     cudaError_t e = cudaSuccess;
-    if (!st) {
-        e = cudaMemcpyAsync(plan->hbuf, h_in, bytes, cudaMemcpyHostToDevice, s);
-        if (e != cudaSuccess) st = cuda_fail(e, "H2D copy");
+    // Shared-memory-resident plans need no workspace, so the batch is cut into
+    // chunks pipelined over three streams: H2D of chunk c+1, the transform of c
+    // and the D2H of c-1 overlap (copy engines are full duplex).  Multi-pass
+    // plans share one workspace and run as a single chunk.
+    const bool resident = ntt_plan_workspace_bytes(plan, 1) == 0;
+    uint64_t chunks = 1;
+    if (resident && bytes >= (16ull << 20)) chunks = bytes >= (64ull << 20) ? 8 : 4;
+    if (chunks > batch) chunks = batch;
+    (void)stream;
+    char* d = static_cast<char*>(plan->hbuf);
+    for (uint64_t c = 0; !st && c < chunks; ++c) {
+        const uint64_t r0 = batch * c / chunks, r1 = batch * (c + 1) / chunks;
+        const uint64_t off = r0 * row_bytes, nb = (r1 - r0) * row_bytes;
+        cudaStream_t s = plan->hs[c % 3];
+        e = cudaMemcpyAsync(d + off, static_cast<const char*>(h_in) + off, nb, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) { st = cuda_fail(e, "H2D copy"); break; }
+        st = exec_device(plan, d + off, d + off, r1 - r0, flags, s);
+        if (st) break;
+        e = cudaMemcpyAsync(static_cast<char*>(h_out) + off, d + off, nb, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) { st = cuda_fail(e, "D2H copy"); break; }
     }
-    if (!st) st = exec_device(plan, plan->hbuf, plan->hbuf, batch, flags, s);
-    if (!st) {
-        e = cudaMemcpyAsync(h_out, plan->hbuf, bytes, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) st = cuda_fail(e, "D2H copy");
+    for (auto hs : plan->hs) {
+        cudaError_t e2 = cudaStreamSynchronize(hs);
+        if (!st && e2 != cudaSuccess) st = cuda_fail(e2, "host exec");
     }
     if (cur != plan->device) cudaSetDevice(cur);
     return st;

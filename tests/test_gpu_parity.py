@@ -370,3 +370,19 @@ def test_cli_verify_and_bench(tmp_path):
     rows = out.read_text().splitlines()
     assert rows[0].startswith("algo,n,prime,reps,mean_ns,median_ns,min_ns,checksum")
     assert rows[1].split(",")[7] == "467606314"       # cli.py bench known answer
+
+
+@pytest.mark.parametrize("variant", ["pease_nc", "dit"])
+def test_host_buffer_path_config2(variant):
+    """ntt_exec_host (numpy in / numpy out, chunk-pipelined over three streams)
+    reproduces the reference's config-2 output hash."""
+    w = CONFIGS[2]
+    x = seeded_input(w)
+    params = P.FieldParams(w.p, w.g, w.w)
+    y = P.ntt(x, P.build_table(params, w.n), variant)
+    assert isinstance(y, np.ndarray) and O.sha256_le(y) == GOLDEN[2][1]
+    pinned = torch.from_numpy(x.view(np.int32)).pin_memory()
+    out = torch.empty_like(pinned).pin_memory()
+    dp = P.algorithms.device_plan_for(P.make_plan(params, variant, w.n), 4, 0)
+    dp.exec_host(pinned.data_ptr(), out.data_ptr(), w.batch, False)
+    assert O.sha256_le(out.numpy().view(np.uint32)) == GOLDEN[2][1]

@@ -145,3 +145,62 @@ if __name__ == "__main__":
     random.seed(1)
     for L, K0 in ((6, 3), (7, 3), (7, 4), (8, 4), (9, 5)):
         print(L, K0, check(L, K0))
+
+
+def check3(L, a, b):
+    """3-pass split (a, b, c) for DIT and Pease: the middle pass (S0=a, K=b)
+    and last pass as twist + local transform, twist W^(r * rev_K(x)) with
+    W = w^(N / 2^(S0+K)) and r = the network part that enters the twiddles."""
+    n, w, wp = tables(L)
+    c = L - a - b
+    x = [random.randrange(P) for _ in range(n)]
+    ok = {}
+    # ---- DIT
+    d = [x[rev(i, L)] for i in range(n)]
+    ref = list(d)
+    for s in range(1, L + 1):
+        dit_stage(ref, s, L, wp)
+    cur = list(d)
+    for s in range(1, a + 1):
+        dit_stage(cur, s, L, wp)
+    for (S0, K) in ((a, b), (a + b, c)):
+        W = pow(w, n >> (S0 + K), P)
+        _, _, wpl = tables(K)
+        out = list(cur)
+        for Q in range(1 << (L - K)):
+            low, high = Q & ((1 << S0) - 1), Q >> S0
+            pos = [low | (xx << S0) | (high << (S0 + K)) for xx in range(1 << K)]
+            v = [cur[pp] * pow(W, low * rev(xx, K), P) % P for xx, pp in enumerate(pos)]
+            for s in range(1, K + 1):
+                dit_stage(v, s, K, wpl)
+            for xx, pp in enumerate(pos):
+                out[pp] = v[xx]
+        cur = out
+    ok["dit"] = cur == ref
+    # ---- Pease: network Q, local x at Q*2^K + x; enters via qtop = Q >> (L-K-S0)
+    e = [x[rev(i, L)] for i in range(n)]
+    ref = list(e)
+    for s in range(1, L + 1):
+        ref = pease_stage(ref, s, L, wp)
+    cur = list(e)
+    for s in range(1, a + 1):
+        cur = pease_stage(cur, s, L, wp)
+    for (S0, K) in ((a, b), (a + b, c)):
+        W = pow(w, n >> (S0 + K), P)
+        _, _, wpl = tables(K)
+        out = [0] * n
+        for Q in range(1 << (L - K)):
+            qtop = Q >> (L - K - S0)
+            v = [cur[(Q << K) + xx] * pow(W, qtop * rev(xx, K), P) % P for xx in range(1 << K)]
+            for s in range(1, K + 1):
+                v = pease_stage(v, s, K, wpl)
+            for R in range(1 << K):
+                out[Q | (R << (L - K))] = v[R]
+        cur = out
+    ok["pease"] = cur == ref
+    return ok
+
+
+if __name__ == "__main__":
+    for L, a, b in ((6, 2, 2), (7, 3, 2), (8, 3, 3), (9, 3, 3), (10, 4, 3)):
+        print("3-pass", L, a, b, check3(L, a, b))
