@@ -55,7 +55,9 @@ struct TileArgs {
     int scale;
     Tw ninv;
     int twist;                 // four-step factorisation of a late pass (docs/PASS_ALGEBRA.md):
-                               // 0 none, 1 pre w^(Q*rev(x)), 2 pre w^(Q*x), 3 post w^(Q*rev(x))
+                               // 0 none, 1 pre W^(r*rev(x)), 2 pre W^(r*x), 3 post W^(r*rev(x)),
+                               // W = w^(N / 2^(S0+K)); r = the network's twiddle-carrying bits:
+    int tw_rsel;               //   0: Q mod 2^S0 (DIT/DIF), 1: Q >> (L-K-S0) (Pease qtop / Stockham ghi)
     const Tw* tw_lo;           // w^j, j < 2^th          (the plan's main table prefix)
     const Tw* tw_hi;           // w^(j*2^th), j < 2^(L-th)
     int th;
@@ -239,6 +241,12 @@ struct TileGeo {
 };
 
 // ----------------------------------------------------------------- kernel --
+// per-network twist table shape: w^(r*xr) = lo[xr & 31] * hi[xr >> 5], xr < 2^K
+template <int K> constexpr int twc_lo() { return K < 5 ? (1 << K) : 32; }
+template <int K> constexpr int twc_hi() { return K > 5 ? (1 << (K - 5)) : 1; }
+template <int K> constexpr int tw_row() { return twc_lo<K>() + 1 + twc_hi<K>() + 1; }   // odd-padded rows
+constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
+
 template <class A, int V, int K, int TQ, int NT, int LAY, int SMB, int TWB>
 __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 2))) k_tile(TileArgs<A> a) {
     using T = typename A::T;
@@ -258,17 +266,18 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
     __shared__ uint64_t Gin[TQ], Gout[TQ];
     Tw* tws = reinterpret_cast<Tw*>(smem_raw);
     // per-tile twist tables (only when a.twist): network t, j < 32:
-    //   twl[t][j] = w^(Q_t * j), twh[t][j] = w^(Q_t * 32 * j)  (rows padded to 33)
+    //   twl[t][j] = w^(Q_t * j), twh[t][j] = w^(Q_t * 32 * j)  (rows odd-padded)
+    constexpr int TSL = twc_lo<K>() + 1, TSH = twc_hi<K>() + 1;
     Tw* twl = tws + (1 << SMB);
-    Tw* twh = twl + TQ * 33;
-    T* bufA = reinterpret_cast<T*>(smem_raw + ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * 66 : 0));
+    Tw* twh = twl + TQ * TSL;
+    T* bufA = reinterpret_cast<T*>(smem_raw + ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * tw_row<K>() : 0));
     T* bufB = PP ? bufA + TQ * NP : bufA;
     A ar;
     ar.init(a.p);
     const int L = a.L, S0 = a.S0;
     const int M = (LAY == TL_VARIANT) ? L - K : (LAY == TL_SIX_A ? a.l1 : a.l2);
     const uint64_t N = 1ull << L;
-    constexpr int LTQ = TQ == 1 ? 0 : (TQ == 2 ? 1 : (TQ == 4 ? 2 : (TQ == 8 ? 3 : (TQ == 16 ? 4 : (TQ == 32 ? 5 : 6)))));
+    constexpr int LTQ = ilog2c(TQ);
     const int ltpr = M - LTQ;                          // log2 tiles per row
     const uint64_t tiles_per_row = 1ull << ltpr;
     const uint64_t ntiles = a.batch << ltpr;
@@ -287,7 +296,8 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
     // twist factor w^(Q_t * xr) = twl[t][xr mod 32] * twh[t][xr >> 5] applied to v
     auto twistv = [&](T v, uint32_t t, uint32_t x) -> T {
         const uint32_t xr = (a.twist == 2) ? x : brev(x, K);
-        return ar.mulc(ar.mulc(v, twl[t * 33 + (xr & 31)]), twh[t * 33 + (xr >> 5)]);
+        if (K <= 5) return ar.mulc(v, twl[t * TSL + xr]);
+        return ar.mulc(ar.mulc(v, twl[t * TSL + (xr & 31)]), twh[t * TSH + (xr >> 5)]);
     };
 
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -311,10 +321,14 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
         __syncthreads();
         if (TWB && a.twist) {                 // per-network twist tables from the main table w^i
             const uint64_t nm = N - 1;
-            for (uint32_t i = threadIdx.x; i < TQ * 64u; i += NT) {
-                const uint32_t t = i >> 6, j = i & 31;
-                const uint64_t e = (i & 32) ? ((uint64_t)Qs[t] * 32u * j) & nm : ((uint64_t)Qs[t] * j) & nm;
-                ((i & 32) ? twh : twl)[t * 33 + j] = __ldg(a.tw_lo + e);
+            const int sh = L - S0 - K;
+            constexpr uint32_t CL = twc_lo<K>(), CH = K > 5 ? twc_hi<K>() : 0;
+            for (uint32_t i = threadIdx.x; i < TQ * (CL + CH); i += NT) {
+                const uint32_t t = i / (CL + CH), j = i % (CL + CH);
+                const uint32_t Q = Qs[t];
+                const uint64_t r = a.tw_rsel ? (uint64_t)(Q >> (L - K - S0)) : (uint64_t)(Q & ((1u << S0) - 1));
+                if (j < CL) twl[t * TSL + j] = __ldg(a.tw_lo + (((r * j) << sh) & nm));
+                else twh[t * TSH + (j - CL)] = __ldg(a.tw_lo + (((r * 32u * (j - CL)) << sh) & nm));
             }
             __syncthreads();
         }
@@ -524,7 +538,7 @@ cudaError_t launch_tile(const TileArgs<A>& a, cudaStream_t s, int num_sms, int* 
     using T = typename A::T;
     using Tw = typename A::Tw;
     constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);
-    constexpr size_t smem = ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * 66 : 0) +
+    constexpr size_t smem = ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * tw_row<K>() : 0) +
                             (PP ? 2 : 1) * (size_t)TQ * tile_stride<T, K, TQ>() * sizeof(T);
     if (a.twist && K > 10) return cudaErrorInvalidValue;   // twist tables cover xr < 2^10
     auto kern = k_tile<A, V, K, TQ, NT, LAY, SMB, TWB>;

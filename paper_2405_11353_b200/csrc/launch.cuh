@@ -149,10 +149,9 @@ cudaError_t run_variant(const MultipassReq& r) {
     const T* cur = static_cast<const T*>(r.in);
     cudaError_t e = cudaSuccess;
     if (V == V_FLAT) {                     // bit_reverse_permute as its own HBM pass
-        dim3 blk(32, 8);
-        uint64_t blocks = r.batch << (L - 10);
+        uint64_t blocks = r.batch << (L - 12);
         uint64_t cap = (uint64_t)r.num_sms * 8;
-        k_bitrev<T><<<(unsigned)(blocks < cap ? blocks : cap), blk, 0, r.stream>>>(cur, ws1, r.batch, L, r.counters);
+        k_bitrev<T><<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, r.stream>>>(cur, ws1, r.batch, L, r.counters);
         if (r.launches) ++*r.launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         cur = ws1;

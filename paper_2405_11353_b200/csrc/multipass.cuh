@@ -177,31 +177,31 @@ __global__ void __launch_bounds__(kThreads) k_pass(PassArgs<F> a) {
 }
 
 // Standalone bit-reverse permutation out[i] = in[rev(i)] (modmath.py:171-177)
-// for the multi-pass Flat transform; 32x32 tiles through shared memory so
-// both sides are coalesced: i = [a | m | b] (5-bit a, b).
+// -- the reference's own separate pass (algorithms.py:174,238,255) for the
+// multi-pass Flat / Pease / Pease_nc transforms.  64 x 64 tiles through
+// shared memory so BOTH sides move 64-residue (>= 256-byte) runs:
+// i = [a | m | b] (6-bit a, b), out[[a|m|b]] = in[[rev(b)|rev(m)|rev(a)]].
 template <class T>
-__global__ void k_bitrev(const T* in, T* out, uint64_t batch, int L, unsigned long long* counters) {
-    __shared__ T tile[32][33];
-    const int mb = L - 10;
+__global__ void __launch_bounds__(256) k_bitrev(const T* in, T* out, uint64_t batch, int L, unsigned long long* counters) {
+    __shared__ T tile[64][65];
+    const int mb = L - 12;
     const uint64_t N = 1ull << L;
     const uint64_t per_row = 1ull << mb;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;     // 64 x 4
     for (uint64_t blk = blockIdx.x; blk < batch * per_row; blk += gridDim.x) {
-        const uint64_t row = blk / per_row;
-        const uint32_t m = (uint32_t)(blk % per_row);
+        const uint64_t row = blk >> mb;
+        const uint32_t m = (uint32_t)(blk & (per_row - 1));
         const T* src = in + row * N;
         T* dst = out + row * N;
-        const uint32_t rm = brev(m, mb);
-        // read in[[r | rev(m) | c]] for c fast: row r = rev(b), column c = rev(a)
-        for (int k = threadIdx.y; k < 32; k += blockDim.y)
-            tile[k][threadIdx.x] = src[((uint64_t)k << (L - 5)) | ((uint64_t)rm << 5) | threadIdx.x];
+        const uint64_t rm = (uint64_t)brev(m, mb) << 6;
+        for (int k = ty; k < 64; k += 4)                        // read in[[k | rev(m) | tx]]
+            tile[k][tx] = src[((uint64_t)k << (L - 6)) | rm | tx];
         __syncthreads();
-        // write out[[a | m | b]] = in[[rev(b) | rev(m) | rev(a)]] for b fast
-        for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-            const uint32_t aa = k, bb = threadIdx.x;
-            dst[((uint64_t)aa << (L - 5)) | ((uint64_t)m << 5) | bb] = tile[brev(bb, 5)][brev(aa, 5)];
-        }
+        const uint32_t rb = brev(tx, 6);
+        for (int k = ty; k < 64; k += 4)                        // write out[[k | m | tx]] = in[[rev(tx)|rev(m)|rev(k)]]
+            dst[((uint64_t)k << (L - 6)) | ((uint64_t)m << 6) | tx] = tile[rb][brev(k, 6)];
         __syncthreads();
-        if (counters && threadIdx.x == 0 && threadIdx.y == 0 && m == 0) atomicAdd(counters + C_BITREV, 1ull);
+        if (counters && threadIdx.x == 0 && m == 0) atomicAdd(counters + C_BITREV, 1ull);
     }
 }
 

@@ -62,20 +62,30 @@ cudaError_t pass_any(int K, const TileArgs<A>& a, cudaStream_t s, int sms, int* 
     return cudaSuccess;
 }
 
-inline int tile_plan(int L, int word, int* K) {
-    const int kmax = word == 4 ? 10 : 9, kmin = 7;
-    int P = (L + kmax - 1) / kmax;
-    if (P < 2) P = 2;
-    for (int i = 0; i < P; ++i) K[i] = L / P + (i < L % P ? 1 : 0);
-    for (int i = 0; i < P; ++i)
-        if (K[i] < kmin || K[i] > kmax) return 0;
-    return P;
-}
-
 // NTT_TILE_DIAG=1|2: diagnostics (skip compute | skip data movement); never set in production
 inline int tile_diag() {
     static int d = [] { const char* e = getenv("NTT_TILE_DIAG"); return e ? atoi(e) : 0; }();
     return d;
+}
+
+// Pass plan.  Tiles hold 2^13 (u32) / 2^12 (u64) residues, so a pass of K
+// stages has TQ = 2^(13-K) networks and every strided HBM side moves runs of
+// TQ residues.  Measured on B200 (profiles/r1/summary.md): the tile kernel is
+// issue/latency bound, not run-length bound -- a 3-pass 2^20 plan with 256 B
+// runs (K = 7,7,6) ran 10.1 ms against 4.8 ms for 2 passes of K = 10 with
+// 32 B runs, because per-pass overhead instructions dominate.  So: fewest
+// passes, K <= 10.
+inline int tile_plan(int L, int word, int* K) {
+    int kmax;
+    if (word == 4) kmax = 10;
+    else kmax = 9;
+    const int kmin = 7;
+    int P = (L + kmax - 1) / kmax;
+    if (P < 2) P = 2;
+    for (int i = 0; i < P; ++i) K[i] = L / P + (i < L % P ? 1 : 0);
+    for (int i = 0; i < P; ++i)
+        if (K[i] < kmin || K[i] > 10) return 0;
+    return P;
 }
 
 template <class A>
@@ -112,15 +122,20 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
     T* ws1 = ws0 + r.batch * N;
     const T* cur = static_cast<const T*>(r.in);
     const bool al = aligned16(r.in) && aligned16(r.out) && aligned16(r.ws);
-    // four-step factorisation of the late pass (u32 fields, 2-pass plans): the
-    // network-dependent stage twiddles become one per-element twist
-    const bool fac = sizeof(T) == 4 && P == 2 && K[0] <= 10 && K[1] <= 10;
+    // four-step factorisation of the later passes (u32): the network-dependent
+    // stage twiddles become one per-element twist W^(r*x'), docs/PASS_ALGEBRA.md
+    const bool fac = sizeof(T) == 4;
+    // Pease with >= 3 passes: the reference's separate bit_reverse_permute pass
+    // (algorithms.py:238,255) as a 64x64 transpose, so every Pease pass reads
+    // contiguous networks and writes TQ-residue runs; 2-pass Pease fuses the
+    // reversal into the first gather and writes a row-bit-reversed transpose
+    const bool pease = (V == V_PEASE || V == V_PEASE_NC);
+    const bool sep_bitrev = (V == V_FLAT) || (pease && P >= 3);
     cudaError_t e = cudaSuccess;
-    if (V == V_FLAT) {                     // bit_reverse_permute as its own HBM pass
-        dim3 blk(32, 8);
-        uint64_t blocks = r.batch << (L - 10);
+    if (sep_bitrev) {
+        uint64_t blocks = r.batch << (L - 12);
         uint64_t cap = (uint64_t)r.num_sms * 8;
-        k_bitrev<T><<<(unsigned)(blocks < cap ? blocks : cap), blk, 0, r.stream>>>(cur, ws1, r.batch, L, r.counters);
+        k_bitrev<T><<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, r.stream>>>(cur, ws1, r.batch, L, r.counters);
         if (r.launches) ++*r.launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         cur = ws1;
@@ -149,7 +164,7 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
                 a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_T_FAST;
             }
             a.vec_in = a.vec_out = al && tq >= VE;
-            if (fac && i == 1) a.twist = 1;
+            if (fac && i > 0) { a.twist = 1; a.tw_rsel = 0; }
             e = pass_any<A, V_DIT>(k, a, r.stream, r.num_sms, r.launches, &okp);
             done += k;
         } else if (V == V_DIF) {
@@ -161,33 +176,30 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
                 a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_T_FAST;
             }
             a.vec_in = a.vec_out = al && (1 << (tile_e<T>() - k)) >= VE;
-            if (fac && i == 0) a.twist = 3;
+            if (fac && !last) { a.twist = 3; a.tw_rsel = 0; }
             e = pass_any<A, V_DIF>(k, a, r.stream, r.num_sms, r.launches, &okp);
             done += k;
-        } else if (V == V_PEASE || V == V_PEASE_NC) {
+        } else if (pease) {
             a.S0 = done;
-            if (i == 0 && P == 2) {
-                // networks with consecutive rev(Q): natural-order gather runs; the
-                // stage state is written row-bit-reversed-transposed (out_trb) so the
-                // scatter runs are contiguous too; pass 1 undoes it (rev_local)
+            if (sep_bitrev) {
+                a.qmode = TQM_LINEAR; a.in_order = TO_C_FAST; a.out_order = TO_T_FAST;
+                a.vec_in = al;
+                a.vec_out = al && tq >= VE;
+                if (i == 0) a.count_bitrev = 0;
+                if (fac && i > 0) { a.twist = 1; a.tw_rsel = 1; }
+            } else if (i == 0) {
+                // P == 2: networks with consecutive rev(Q); the stage state is
+                // written row-bit-reversed-transposed (out_trb), pass 1 undoes it
                 a.qmode = TQM_REV; a.rev_in = 1; a.out_trb = 1;
                 a.in_order = TO_T_FAST; a.out_order = TO_T_FAST; a.count_bitrev = 1;
                 a.vec_in = a.vec_out = al && tq >= VE;
-            } else if (i == 0) {
-                int ta = 1;
-                while (ta * ta < tq) ta <<= 1;
-                a.TA = ta;
-                a.la = __builtin_ctz(ta);
-                a.qmode = TQM_2D; a.rev_in = 1; a.in_order = TO_T_FAST; a.out_order = TO_TB_FAST; a.count_bitrev = 1;
-                a.vec_in = al && ta >= VE;
-                a.vec_out = 0;
             } else {
                 a.qmode = TQM_LINEAR; a.in_order = TO_C_FAST; a.out_order = TO_T_FAST;
-                a.rev_local = (P == 2);
+                a.rev_local = 1;
                 a.vec_in = al;
                 a.vec_out = al && tq >= VE;
+                if (fac) { a.twist = 1; a.tw_rsel = 1; }
             }
-            if (fac && i == 1) a.twist = 1;
             e = pass_any<A, V_PEASE_NC>(k, a, r.stream, r.num_sms, r.launches, &okp);
             done += k;
         } else {  // Stockham
@@ -198,7 +210,7 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
             a.out_order = TO_T_FAST;
             a.vec_in = al && (glob == 0 || (1 << glob) >= VE) && tq >= VE;
             a.vec_out = al && tq >= VE;
-            if (fac && i == 1) a.twist = 2;
+            if (fac && i > 0) { a.twist = 2; a.tw_rsel = 1; }
             e = pass_any<A, V_STOCKHAM>(k, a, r.stream, r.num_sms, r.launches, &okp);
             done += k;
         }

@@ -204,3 +204,61 @@ def check3(L, a, b):
 if __name__ == "__main__":
     for L, a, b in ((6, 2, 2), (7, 3, 2), (8, 3, 3), (9, 3, 3), (10, 4, 3)):
         print("3-pass", L, a, b, check3(L, a, b))
+
+
+def check3b(L, a, b):
+    """3-pass DIF (windows from the top) and Stockham with the generalised twist."""
+    n, w, wp = tables(L)
+    c = L - a - b
+    x = [random.randrange(P) for _ in range(n)]
+    ok = {}
+    # ---- DIF: windows [L-a, L), [L-a-b, L-a), [0, c); post-twist W^(r*rev(x)), r = low S0 bits
+    ref = list(x)
+    for s in range(L, 0, -1):
+        dif_stage(ref, s, L, wp)
+    cur = list(x)
+    for (S0, K) in ((L - a, a), (c, b)):
+        W = pow(w, n >> (S0 + K), P)
+        _, _, wpl = tables(K)
+        out = list(cur)
+        for Q in range(1 << (L - K)):
+            low, high = Q & ((1 << S0) - 1), Q >> S0
+            pos = [low | (xx << S0) | (high << (S0 + K)) for xx in range(1 << K)]
+            v = [cur[pp] for pp in pos]
+            for s in range(K, 0, -1):
+                dif_stage(v, s, K, wpl)
+            v = [v[xx] * pow(W, low * rev(xx, K), P) % P for xx in range(1 << K)]
+            for xx, pp in enumerate(pos):
+                out[pp] = v[xx]
+        cur = out
+    for s in range(c, 0, -1):          # last window [0, c): local twiddles only
+        dif_stage(cur, s, L, wp)
+    ok["dif"] = cur == ref
+    # ---- Stockham: passes (0..a-1), (a..a+b-1), (a+b..L-1); twist W^(ghi * x), natural x
+    ref = list(x)
+    for s in range(L):
+        ref = stockham_stage(ref, s, L, wp)
+    cur = list(x)
+    for s in range(a):
+        cur = stockham_stage(cur, s, L, wp)
+    for (S0, K) in ((a, b), (a + b, c)):
+        W = pow(w, n >> (S0 + K), P)
+        _, _, wpl = tables(K)
+        glob = L - S0 - K
+        out = [0] * n
+        for Q in range(1 << (L - K)):
+            ghi, glo = Q >> glob, Q & ((1 << glob) - 1)
+            pos = [(ghi << (L - S0)) | (xx << glob) | glo for xx in range(1 << K)]
+            v = [cur[pp] * pow(W, ghi * xx, P) % P for xx, pp in enumerate(pos)]
+            for s in range(K):
+                v = stockham_stage(v, s, K, wpl)
+            for R in range(1 << K):
+                out[(R << (L - K)) | Q] = v[R]
+        cur = out
+    ok["stockham"] = cur == ref
+    return ok
+
+
+if __name__ == "__main__":
+    for L, a, b in ((6, 2, 2), (7, 3, 2), (8, 3, 3), (9, 3, 3), (10, 4, 3)):
+        print("3-pass b", L, a, b, check3b(L, a, b))
