@@ -224,7 +224,9 @@ NTT_D void stockham_regs(const A& ar, typename A::T (&v)[16], uint32_t hi, const
 }
 
 // -------------------------------------------------------------- kernel ----
-template <class A, int V, int L, int TEAMS>
+// SC: n^-1 scaling compiled in (a runtime flag would leave the predicated-off
+// multiply in the store loop: 5 issue slots per residue)
+template <class A, int V, int L, int TEAMS, bool SC>
 __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                     for (int c = 0; c < 16; ++c) {
                         const uint32_t pos = pbase | ((uint32_t)c << B);
                         T r = ar.fin(v[c]);
-                        if (a.scale) r = ar.mulc(r, a.ninv);
+                        if (SC) r = ar.mulc(r, a.ninv);
                         gout[V == V_DIF ? brev(pos, L) : pos] = r;
                     }
                 }
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                         const uint32_t pos = (((u << (4 - kg)) | n)) | (R << (L - kg));
                         if (last) {
                             T r = ar.fin(v[c]);
-                            if (a.scale) r = ar.mulc(r, a.ninv);
+                            if (SC) r = ar.mulc(r, a.ninv);
                             gout[pos] = r;
                         } else db[padpos<T>(n | (R << (L - kg)))] = v[c];
                     }
@@ -429,7 +431,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                         const uint32_t pos = (R << (L - kg)) | (hi << lob) | (x << (lob - (4 - kg))) | lo;
                         if (last) {
                             T r = ar.fin(v[c]);
-                            if (a.scale) r = ar.mulc(r, a.ninv);
+                            if (SC) r = ar.mulc(r, a.ninv);
                             gout[pos] = r;
                         } else db[padpos<T>((R << (L - kg)) | (x << (lob - (4 - kg))))] = v[c];
                     }
@@ -484,7 +486,7 @@ cudaError_t launch_fast_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int
         *ok = false;
         return cudaSuccess;
     } else {
-        auto kern = k_fast<A, V, L, C::TEAMS>;
+        auto kern = a.scale ? k_fast<A, V, L, C::TEAMS, true> : k_fast<A, V, L, C::TEAMS, false>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
         if (e != cudaSuccess) return e;
         uint64_t ctas = (a.batch + C::TEAMS - 1) / C::TEAMS;

@@ -17,21 +17,26 @@ struct LazyF32 {
     using Tw = uint2;
     using Field = F32S;
     static constexpr bool lazy = true;
-    uint32_t p, p2;
-    NTT_D void init(uint64_t pp) { p = (uint32_t)pp; p2 = 2u * (uint32_t)pp; }
+    uint32_t p, p2, p4;
+    NTT_D void init(uint64_t pp) { p = (uint32_t)pp; p2 = 2u * (uint32_t)pp; p4 = 4u * (uint32_t)pp; }
+    // x + t written as min(x + t, 4p) (an identity: x + t < 4p): one VIADDMNMX on
+    // the ALU pipe, so ptxas cannot move the add onto the FMA pipe (IMAD.IADD),
+    // which IMAD.HI + 2 IMAD already saturate (tools/ubench_pipes.cu: IMAD 2,
+    // IMAD.HI 4 cycles per warp instruction)
+    NTT_D T add4(T a, T b) const { return umin32(a + b, p4); }
     // DIT / Pease / Stockham butterfly: (x, y) -> (x + w*y, x - w*y); in/out [0,4p)
     NTT_D void dit(T& x, T& y, Tw w) const {
         const T xr = umin32(x, x - p2);
         const T q = __umulhi(y, w.y);
         const T t = y * w.x - q * p;          // [0,2p)
-        x = xr + t;
+        x = add4(xr, t);
         y = xr - t + p2;
     }
     // butterfly with twiddle 1: t = y mod 2p
     NTT_D void dit1(T& x, T& y) const {
         const T xr = umin32(x, x - p2);
         const T t = umin32(y, y - p2);
-        x = xr + t;
+        x = add4(xr, t);
         y = xr - t + p2;
     }
     // DIF butterfly: (x, y) -> (x + y, w*(x - y)); in/out [0,2p)

@@ -36,6 +36,51 @@ struct LazyF32c : LazyF32 {      // q*p folded: t = y*w - q*p via mad with negat
     }
 };
 
+
+// quotient q = floor(y*w'/2^32) on the FP64 pipe instead of IMAD.HI:
+// fma_rz(2^52 + y, w'/2^32, 2^52 - w'*2^20) = 2^52 + y*w'/2^32 exactly before
+// the one rounding, so the low word of the result is Shoup's q bit-for-bit.
+struct TwD { uint32_t w, ws; double wd, c; };
+struct LazyF32D : LazyF32 {
+    using Tw = TwD;
+    NTT_D void dit(T& x, T& y, Tw w) const {
+        const T xr = umin32(x, x - p2);
+        const double qd = __fma_rz(__hiloint2double(0x43300000, (int)y), w.wd, w.c);
+        const T q = (T)__double2loint(qd);
+        const T t = y * w.w - q * p;
+        x = xr + t;
+        y = xr - t + p2;
+    }
+};
+// per-butterfly conversion of w' (no precomputed doubles)
+struct LazyF32E : LazyF32 {
+    NTT_D void dit(T& x, T& y, Tw w) const {
+        const T xr = umin32(x, x - p2);
+        const double wd = __hiloint2double(0x41300000, (int)w.y) - 1048576.0;
+        const double c = __fma_rn(-4503599627370496.0, wd, 4503599627370496.0);
+        const double qd = __fma_rz(__hiloint2double(0x43300000, (int)y), wd, c);
+        const T q = (T)__double2loint(qd);
+        const T t = y * w.x - q * p;
+        x = xr + t;
+        y = xr - t + p2;
+    }
+};
+// butterflies with bit 1 of the register index on the FP64 pipe, the rest on IMAD.HI
+struct LazyF32M : LazyF32D {};
+template <class A, class T, class W>
+__device__ __forceinline__ void bf(const A& ar, int c, T& x, T& y, W w) { ar.dit(x, y, w); }
+template <class T, class W>
+__device__ __forceinline__ void bf(const LazyF32M& ar, int c, T& x, T& y, W w) {
+    if (c & 2) ar.LazyF32D::dit(x, y, w);
+    else {
+        const T xr = umin32(x, x - ar.p2);
+        const T q = __umulhi(y, w.ws);
+        const T t = y * w.w - q * ar.p;
+        x = xr + t;
+        y = xr - t + ar.p2;
+    }
+}
+
 template <class A>
 __global__ void k_bfly(typename A::T* out, uint64_t p, int iters, typename A::Tw w0, typename A::Tw w1) {
     using T = typename A::T;
@@ -51,14 +96,14 @@ __global__ void k_bfly(typename A::T* out, uint64_t p, int iters, typename A::Tw
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
                 if (c & (1 << j)) continue;
-                ar.dit(v[c], v[c | (1 << j)], w);
+                bf(ar, c, v[c], v[c | (1 << j)], w);
             }
         }
         w = (it & 1) ? w0 : w1;
     }
     T acc = 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc ^= v[i];
+    for (int i = 0; i < 16; ++i) acc = (T)(((uint64_t)acc * 3 + v[i] % (T)p) % p);
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
@@ -82,8 +127,14 @@ void run(const char* name, uint64_t p, typename A::Tw w0, typename A::Tw w1, int
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
     double bfly = (double)blocks * threads * iters * 32;   // 4 stages x 8 butterflies
-    printf("%-12s threads/blk=%4d  %.3f ms  %.2f Tbfly/s  (%.2f warp-bfly/clk/SM at 1.9GHz)\n", name, threads, ms,
-           bfly / ms / 1e9, bfly / 32 / (ms * 1e-3) / sms / 1.9e9);
+    const size_t nout = (size_t)blocks * threads;
+    T* h = (T*)malloc(nout * sizeof(T));
+    cudaMemcpy(h, out, nout * sizeof(T), cudaMemcpyDeviceToHost);
+    unsigned long long hs = 1469598103934665603ull;
+    for (size_t i = 0; i < nout; ++i) hs = (hs ^ (unsigned long long)h[i]) * 1099511628211ull;
+    free(h);
+    printf("%-12s threads/blk=%4d  %.3f ms  %.2f Tbfly/s  (%.2f warp-bfly/clk/SM at 1.9GHz)  out-hash %016llx\n", name, threads, ms,
+           bfly / ms / 1e9, bfly / 32 / (ms * 1e-3) / sms / 1.9e9, hs);
     cudaFree(out);
 }
 
@@ -120,6 +171,13 @@ int main() {
     run<LazyF32>("lazy-u32", p, w0, w1, 512);
     run<LazyF32b>("lazy-vadd", p, w0, w1, 256);
     run<LazyF32c>("lazy-mad", p, w0, w1, 256);
+    auto mk = [&](uint2 w) { TwD d; d.w = w.x; d.ws = w.y; d.wd = (double)w.y / 4294967296.0;
+                             d.c = 4503599627370496.0 - (double)w.y * 1048576.0; return d; };
+    run<LazyF32D>("lazy-fp64q", p, mk(w0), mk(w1), 256);
+    run<LazyF32D>("lazy-fp64q", p, mk(w0), mk(w1), 512);
+    run<LazyF32E>("lazy-fp64cv", p, w0, w1, 256);
+    run<LazyF32M>("lazy-mix", p, mk(w0), mk(w1), 256);
+    run<LazyF32M>("lazy-mix", p, mk(w0), mk(w1), 512);
     run<Canon<F32S>>("canon-u32", p, w0, w1, 256);
     const uint64_t G = 0xFFFFFFFF00000001ull;
     run<Canon<FGold>>("goldilocks", G, 7ull, 49ull, 256);
