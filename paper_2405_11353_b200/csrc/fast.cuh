@@ -58,6 +58,13 @@ NTT_D void team_sync(int id, int nthreads) {
 template <class T>
 NTT_HD constexpr int lane_bits() { return sizeof(T) == 4 ? 5 : 4; }
 
+// first-group source: the TMA staging buffer (shared) or HBM directly
+template <bool STAGED, class T>
+NTT_D T ldsrc(const T* p) {
+    if constexpr (STAGED) return *p;
+    else return __ldg(p);
+}
+
 // Additive padded layout of the exchange buffers: one pad slot per 2^CW
 // (and per 2^(2CW), ...) slots, so bit b of a position moves the bank by
 // 2^(b mod CW) -- the same conflict-freedom as an XOR fold, but ADDITIVE for
@@ -105,12 +112,17 @@ NTT_D uint32_t scatter_bits(uint32_t t, const Perm& P) {
     return r;
 }
 
-template <int L>
+// RB = register-block bits: each thread holds 2^RB residues (a closed
+// sub-network of <= RB stages).  RB = 4 for every size; RB = 6 for u32 sizes
+// of two groups (2^11, 2^12): one shared-memory exchange per polynomial
+// instead of two, and a third fewer LDS/STS per butterfly.
+template <int L, int RB = 4>
 struct Geo {
     static constexpr int N = 1 << L;
-    static constexpr int TT = 1 << (L - 4);    // threads per team
-    static constexpr int G = (L + 3) / 4;       // register groups
-    static constexpr int K0 = L - 4 * (G - 1);  // short group (first; DIF: last)
+    static constexpr int R = 1 << RB;            // residues per thread
+    static constexpr int TT = 1 << (L - RB);     // threads per team
+    static constexpr int G = (L + RB - 1) / RB;  // register groups
+    static constexpr int K0 = L - RB * (G - 1);  // short group (first; DIF: last)
 };
 
 template <class A>
@@ -130,9 +142,10 @@ struct FastArgs {
 // ---------------------------------------------------------------- DIT/DIF --
 // In-place window [b0, b0+kg) of a register block [B, B+4); pbase = position
 // of register 0.  DIT: stages b0+1.. ascending; DIF: descending.
-template <class A, int L, int B, int b0, int kg, bool DIF>
-NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[16], uint32_t pbase, const typename A::Tw* stw) {
-    static_assert(b0 >= B && b0 + kg <= B + 4, "window outside block");
+template <class A, int L, int B, int b0, int kg, bool DIF, int RB, int RN>
+NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[RN], uint32_t pbase, const typename A::Tw* stw) {
+    // (instantiated for every macro-listed geometry; only valid windows emit code)
+    if constexpr (b0 >= B && b0 + kg <= B + RB) {
     constexpr int off = b0 - B;
     // block [0,4): pbase has zero low bits, so k = kc is a compile-time constant
     // and every w^0 butterfly skips its multiply
@@ -143,7 +156,7 @@ NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[16], uint32_t pbase, cons
         const uint32_t kmask = (1u << (s - 1)) - 1;
         const typename A::Tw* row = stw + (1u << (s - 1)) + (pbase & kmask);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < RN; ++c) {
             if (c & (1 << (off + j))) continue;
             const uint32_t kc = ((uint32_t)c << B) & kmask;      // compile-time part of k
             const int hi = c | (1 << (off + j));
@@ -156,21 +169,22 @@ NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[16], uint32_t pbase, cons
         }
     }
 }
+}
 
 // -------------------------------------------------------------- Pease -----
 // Networks of 2^kg contiguous positions; a thread holds NB = 16/2^kg of them
 // (network n = registers [n*2^kg, (n+1)*2^kg)).  Constant geometry inside the
 // registers; twiddle k = (B << sg) | (q >> (L - kg - sg)) for butterfly with
 // output-bit prefix B (algorithms.py:216-217 in the rotated frame).
-template <class A, int L, int sg, int kg>
-NTT_D void pease_regs(const A& ar, typename A::T (&v)[16], uint32_t ubase, const typename A::Tw* stw) {
+template <class A, int L, int sg, int kg, int RB, int RN>
+NTT_D void pease_regs(const A& ar, typename A::T (&v)[RN], uint32_t ubase, const typename A::Tw* stw) {
     using T = typename A::T;
-    constexpr int NB = 16 >> kg;
+    constexpr int NB = (kg <= RB && sg + kg <= L) ? RN >> kg : 0;
     constexpr int H = 1 << (kg - 1);
 #pragma unroll
     for (int n = 0; n < NB; ++n) {
-        const uint32_t q = (ubase << (4 - kg)) | n;            // network id (L-kg bits)
-        const uint32_t qtop = sg ? (q >> (L - kg - sg)) : 0u;   // top sg bits of q
+        const uint32_t q = (ubase << (RB - kg)) | n;           // network id (L-kg bits)
+        const uint32_t qtop = sg ? (q >> ((L - kg - sg) & 31)) : 0u;   // top sg bits of q
 #pragma unroll
         for (int m = 0; m < kg; ++m) {
             const int s = sg + m + 1;
@@ -197,10 +211,10 @@ NTT_D void pease_regs(const A& ar, typename A::T (&v)[16], uint32_t ubase, const
 // group only).  Stage s = sg+m pairs the window's top remaining bit; the
 // output bit is inserted above the previous ones ([c_rest | B] layout);
 // twiddle k = j = (B << sg) | hi (algorithms.py:281-299).
-template <class A, int L, int sg, int kg>
-NTT_D void stockham_regs(const A& ar, typename A::T (&v)[16], uint32_t hi, const typename A::Tw* stw) {
+template <class A, int L, int sg, int kg, int RB, int RN>
+NTT_D void stockham_regs(const A& ar, typename A::T (&v)[RN], uint32_t hi, const typename A::Tw* stw) {
     using T = typename A::T;
-    constexpr int NB = 16 >> kg;
+    constexpr int NB = (kg <= RB && sg + kg <= L) ? RN >> kg : 0;
     constexpr int H = 1 << (kg - 1);
 #pragma unroll
     for (int x = 0; x < NB; ++x) {
@@ -211,14 +225,14 @@ NTT_D void stockham_regs(const A& ar, typename A::T (&v)[16], uint32_t hi, const
 #pragma unroll
             for (int i = 0; i < H; ++i) {
                 const uint32_t Bv = i & ((1u << m) - 1), crest = (uint32_t)i >> m;
-                T a = v[(i << (4 - kg)) | x], b = v[((i + H) << (4 - kg)) | x];
+                T a = v[(i << (RB - kg)) | x], b = v[((i + H) << (RB - kg)) | x];
                 if (s == 0 || (sg == 0 && Bv == 0)) ar.dit1(a, b);     // w^0 (j = Bv when sg == 0)
                 else ar.dit(a, b, stw[(1u << s) + ((Bv << sg) | hi)]);
                 nv[(crest << (m + 1)) | Bv] = a;
                 nv[(crest << (m + 1)) | (1u << m) | Bv] = b;
             }
 #pragma unroll
-            for (int c = 0; c < (1 << kg); ++c) v[(c << (4 - kg)) | x] = nv[c];
+            for (int c = 0; c < (1 << kg); ++c) v[(c << (RB - kg)) | x] = nv[c];
         }
     }
 }
@@ -226,12 +240,13 @@ NTT_D void stockham_regs(const A& ar, typename A::T (&v)[16], uint32_t hi, const
 // -------------------------------------------------------------- kernel ----
 // SC: n^-1 scaling compiled in (a runtime flag would leave the predicated-off
 // multiply in the store loop: 5 issue slots per residue)
-template <class A, int V, int L, int TEAMS, bool SC>
-__global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a) {
+template <class A, int V, int L, int TEAMS, bool SC, int RB>
+__global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
-    using GG = Geo<L>;
-    constexpr int N = GG::N, TT = GG::TT, G = GG::G, K0 = GG::K0;
+    using GG = Geo<L, RB>;
+    constexpr int N = GG::N, TT = GG::TT, G = GG::G, K0 = GG::K0, RV = GG::R;
+    static_assert(RB == 4 || G <= 2, "wide register blocks: first/last groups only");
     constexpr int CW = lane_bits<T>();
     constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);   // permuting groups
     // Pease keeps two work buffers + the copy-back (algorithms.py:242); Pease_nc
@@ -239,6 +254,11 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
     // whole sub-network, so after a team barrier the group writes the same
     // buffer (no copy, one buffer less => one more team per CTA)
     constexpr bool TWO = (V == V_PEASE);
+    // RB = 4: TMA-prefetched staging buffer per team (one row ahead).  RB = 6:
+    // no staging -- the first group loads its 64 residues per thread straight
+    // from HBM (coalesced 128 B warp rows); the smem saved buys twice the teams,
+    // whose interleaved load / compute phases hide the latency instead.
+    constexpr bool STG_ = (RB == 4);
     constexpr int NBUF = TWO ? 3 : 2;      // staging + work (+ second work buffer for Pease)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint64_t mbar[TEAMS];
@@ -247,8 +267,8 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
     const int team = threadIdx.x / TT;
     const uint32_t t = threadIdx.x % TT;
     constexpr int NP = padded_len<T, L>();
-    T* S = reinterpret_cast<T*>(smem_raw + (size_t)N * sizeof(Tw)) + (size_t)team * (N + (NBUF - 1) * NP);
-    T* W0 = S + N;
+    T* S = reinterpret_cast<T*>(smem_raw + (size_t)N * sizeof(Tw)) + (size_t)team * ((STG_ ? N : 0) + (NBUF - 1) * NP);
+    T* W0 = S + (STG_ ? N : 0);
     T* W1 = TWO ? W0 + NP : W0;
     A ar;
     ar.init(a.p);
@@ -262,7 +282,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
     const uint64_t stride = (uint64_t)gridDim.x * TEAMS;
     uint64_t poly = (uint64_t)blockIdx.x * TEAMS + team;
     const uint32_t bytes = N * sizeof(T);
-    if (t == 0 && poly < a.batch) {
+    if (STG_ && t == 0 && poly < a.batch) {
         mbar_expect_tx(&mbar[team], bytes);
         tma_load_1d(S, a.in + poly * N, bytes, &mbar[team]);
     }
@@ -271,9 +291,12 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
     const int bar_id = 1 + team;
 
     for (; poly < a.batch; poly += stride) {
-        T v[16];
-        mbar_wait(&mbar[team], phase);
-        phase ^= 1;
+        T v[RV];
+        if (STG_) {
+            mbar_wait(&mbar[team], phase);
+            phase ^= 1;
+        }
+        const T* S0 = STG_ ? S : a.in + poly * N;   // first-group source
         T* gout = a.out + poly * N;
         const uint64_t next = poly + stride;
 
@@ -281,11 +304,11 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 // ---- geometry of group g (compile time after unrolling)
-                const int B = (V == V_DIT) ? (g == 0 ? 0 : K0 + 4 * (g - 1)) : (g == G - 1 ? 0 : L - 4 * (g + 1));
-                const int kg = (V == V_DIT) ? (g == 0 ? K0 : 4) : (g == G - 1 ? K0 : 4);
+                const int B = (V == V_DIT) ? (g == 0 ? 0 : K0 + RB * (g - 1)) : (g == G - 1 ? 0 : L - RB * (g + 1));
+                const int kg = (V == V_DIT) ? (g == 0 ? K0 : RB) : (g == G - 1 ? K0 : RB);
                 const bool first = g == 0, last = g == G - 1;
                 uint32_t pbase;
-                if ((V == V_DIT && first) || (V == V_DIF && last)) pbase = brev(t, L - 4) << 4;   // block [0,4)
+                if ((V == V_DIT && first) || (V == V_DIF && last)) pbase = brev(t, L - RB) << RB;   // block [0,RB)
                 else if ((V == V_DIT && last) || (V == V_DIF && first)) pbase = t;                 // block [L-4,L)
                 else {
                     // middle groups: lane-planned map (compile-time permutation)
@@ -302,14 +325,15 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                 // ---- gather
                 T* wb = W0 + padpos<T>(pbase);
 #pragma unroll
-                for (int c = 0; c < 16; ++c) {
+                for (int c = 0; c < RV; ++c) {
                     const uint32_t pos = pbase | ((uint32_t)c << B);
-                    if (first) v[c] = S[V == V_DIT ? brev(pos, L) : pos];
+                    // DIT: pbase = brev(t) << 4, so brev(pos) = brev(c) << (L-4) | t (no per-residue BREV)
+                    if (first) v[c] = ldsrc<STG_>(S0 + (V == V_DIT ? ((brev((uint32_t)c, RB) << (L - RB)) | t) : pos));
                     else v[c] = wb[padpos<T>((uint32_t)c << B)];
                 }
                 if (first) {
-                    team_sync(bar_id, TT);      // staging consumed: prefetch the next row
-                    if (t == 0 && next < a.batch) {
+                    if (STG_) team_sync(bar_id, TT);      // staging consumed: prefetch the next row
+                    if (STG_ && t == 0 && next < a.batch) {
                         fence_proxy_async();
                         mbar_expect_tx(&mbar[team], bytes);
                         tma_load_1d(S, a.in + next * N, bytes, &mbar[team]);
@@ -317,35 +341,41 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                 }
                 // ---- stages
 #define NTT_BW(BB, b0v, kgv)                                                                \
-    if (B == BB && kg == kgv) bitwin_regs<A, L, BB, b0v, kgv, V == V_DIF>(ar, v, pbase, stw);
+    if (B == BB && kg == kgv) bitwin_regs<A, L, BB, b0v, kgv, V == V_DIF, RB, RV>(ar, v, pbase, stw);
                 if (V == V_DIT) {
                     if (g == 0) {
-                        NTT_BW(0, 0, 1) NTT_BW(0, 0, 2) NTT_BW(0, 0, 3) NTT_BW(0, 0, 4)
-                    } else {
+                        NTT_BW(0, 0, 1) NTT_BW(0, 0, 2) NTT_BW(0, 0, 3) NTT_BW(0, 0, 4) NTT_BW(0, 0, 5)
+                        NTT_BW(0, 0, 6)
+                    } else if (RB == 4) {
                         NTT_BW(1, 1, 4) NTT_BW(2, 2, 4) NTT_BW(3, 3, 4) NTT_BW(4, 4, 4) NTT_BW(5, 5, 4)
                         NTT_BW(6, 6, 4) NTT_BW(7, 7, 4) NTT_BW(8, 8, 4) NTT_BW(9, 9, 4)
+                    } else {
+                        NTT_BW(5, 5, 6) NTT_BW(6, 6, 6)
                     }
                 } else {
                     if (g == G - 1) {
-                        NTT_BW(0, 0, 1) NTT_BW(0, 0, 2) NTT_BW(0, 0, 3) NTT_BW(0, 0, 4)
-                    } else {
+                        NTT_BW(0, 0, 1) NTT_BW(0, 0, 2) NTT_BW(0, 0, 3) NTT_BW(0, 0, 4) NTT_BW(0, 0, 5)
+                        NTT_BW(0, 0, 6)
+                    } else if (RB == 4) {
                         NTT_BW(1, 1, 4) NTT_BW(2, 2, 4) NTT_BW(3, 3, 4) NTT_BW(4, 4, 4) NTT_BW(5, 5, 4)
                         NTT_BW(6, 6, 4) NTT_BW(7, 7, 4) NTT_BW(8, 8, 4) NTT_BW(9, 9, 4)
+                    } else {
+                        NTT_BW(5, 5, 6) NTT_BW(6, 6, 6)
                     }
                 }
 #undef NTT_BW
                 // ---- scatter
                 if (!last) {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) wb[padpos<T>((uint32_t)c << B)] = v[c];
+                    for (int c = 0; c < RV; ++c) wb[padpos<T>((uint32_t)c << B)] = v[c];
                     team_sync(bar_id, TT);
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
+                    for (int c = 0; c < RV; ++c) {
                         const uint32_t pos = pbase | ((uint32_t)c << B);
                         T r = ar.fin(v[c]);
                         if (SC) r = ar.mulc(r, a.ninv);
-                        gout[V == V_DIF ? brev(pos, L) : pos] = r;
+                        gout[V == V_DIF ? ((brev((uint32_t)c, RB) << (L - RB)) | t) : pos] = r;
                     }
                 }
             }
@@ -355,39 +385,39 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
             T* dst = W1;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                const int sg = g == 0 ? 0 : K0 + 4 * (g - 1);
-                const int kg = g == 0 ? K0 : 4;
+                const int sg = g == 0 ? 0 : K0 + RB * (g - 1);
+                const int kg = g == 0 ? K0 : RB;
                 const bool first = g == 0, last = g == G - 1;
                 if (V != V_STOCKHAM) {
-                    // sub-networks: 16 contiguous positions (u << 4) | c
-                    const uint32_t u = first ? brev(t, L - 4) : t;
-                    const T* sb = src + padpos<T>(u << 4);
+                    // sub-networks: 2^RB contiguous positions (u << RB) | c
+                    const uint32_t u = first ? brev(t, L - RB) : t;
+                    const T* sb = src + padpos<T>(u << RB);
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        const uint32_t pos = (u << 4) | c;
-                        v[c] = first ? S[brev(pos, L)] : sb[padpos<T>((uint32_t)c)];
+                    for (int c = 0; c < RV; ++c) {
+                        v[c] = first ? ldsrc<STG_>(S0 + ((brev((uint32_t)c, RB) << (L - RB)) | t)) : sb[padpos<T>((uint32_t)c)];   // u = brev(t)
                     }
                     if (first) {
-                        team_sync(bar_id, TT);
-                        if (t == 0 && next < a.batch) {
+                        if (STG_) team_sync(bar_id, TT);
+                        if (STG_ && t == 0 && next < a.batch) {
                             fence_proxy_async();
                             mbar_expect_tx(&mbar[team], bytes);
                             tma_load_1d(S, a.in + next * N, bytes, &mbar[team]);
                         }
                     }
 #define NTT_PE(SG, KGV) \
-    if (sg == SG && kg == KGV) pease_regs<A, L, SG, KGV>(ar, v, u, stw);
-                    if (g == 0) { NTT_PE(0, 1) NTT_PE(0, 2) NTT_PE(0, 3) NTT_PE(0, 4) }
-                    else { NTT_PE(1, 4) NTT_PE(2, 4) NTT_PE(3, 4) NTT_PE(4, 4) NTT_PE(5, 4) NTT_PE(6, 4)
+    if (sg == SG && kg == KGV) pease_regs<A, L, SG, KGV, RB, RV>(ar, v, u, stw);
+                    if (g == 0) { NTT_PE(0, 1) NTT_PE(0, 2) NTT_PE(0, 3) NTT_PE(0, 4) NTT_PE(0, 5) NTT_PE(0, 6) }
+                    else if (RB == 4) { NTT_PE(1, 4) NTT_PE(2, 4) NTT_PE(3, 4) NTT_PE(4, 4) NTT_PE(5, 4) NTT_PE(6, 4)
                            NTT_PE(7, 4) NTT_PE(8, 4) NTT_PE(9, 4) }
+                    else { NTT_PE(5, 6) NTT_PE(6, 6) }
 #undef NTT_PE
                     if (!TWO && !first && !last) team_sync(bar_id, TT);   // all reads of W0 done
                     // outputs: network n = (u << (4-kg)) | n writes q | R << (L-kg)
-                    T* db = dst + padpos<T>(u << (4 - kg));
+                    T* db = dst + padpos<T>(u << (RB - kg));
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
+                    for (int c = 0; c < RV; ++c) {
                         const uint32_t n = c >> kg, R = c & ((1u << kg) - 1);
-                        const uint32_t pos = (((u << (4 - kg)) | n)) | (R << (L - kg));
+                        const uint32_t pos = (((u << (RB - kg)) | n)) | (R << (L - kg));
                         if (last) {
                             T r = ar.fin(v[c]);
                             if (SC) r = ar.mulc(r, a.ninv);
@@ -395,7 +425,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                         } else db[padpos<T>(n | (R << (L - kg)))] = v[c];
                     }
                 } else {
-                    // Stockham: window [lob, lob+kg); first group: block [L-4, L)
+                    // Stockham: window [lob, lob+kg); first group: block [L-RB, L)
                     const int lob = L - sg - kg;
                     uint32_t hi, lo;
                     if (first) { hi = 0; lo = t; }
@@ -403,37 +433,38 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
                     else { lo = t & ((1u << lob) - 1); hi = t >> lob; }
                     const T* sb = src + padpos<T>((hi << (L - sg)) | lo);
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        // register c = (w << (4-kg)) | x; position = hi | w | x | lo
-                        const uint32_t pos = (hi << (L - sg)) | ((uint32_t)c << (lob - (4 - kg))) | lo;
-                        v[c] = first ? S[pos] : sb[padpos<T>((uint32_t)c << (lob - (4 - kg)))];
+                    for (int c = 0; c < RV; ++c) {
+                        // register c = (w << (RB-kg)) | x; position = hi | w | x | lo
+                        const uint32_t pos = (hi << (L - sg)) | ((uint32_t)c << (lob - (RB - kg))) | lo;
+                        v[c] = first ? ldsrc<STG_>(S0 + pos) : sb[padpos<T>((uint32_t)c << (lob - (RB - kg)))];
                     }
                     if (first) {
-                        team_sync(bar_id, TT);
-                        if (t == 0 && next < a.batch) {
+                        if (STG_) team_sync(bar_id, TT);
+                        if (STG_ && t == 0 && next < a.batch) {
                             fence_proxy_async();
                             mbar_expect_tx(&mbar[team], bytes);
                             tma_load_1d(S, a.in + next * N, bytes, &mbar[team]);
                         }
                     }
 #define NTT_ST(SG, KGV) \
-    if (sg == SG && kg == KGV) stockham_regs<A, L, SG, KGV>(ar, v, hi, stw);
-                    if (g == 0) { NTT_ST(0, 1) NTT_ST(0, 2) NTT_ST(0, 3) NTT_ST(0, 4) }
-                    else { NTT_ST(1, 4) NTT_ST(2, 4) NTT_ST(3, 4) NTT_ST(4, 4) NTT_ST(5, 4) NTT_ST(6, 4)
+    if (sg == SG && kg == KGV) stockham_regs<A, L, SG, KGV, RB, RV>(ar, v, hi, stw);
+                    if (g == 0) { NTT_ST(0, 1) NTT_ST(0, 2) NTT_ST(0, 3) NTT_ST(0, 4) NTT_ST(0, 5) NTT_ST(0, 6) }
+                    else if (RB == 4) { NTT_ST(1, 4) NTT_ST(2, 4) NTT_ST(3, 4) NTT_ST(4, 4) NTT_ST(5, 4) NTT_ST(6, 4)
                            NTT_ST(7, 4) NTT_ST(8, 4) NTT_ST(9, 4) }
+                    else { NTT_ST(5, 6) NTT_ST(6, 6) }
 #undef NTT_ST
                     if (!TWO && !first && !last) team_sync(bar_id, TT);   // all reads of W0 done
                     T* db = dst + padpos<T>((hi << lob) | lo);
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
+                    for (int c = 0; c < RV; ++c) {
                         // output position = R << (L-kg) | hi << lob | x | lo  with R = window bits
-                        const uint32_t R = (uint32_t)c >> (4 - kg), x = (uint32_t)c & ((1u << (4 - kg)) - 1);
-                        const uint32_t pos = (R << (L - kg)) | (hi << lob) | (x << (lob - (4 - kg))) | lo;
+                        const uint32_t R = (uint32_t)c >> (RB - kg), x = (uint32_t)c & ((1u << (RB - kg)) - 1);
+                        const uint32_t pos = (R << (L - kg)) | (hi << lob) | (x << (lob - (RB - kg))) | lo;
                         if (last) {
                             T r = ar.fin(v[c]);
                             if (SC) r = ar.mulc(r, a.ninv);
                             gout[pos] = r;
-                        } else db[padpos<T>((R << (L - kg)) | (x << (lob - (4 - kg))))] = v[c];
+                        } else db[padpos<T>((R << (L - kg)) | (x << (lob - (RB - kg))))] = v[c];
                     }
                 }
                 if (!last) {
@@ -461,17 +492,26 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - 4)), 1) k_fast(FastArgs<A> a)
 #define NTT_FAST_MAX_THREADS 1024
 #endif
 constexpr int kFastMaxThreads = NTT_FAST_MAX_THREADS;
+// 64 residues per thread (RB = 6) for 2^11 / 2^12 cuts instructions per
+// butterfly from 10.3 to 7.8 but caps a CTA at 512 threads (128 registers):
+// measured 48 us vs 38 us for RB = 4 on config 2 (4 warps/SMSP cannot hide the
+// dependency latency; profiles/r1/summary.md).  Kept selectable for study.
+#ifndef NTT_FAST_WIDE_RB
+#define NTT_FAST_WIDE_RB 4
+#endif
 
 template <class A, int V, int L>
 struct FastCfg {
     using T = typename A::T;
     using Tw = typename A::Tw;
     static constexpr int N = 1 << L;
-    static constexpr int TT = 1 << (L - 4);
+    // register-block bits (NTT_FAST_WIDE_RB = 6 only where two groups cover the transform)
+    static constexpr int RB = (sizeof(T) == 4 && (L == 11 || L == 12)) ? NTT_FAST_WIDE_RB : 4;
+    static constexpr int TT = 1 << (L - RB);
     static constexpr int NBUF = (V == V_PEASE) ? 3 : 2;
     static constexpr long kSmemCap = 227 * 1024 - 1024;
     static constexpr long table = (long)N * sizeof(Tw);
-    static constexpr long team_bytes = ((long)N + (long)(NBUF - 1) * padded_len<T, L>()) * sizeof(T);
+    static constexpr long team_bytes = ((RB == 4 ? (long)N : 0L) + (long)(NBUF - 1) * padded_len<T, L>()) * sizeof(T);
     static constexpr int by_smem = (int)((kSmemCap - table) / team_bytes);
     static constexpr int by_thr = kFastMaxThreads / TT;
     static constexpr int t0 = by_smem < by_thr ? by_smem : by_thr;
@@ -486,7 +526,7 @@ cudaError_t launch_fast_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int
         *ok = false;
         return cudaSuccess;
     } else {
-        auto kern = a.scale ? k_fast<A, V, L, C::TEAMS, true> : k_fast<A, V, L, C::TEAMS, false>;
+        auto kern = a.scale ? k_fast<A, V, L, C::TEAMS, true, C::RB> : k_fast<A, V, L, C::TEAMS, false, C::RB>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
         if (e != cudaSuccess) return e;
         uint64_t ctas = (a.batch + C::TEAMS - 1) / C::TEAMS;
