@@ -12,6 +12,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <cstdlib>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -242,7 +243,11 @@ struct ntt_plan_s {
     uint64_t ws_bytes = 0;
     void* hbuf = nullptr;
     uint64_t hbuf_bytes = 0;
-    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};   // host-exec pipeline streams
+    // host-exec pipeline: hs[0] H2D copies, hs[1] transforms, hs[2] D2H copies,
+    // chained per chunk by events (kMaxChunks x {copied-in, transformed})
+    static constexpr int kMaxChunks = 64;
+    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t hev[2 * kMaxChunks] = {};
     std::mutex mu;
     ~ntt_plan_s() {
         int cur = 0;
@@ -252,6 +257,8 @@ struct ntt_plan_s {
         if (hbuf) cudaFree(hbuf);
         for (auto st : hs)
             if (st) cudaStreamDestroy(st);
+        for (auto ev : hev)
+            if (ev) cudaEventDestroy(ev);
         if (cor_lo) cudaFree(cor_lo);
         if (cor_hi) cudaFree(cor_hi);
         if (twh) cudaFree(twh);
@@ -530,28 +537,62 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
         for (auto& hs : plan->hs)
             if (!st && !hs && cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking) != cudaSuccess)
                 st = fail(NTT_E_CUDA, "stream creation failed");
+        for (auto& ev : plan->hev)
+            if (!st && !ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+                st = fail(NTT_E_CUDA, "event creation failed");
     }
     cudaError_t e = cudaSuccess;
     // Shared-memory-resident plans need no workspace, so the batch is cut into
-    // chunks pipelined over three streams: H2D of chunk c+1, the transform of c
-    // and the D2H of c-1 overlap (copy engines are full duplex).  Multi-pass
-    // plans share one workspace and run as a single chunk.
+    // chunks: all H2D copies run back to back on one stream, all D2H copies on
+    // another, and the transform of chunk c waits only for its own copy-in
+    // (events) -- both copy engines stay busy (PCIe is full duplex: 55 GB/s
+    // each way alone, 97 GB/s aggregate concurrently; tools/pcie_bw.py).
+    // (A zero-copy variant -- the kernel reading and writing the pinned host
+    // buffers through UVA -- is bit-exact but measured slower: 1.81 vs 1.69 ms
+    // for config 2, tools/pcie_pipe.py.)
+    // Multi-pass plans share one workspace and run as a single chunk.
     const bool resident = ntt_plan_workspace_bytes(plan, 1) == 0;
     uint64_t chunks = 1;
+    // 8 chunks measured best for 64 MiB each way (tools/e2e_sweep.py): every
+    // pinned copy costs ~20 us on the copy engines, so more chunks lose more
+    // than the shorter pipeline fill/drain gains
     if (resident && bytes >= (16ull << 20)) chunks = bytes >= (64ull << 20) ? 8 : 4;
+    static const int env_chunks = [] { const char* v = getenv("NTT_HOST_CHUNKS"); return v ? atoi(v) : 0; }();
+    if (resident && env_chunks > 0) chunks = (uint64_t)env_chunks;     // tuning knob (tools/e2e_sweep.py)
+    if (chunks > (uint64_t)ntt_plan_s::kMaxChunks) chunks = ntt_plan_s::kMaxChunks;
     if (chunks > batch) chunks = batch;
     (void)stream;
     char* d = static_cast<char*>(plan->hbuf);
+    cudaStream_t sH = plan->hs[0], sC = plan->hs[1], sD = plan->hs[2];
+    auto span = [&](uint64_t c, uint64_t& r0, uint64_t& off, uint64_t& nb) {
+        r0 = batch * c / chunks;
+        const uint64_t r1 = batch * (c + 1) / chunks;
+        off = r0 * row_bytes;
+        nb = (r1 - r0) * row_bytes;
+        return r1 - r0;
+    };
+    // enqueue order: every copy-in first (the H2D engine starts at once and
+    // never waits on the host), then the transforms, then every copy-out
+    uint64_t r0, off, nb;
     for (uint64_t c = 0; !st && c < chunks; ++c) {
-        const uint64_t r0 = batch * c / chunks, r1 = batch * (c + 1) / chunks;
-        const uint64_t off = r0 * row_bytes, nb = (r1 - r0) * row_bytes;
-        cudaStream_t s = plan->hs[c % 3];
-        e = cudaMemcpyAsync(d + off, static_cast<const char*>(h_in) + off, nb, cudaMemcpyHostToDevice, s);
-        if (e != cudaSuccess) { st = cuda_fail(e, "H2D copy"); break; }
-        st = exec_device(plan, d + off, d + off, r1 - r0, flags, s);
-        if (st) break;
-        e = cudaMemcpyAsync(static_cast<char*>(h_out) + off, d + off, nb, cudaMemcpyDeviceToHost, s);
-        if (e != cudaSuccess) { st = cuda_fail(e, "D2H copy"); break; }
+        span(c, r0, off, nb);
+        e = cudaMemcpyAsync(d + off, static_cast<const char*>(h_in) + off, nb, cudaMemcpyHostToDevice, sH);
+        if (e == cudaSuccess) e = cudaEventRecord(plan->hev[2 * c], sH);
+        if (e != cudaSuccess) st = cuda_fail(e, "H2D copy");
+    }
+    for (uint64_t c = 0; !st && c < chunks; ++c) {
+        const uint64_t rows = span(c, r0, off, nb);
+        e = cudaStreamWaitEvent(sC, plan->hev[2 * c], 0);
+        if (e != cudaSuccess) { st = cuda_fail(e, "stream wait"); break; }
+        st = exec_device(plan, d + off, d + off, rows, flags, sC);
+        if (!st && (e = cudaEventRecord(plan->hev[2 * c + 1], sC)) != cudaSuccess) st = cuda_fail(e, "event");
+    }
+    for (uint64_t c = 0; !st && c < chunks; ++c) {
+        span(c, r0, off, nb);
+        e = cudaStreamWaitEvent(sD, plan->hev[2 * c + 1], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(static_cast<char*>(h_out) + off, d + off, nb, cudaMemcpyDeviceToHost, sD);
+        if (e != cudaSuccess) st = cuda_fail(e, "D2H copy");
     }
     for (auto hs : plan->hs) {
         cudaError_t e2 = cudaStreamSynchronize(hs);
