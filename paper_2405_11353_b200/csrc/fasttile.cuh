@@ -240,12 +240,34 @@ struct TileGeo {
     static constexpr int K0 = K - 4 * (G - 1);
 };
 
+// --------------------------------------------------------------- cp.async --
+NTT_D void cp_async(void* smem, const void* g, int bytes) {
+    const uint32_t d = fastk::smem_u32(smem);
+    if (bytes == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(g) : "memory");
+    else if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(g) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(g) : "memory");
+}
+NTT_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+NTT_D void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ----------------------------------------------------------------- kernel --
 // per-network twist table shape: w^(r*xr) = lo[xr & 31] * hi[xr >> 5], xr < 2^K
 template <int K> constexpr int twc_lo() { return K < 5 ? (1 << K) : 32; }
 template <int K> constexpr int twc_hi() { return K > 5 ? (1 << (K - 5)) : 1; }
 template <int K> constexpr int tw_row() { return twc_lo<K>() + 1 + twc_hi<K>() + 1; }   // odd-padded rows
 constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
+
+// shared-memory footprint of one k_tile instantiation (bytes)
+template <class T, class Tw, int V, int K, int TQ, int NT, int LAY, int SMB, int TWB>
+constexpr size_t tile_smem_bytes() {
+    constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);
+    constexpr int TT = 1 << (K - 4);
+    constexpr bool ONEBUF = (TQ * TT) / NT == 1;
+    const size_t bufs = (PP && !ONEBUF ? 2 : 1) * (size_t)TQ * tile_stride<T, K, TQ>() * sizeof(T);
+    const size_t head = ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * tw_row<K>() : 0);
+    return ((head + bufs + 15) & ~(size_t)15) + (LAY == 0 ? ((size_t)TQ << K) * sizeof(T) : 0);
+}
+
 
 template <class A, int V, int K, int TQ, int NT, int LAY, int SMB, int TWB>
 __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 2))) k_tile(TileArgs<A> a) {
@@ -259,11 +281,18 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
     constexpr int REP = (TQ * TT) / NT;             // sub-networks per thread per group
     constexpr int VE = 16 / sizeof(T);              // residues per 16-byte vector
     static_assert(REP >= 1 && REP * NT == TQ * TT, "thread count must divide the tile");
+    // ping-pong variants keep ONE work buffer when each thread holds its whole
+    // sub-network in registers across a barrier (REP == 1), as in the
+    // single-pass kernel; the freed space holds the staged NEXT tile
+    constexpr bool ONEBUF = (REP == 1);
+    // staged prefetch of the next tile (variant passes; the six-step layouts
+    // keep whole sub-transform tables in shared memory and gather directly)
+    constexpr bool PF = (LAY == TL_VARIANT);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint32_t Qs[TQ];
     __shared__ uint64_t Rb[TQ];
     // every layout is additive over disjoint bits: gpos(Q, x) = gpos(Q, 0) + gpos(0, x)
-    __shared__ uint64_t Gin[TQ], Gout[TQ];
+    __shared__ uint64_t GinB[2][TQ], Gout[TQ];
     Tw* tws = reinterpret_cast<Tw*>(smem_raw);
     // per-tile twist tables (only when a.twist): network t, j < 32:
     //   twl[t][j] = w^(Q_t * j), twh[t][j] = w^(Q_t * 32 * j)  (rows odd-padded)
@@ -271,7 +300,11 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
     Tw* twl = tws + (1 << SMB);
     Tw* twh = twl + TQ * TSL;
     T* bufA = reinterpret_cast<T*>(smem_raw + ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * tw_row<K>() : 0));
-    T* bufB = PP ? bufA + TQ * NP : bufA;
+    T* bufB = (PP && !ONEBUF) ? bufA + TQ * NP : bufA;
+    // staging buffer: the next tile's input, raw gather order, filled by
+    // cp.async while the current tile runs its register groups
+    T* stage = !PF ? nullptr : reinterpret_cast<T*>(
+        (reinterpret_cast<uintptr_t>(bufA + ((PP && !ONEBUF) ? 2 : 1) * TQ * NP) + 15) & ~(uintptr_t)15);
     A ar;
     ar.init(a.p);
     const int L = a.L, S0 = a.S0;
@@ -300,25 +333,63 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
         return ar.mulc(ar.mulc(v, twl[t * TSL + (xr & 31)]), twh[t * TSH + (xr >> 5)]);
     };
 
+    // network ids of a tile (qmode) -- shared by the prefetch and the tile body
+    auto tileQ = [&](uint64_t tl, uint32_t t) -> uint32_t {
+        const uint32_t tr = (uint32_t)(tl & (tiles_per_row - 1));
+        if (a.qmode == TQM_LINEAR) return tr * TQ + t;
+        if (a.qmode == TQM_REV) return brev(tr * TQ + t, M);
+        const int hb = LTQ - a.la;
+        return (brev(tr * a.TA + (t & (a.TA - 1)), M - hb) << hb) | (t >> a.la);
+    };
+    // issue the cp.async copies of tile tl into the staging buffer (raw order
+    // of the gather loops below: vector i -> stage[i*VE], scalar i -> stage[i])
+    auto prefetch = [&](uint64_t tl, const uint64_t* Gin) {
+        if (a.diag == 2) return;
+        if (a.vec_in && a.in_order == TO_T_FAST) {
+            const uint64_t gb = Gin[(threadIdx.x % (TQ / VE)) * VE];
+#pragma unroll 4
+            for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
+                const uint32_t x = i / (TQ / VE);
+                cp_async(stage + i * VE, a.in + gb + t_gpos_in<A, V, K, LAY>(a, 0u, x), 16);
+            }
+        } else if (a.vec_in && a.in_order == TO_C_FAST) {
+#pragma unroll 4
+            for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
+                const uint32_t t = i / ((1u << K) / VE), x0 = (i % ((1u << K) / VE)) * VE;
+                cp_async(stage + i * VE, a.in + Gin[t] + t_gpos_in<A, V, K, LAY>(a, 0u, x0), 16);
+            }
+        } else {
+#pragma unroll 4
+            for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K); i += NT) {
+                uint32_t t, x;
+                if (a.in_order == TO_C_FAST) { t = i >> K; x = i & ((1u << K) - 1); }
+                else if (a.in_order == TO_T_FAST) { t = i % TQ; x = i / TQ; }
+                else { const int lb = LTQ - a.la; const uint32_t tb = i & ((1u << lb) - 1), ta = (i >> lb) & (a.TA - 1); t = ta + (tb << a.la); x = i / TQ; }
+                cp_async(stage + i, a.in + Gin[t] + t_gpos_in<A, V, K, LAY>(a, 0u, x), (int)sizeof(T));
+            }
+        }
+    };
+    int pbuf = 0;
+    if (threadIdx.x < TQ && (uint64_t)blockIdx.x < ntiles) {
+        const uint64_t row = (uint64_t)blockIdx.x >> ltpr;
+        GinB[0][threadIdx.x] = row * N + t_gpos_in<A, V, K, LAY>(a, tileQ(blockIdx.x, threadIdx.x), 0);
+    }
+    __syncthreads();
+    if (PF && (uint64_t)blockIdx.x < ntiles) prefetch(blockIdx.x, GinB[0]);
+    cp_async_commit();
+
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        __syncthreads();
+        __syncthreads();                       // previous tile's scatter done with the work buffers
         if (threadIdx.x < TQ) {
             const int t = threadIdx.x;
             const uint64_t row = tile >> ltpr;
-            const uint32_t tr = (uint32_t)(tile & (tiles_per_row - 1));
-            uint32_t Q;
-            if (a.qmode == TQM_LINEAR) Q = tr * TQ + t;
-            else if (a.qmode == TQM_REV) Q = brev(tr * TQ + t, M);
-            else {
-                const int hb = LTQ - a.la;
-                Q = (brev(tr * a.TA + (t & (a.TA - 1)), M - hb) << hb) | (t >> a.la);
-            }
+            const uint32_t Q = tileQ(tile, t);
             Qs[t] = Q;
             Rb[t] = row * N;
-            Gin[t] = row * N + t_gpos_in<A, V, K, LAY>(a, Q, 0);
             Gout[t] = row * N + t_gpos_out<A, V, K, LAY>(a, Q, 0);
         }
-        __syncthreads();
+        cp_async_wait_all();
+        __syncthreads();                       // staged tile landed (all threads' copies); Qs visible
         if (TWB && a.twist) {                 // per-network twist tables from the main table w^i
             const uint64_t nm = N - 1;
             const int sh = L - S0 - K;
@@ -335,13 +406,14 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
         // ---- gather (16-byte vectors along the contiguous run when valid)
         if (a.diag == 2) {
         } else if (a.vec_in && a.in_order == TO_T_FAST) {
-            const uint64_t gb = Gin[(threadIdx.x % (TQ / VE)) * VE];
+            const uint64_t gb = GinB[pbuf][(threadIdx.x % (TQ / VE)) * VE];
 #pragma unroll 4
             for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
                 const uint32_t t0 = (i % (TQ / VE)) * VE, x = i / (TQ / VE);
-                const T* src = a.in + gb + t_gpos_in<A, V, K, LAY>(a, 0u, x);
                 T tmp[VE];
-                *reinterpret_cast<uint4*>(tmp) = __ldg(reinterpret_cast<const uint4*>(src));
+                *reinterpret_cast<uint4*>(tmp) =
+                    PF ? *reinterpret_cast<const uint4*>(stage + i * VE)
+                       : __ldg(reinterpret_cast<const uint4*>(a.in + gb + t_gpos_in<A, V, K, LAY>(a, 0u, x)));
 #pragma unroll
                 for (int e = 0; e < VE; ++e) {
                     T v = tmp[e];
@@ -353,9 +425,10 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
 #pragma unroll 4
             for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
                 const uint32_t t = i / ((1u << K) / VE), x0 = (i % ((1u << K) / VE)) * VE;
-                const T* src = a.in + Gin[t] + t_gpos_in<A, V, K, LAY>(a, 0u, x0);
                 T tmp[VE];
-                *reinterpret_cast<uint4*>(tmp) = __ldg(reinterpret_cast<const uint4*>(src));
+                *reinterpret_cast<uint4*>(tmp) =
+                    PF ? *reinterpret_cast<const uint4*>(stage + i * VE)
+                       : __ldg(reinterpret_cast<const uint4*>(a.in + GinB[pbuf][t] + t_gpos_in<A, V, K, LAY>(a, 0u, x0)));
 #pragma unroll
                 for (int e = 0; e < VE; ++e) {
                     T v = tmp[e];
@@ -370,12 +443,28 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
                 if (a.in_order == TO_C_FAST) { t = i >> K; x = i & ((1u << K) - 1); }
                 else if (a.in_order == TO_T_FAST) { t = i % TQ; x = i / TQ; }
                 else { const int lb = LTQ - a.la; const uint32_t tb = i & ((1u << lb) - 1), ta = (i >> lb) & (a.TA - 1); t = ta + (tb << a.la); x = i / TQ; }
-                T v = __ldg(a.in + Gin[t] + t_gpos_in<A, V, K, LAY>(a, 0u, x));
+                T v = PF ? stage[i] : __ldg(a.in + GinB[pbuf][t] + t_gpos_in<A, V, K, LAY>(a, 0u, x));
                 if (TWB && a.twist && a.twist < 3) v = twistv(v, t, a.rev_local ? brev(x, K) : x);
                 bufA[t * NP + padpos<T>(a.rev_local ? brev(x, K) : x)] = v;
             }
         }
-        __syncthreads();
+        __syncthreads();                       // staging consumed, tile in the work buffer
+        {                                      // prefetch the next tile behind this one's compute
+            const uint64_t nxt = tile + gridDim.x;
+            if (nxt < ntiles && !PF) {         // direct gather next time: just its bases
+                if (threadIdx.x < TQ)
+                    GinB[pbuf ^ 1][threadIdx.x] =
+                        (nxt >> ltpr) * N + t_gpos_in<A, V, K, LAY>(a, tileQ(nxt, threadIdx.x), 0);
+            } else if (nxt < ntiles) {
+                if (threadIdx.x < TQ)
+                    GinB[pbuf ^ 1][threadIdx.x] =
+                        (nxt >> ltpr) * N + t_gpos_in<A, V, K, LAY>(a, tileQ(nxt, threadIdx.x), 0);
+                __syncthreads();
+                prefetch(nxt, GinB[pbuf ^ 1]);
+            }
+            cp_async_commit();
+            pbuf ^= 1;
+        }
 
         // ---- register groups
         T* src = bufA;
@@ -440,6 +529,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
                     else { NTT_TPE(1, 4) NTT_TPE(2, 4) NTT_TPE(3, 4) NTT_TPE(4, 4) NTT_TPE(5, 4) NTT_TPE(6, 4)
                            NTT_TPE(7, 4) NTT_TPE(8, 4) NTT_TPE(9, 4) }
 #undef NTT_TPE
+                    if (PP && ONEBUF) __syncthreads();      // every read of the (single) buffer done
                     T* wbo = db + padpos<T>(u << (4 - kg));
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
@@ -469,6 +559,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
                     else { NTT_TST(1, 4) NTT_TST(2, 4) NTT_TST(3, 4) NTT_TST(4, 4) NTT_TST(5, 4) NTT_TST(6, 4)
                            NTT_TST(7, 4) NTT_TST(8, 4) NTT_TST(9, 4) }
 #undef NTT_TST
+                    if (PP && ONEBUF) __syncthreads();
                     T* wbo = db + padpos<T>((hi << lob) | lo);
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
@@ -538,8 +629,7 @@ cudaError_t launch_tile(const TileArgs<A>& a, cudaStream_t s, int num_sms, int* 
     using T = typename A::T;
     using Tw = typename A::Tw;
     constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);
-    constexpr size_t smem = ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * tw_row<K>() : 0) +
-                            (PP ? 2 : 1) * (size_t)TQ * tile_stride<T, K, TQ>() * sizeof(T);
+    constexpr size_t smem = tile_smem_bytes<T, Tw, V, K, TQ, NT, LAY, SMB, TWB>();
     if (a.twist && K > 10) return cudaErrorInvalidValue;   // twist tables cover xr < 2^10
     auto kern = k_tile<A, V, K, TQ, NT, LAY, SMB, TWB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
