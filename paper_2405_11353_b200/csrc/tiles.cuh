@@ -46,6 +46,7 @@ cudaError_t pass_any(int K, const TileArgs<A>& a, cudaStream_t s, int sms, int* 
     *ok = true;
     if (sizeof(T) == 4) {
         switch (K) {
+            case 6: return pass_k<A, V, 6>(a, s, sms, launches);
             case 7: return pass_k<A, V, 7>(a, s, sms, launches);
             case 8: return pass_k<A, V, 8>(a, s, sms, launches);
             case 9: return pass_k<A, V, 9>(a, s, sms, launches);
@@ -70,16 +71,17 @@ inline int tile_diag() {
 
 // Pass plan.  Tiles hold 2^13 (u32) / 2^12 (u64) residues, so a pass of K
 // stages has TQ = 2^(13-K) networks and every strided HBM side moves runs of
-// TQ residues.  Measured on B200 (profiles/r1/summary.md): the tile kernel is
-// issue/latency bound, not run-length bound -- a 3-pass 2^20 plan with 256 B
-// runs (K = 7,7,6) ran 10.1 ms against 4.8 ms for 2 passes of K = 10 with
-// 32 B runs, because per-pass overhead instructions dominate.  So: fewest
-// passes, K <= 10.
+// TQ residues.  Measured on B200 (profiles/r1/summary.md): a 3-pass 2^20 plan
+// with 256 B runs (K = 7,7,6) ran 9-11 ms against 4.6 ms for 2 passes of
+// K = 10 with 32 B runs: the TQ >= 32 tiles fit one CTA per SM and their
+// 8-thread networks share warps with bank-conflicting strides.  So: fewest
+// passes, K <= 10 (NTT_TILE_KMAX overrides, for experiments).
 inline int tile_plan(int L, int word, int* K) {
     int kmax;
-    if (word == 4) kmax = 10;
+    static const int env_kmax = [] { const char* v = getenv("NTT_TILE_KMAX"); return v ? atoi(v) : 0; }();
+    if (word == 4) kmax = env_kmax ? env_kmax : 10;   // NTT_TILE_KMAX: plan experiments (tools/time_case.py)
     else kmax = 9;
-    const int kmin = 7;
+    const int kmin = 6;
     int P = (L + kmax - 1) / kmax;
     if (P < 2) P = 2;
     for (int i = 0; i < P; ++i) K[i] = L / P + (i < L % P ? 1 : 0);
