@@ -14,7 +14,7 @@ import threading
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libntt_b200.so")
+LIB_PATH = os.environ.get("NTT_LIB_PATH") or os.path.join(_HERE, "libntt_b200.so")   # override: experiments only
 
 NTT_OK = 0
 _STATUS_EXC = {

@@ -52,3 +52,22 @@ for _ in range(10):
     dp.exec_device(hin.data_ptr(), hout.data_ptr(), w.batch, False, sC.cuda_stream)
 torch.cuda.synchronize()
 print(f"zero-copy: {(time.perf_counter() - t0) / 10 * 1e3:.3f} ms")
+
+# hybrid: copy engine for H2D, the transform stores straight into pinned host memory
+def run_hybrid(chunks):
+    rows = w.batch // chunks
+    for c in range(chunks):
+        sl = slice(c * rows, (c + 1) * rows)
+        with torch.cuda.stream(sH):
+            d[sl].copy_(hin[sl], non_blocking=True)
+            e = torch.cuda.Event(); e.record(sH)
+        sC.wait_event(e)
+        dp.exec_device(d[sl].data_ptr(), hout[sl].data_ptr(), rows, False, sC.cuda_stream)
+    torch.cuda.synchronize()
+for chunks in (4, 8, 16):
+    hout.zero_()
+    run_hybrid(chunks)
+    ok = bool(torch.equal(hout, ref))
+    t0 = time.perf_counter()
+    for _ in range(10): run_hybrid(chunks)
+    print(f"hybrid chunks={chunks}: {(time.perf_counter() - t0) / 10 * 1e3:.3f} ms, equal={ok}")
