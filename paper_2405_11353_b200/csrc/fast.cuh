@@ -139,6 +139,16 @@ struct FastArgs {
     unsigned long long* counters;
 };
 
+// DIT-type butterfly of global stage s (1-based) of a single-pass transform:
+// stage 1 sees canonical inputs, stage 2 inputs in [0,2p) (lazy bounds)
+// (s is a compile-time constant after the callers' loops unroll)
+template <class A>
+NTT_D void dit_stage_bf(const A& ar, int s, typename A::T& x, typename A::T& y, const typename A::Tw* w, bool triv) {
+    if (s == 1) ar.dit1_c(x, y);
+    else if (s == 2) { if (triv) ar.dit1_2p(x, y); else ar.dit_2p(x, y, *w); }
+    else { if (triv) ar.dit1(x, y); else ar.dit(x, y, *w); }
+}
+
 // ---------------------------------------------------------------- DIT/DIF --
 // In-place window [b0, b0+kg) of a register block [B, B+4); pbase = position
 // of register 0.  DIT: stages b0+1.. ascending; DIF: descending.
@@ -160,11 +170,15 @@ NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[RN], uint32_t pbase, cons
             if (c & (1 << (off + j))) continue;
             const uint32_t kc = ((uint32_t)c << B) & kmask;      // compile-time part of k
             const int hi = c | (1 << (off + j));
-            if (s == 1 || (B == 0 && kc == 0)) {                  // w^0 = 1
-                if (DIF) ar.dif1(v[c], v[hi]); else ar.dit1(v[c], v[hi]);
+            const bool triv = (s == 1 || (B == 0 && kc == 0));      // w^0 = 1
+            if (DIF) {
+                if (triv) ar.dif1(v[c], v[hi]);
+                else ar.dif(v[c], v[hi], row[kc]);
+            } else if (B == 0) {
+                dit_stage_bf(ar, s, v[c], v[hi], row + kc, triv);
             } else {
-                const typename A::Tw w = row[kc];
-                if (DIF) ar.dif(v[c], v[hi], w); else ar.dit(v[c], v[hi], w);
+                if (triv) ar.dit1(v[c], v[hi]);
+                else ar.dit(v[c], v[hi], row[kc]);
             }
         }
     }
@@ -194,8 +208,11 @@ NTT_D void pease_regs(const A& ar, typename A::T (&v)[RN], uint32_t ubase, const
                 const uint32_t R = 2u * i;
                 const uint32_t Bp = R >> (kg - m);               // output bits so far (m bits)
                 T x = v[n * (1 << kg) + 2 * i], y = v[n * (1 << kg) + 2 * i + 1];
-                if (s == 1 || (sg == 0 && Bp == 0)) ar.dit1(x, y);     // w^0 (k = Bp when sg == 0)
-                else ar.dit(x, y, stw[(1u << (s - 1)) + ((Bp << sg) | qtop)]);
+                const bool triv = (s == 1 || (sg == 0 && Bp == 0));     // w^0 (k = Bp when sg == 0)
+                const typename A::Tw* wp = stw + (1u << (s - 1)) + ((Bp << sg) | qtop);
+                if (sg == 0) dit_stage_bf(ar, s, x, y, wp, triv);
+                else if (triv) ar.dit1(x, y);
+                else ar.dit(x, y, *wp);
                 nv[i] = x;
                 nv[i + H] = y;
             }
@@ -226,8 +243,11 @@ NTT_D void stockham_regs(const A& ar, typename A::T (&v)[RN], uint32_t hi, const
             for (int i = 0; i < H; ++i) {
                 const uint32_t Bv = i & ((1u << m) - 1), crest = (uint32_t)i >> m;
                 T a = v[(i << (RB - kg)) | x], b = v[((i + H) << (RB - kg)) | x];
-                if (s == 0 || (sg == 0 && Bv == 0)) ar.dit1(a, b);     // w^0 (j = Bv when sg == 0)
-                else ar.dit(a, b, stw[(1u << s) + ((Bv << sg) | hi)]);
+                const bool triv = (s == 0 || (sg == 0 && Bv == 0));     // w^0 (j = Bv when sg == 0)
+                const typename A::Tw* wp = stw + (1u << s) + ((Bv << sg) | hi);
+                if (sg == 0) dit_stage_bf(ar, s + 1, a, b, wp, triv);
+                else if (triv) ar.dit1(a, b);
+                else ar.dit(a, b, *wp);
                 nv[(crest << (m + 1)) | Bv] = a;
                 nv[(crest << (m + 1)) | (1u << m) | Bv] = b;
             }

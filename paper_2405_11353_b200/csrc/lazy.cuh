@@ -39,6 +39,26 @@ struct LazyF32 {
         x = add4(xr, t);
         y = xr - t + p2;
     }
+    // stage 1 of a single-pass transform: canonical inputs (the reference's
+    // precondition, modmath.py:112), twiddle 1 -> outputs in [0,2p)
+    NTT_D void dit1_c(T& x, T& y) const {
+        const T a = x;
+        x = a + y;
+        y = a - y + p;
+    }
+    // stage 2: inputs in [0,2p) need no reduction before the butterfly
+    NTT_D void dit_2p(T& x, T& y, Tw w) const {
+        const T q = __umulhi(y, w.y);
+        const T t = y * w.x - q * p;
+        const T a = x;
+        x = add4(a, t);
+        y = a - t + p2;
+    }
+    NTT_D void dit1_2p(T& x, T& y) const {
+        const T a = x;
+        x = a + y;
+        y = a - y + p2;
+    }
     // DIF butterfly: (x, y) -> (x + y, w*(x - y)); in/out [0,2p)
     NTT_D void dif(T& x, T& y, Tw w) const {
         const T s = x + y;
@@ -84,6 +104,10 @@ struct Canon {
         x = f.add(a, y);
         y = f.sub(a, y);
     }
+    // canonical policies: the bounded first-stage forms are the plain ones
+    NTT_D void dit1_c(T& x, T& y) const { dit1(x, y); }
+    NTT_D void dit_2p(T& x, T& y, Tw w) const { dit(x, y, w); }
+    NTT_D void dit1_2p(T& x, T& y) const { dit1(x, y); }
     NTT_D void dif(T& x, T& y, Tw w) const {
         const T a = x, b = y;
         x = f.add(a, b);
