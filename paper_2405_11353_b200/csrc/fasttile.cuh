@@ -19,6 +19,13 @@
 #include <cstdint>
 #include "fast.cuh"
 
+// staged prefetch for 64-bit tiles: off by default -- the Goldilocks passes are
+// integer-bound, and the 32 KiB staging buffer costs them a resident CTA
+// (config 3: 0.385 -> 0.399 ms with it)
+#ifndef NTT_TILE_PF_U64
+#define NTT_TILE_PF_U64 0
+#endif
+
 namespace nttb200 {
 namespace ftile {
 
@@ -265,7 +272,7 @@ constexpr size_t tile_smem_bytes() {
     constexpr bool ONEBUF = (TQ * TT) / NT == 1;
     const size_t bufs = (PP && !ONEBUF ? 2 : 1) * (size_t)TQ * tile_stride<T, K, TQ>() * sizeof(T);
     const size_t head = ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * tw_row<K>() : 0);
-    return ((head + bufs + 15) & ~(size_t)15) + (LAY == 0 ? ((size_t)TQ << K) * sizeof(T) : 0);
+    return ((head + bufs + 15) & ~(size_t)15) + ((LAY == 0 && NTT_TILE_PF_U64 >= (int)sizeof(T) - 4) ? ((size_t)TQ << K) * sizeof(T) : 0);
 }
 
 
@@ -287,7 +294,7 @@ __global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 
     constexpr bool ONEBUF = (REP == 1);
     // staged prefetch of the next tile (variant passes; the six-step layouts
     // keep whole sub-transform tables in shared memory and gather directly)
-    constexpr bool PF = (LAY == TL_VARIANT);
+    constexpr bool PF = (LAY == TL_VARIANT) && NTT_TILE_PF_U64 >= (int)sizeof(T) - 4;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint32_t Qs[TQ];
     __shared__ uint64_t Rb[TQ];
