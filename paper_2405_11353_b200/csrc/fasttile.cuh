@@ -277,7 +277,7 @@ constexpr size_t tile_smem_bytes() {
 
 
 template <class A, int V, int K, int TQ, int NT, int LAY, int SMB, int TWB>
-__global__ void __launch_bounds__(NT, (LAY != TL_VARIANT ? 1 : (NT <= 256 ? 3 : 2))) k_tile(TileArgs<A> a) {
+__global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (NT <= 256 ? 3 : 2))) k_tile(TileArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
     using GG = TileGeo<K, TQ>;

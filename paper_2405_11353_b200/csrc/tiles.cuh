@@ -24,13 +24,20 @@ __global__ void k_copy_rows(const T* src, T* dst, uint64_t n, uint64_t rows, uns
 
 namespace ftile {
 
-// Compile-time tile shapes: residues per tile = 2^TE (u32: 2^13, u64: 2^12).
-template <class T>
-constexpr int tile_e() { return sizeof(T) == 4 ? 13 : 12; }
+// Compile-time tile shapes: residues per tile = 2^TE (u32: 2^13, u64: 2^12),
+// except u32 K = 10 passes: 2^14 (TQ = 16 networks, one 1024-thread CTA per
+// SM) -- the strided HBM side then moves 64-byte runs instead of 32-byte ones
+// (a 32-byte-run strided write pass cannot beat 2.2 TB/s).
+#ifndef NTT_TILE_E32_K10
+#define NTT_TILE_E32_K10 14
+#endif
+constexpr int tile_e_rt(int word, int K) { return word == 4 ? (K == 10 ? NTT_TILE_E32_K10 : 13) : 12; }
 template <class T, int K>
-constexpr int tile_tq() { return 1 << (tile_e<T>() - K); }
+constexpr int tile_e() { return tile_e_rt((int)sizeof(T), K); }
 template <class T, int K>
-constexpr int tile_nt() { return (tile_tq<T, K>() << (K - 4)) < 512 ? (tile_tq<T, K>() << (K - 4)) : 512; }
+constexpr int tile_tq() { return 1 << (tile_e<T, K>() - K); }
+template <class T, int K>
+constexpr int tile_nt() { return (tile_tq<T, K>() << (K - 4)) < 1024 ? (tile_tq<T, K>() << (K - 4)) : 1024; }
 constexpr int kSmb = 11;
 
 template <class A, int V, int K>
@@ -153,7 +160,7 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
         a.count_row = last;
         a.scale = last ? r.scale : 0;
         int k = K[i];
-        const int tq = 1 << (tile_e<T>() - k);
+        const int tq = 1 << (tile_e_rt((int)sizeof(T), k) - k);
         bool okp = false;
         if (fac) a.tw_lo = static_cast<const typename A::Tw*>(r.tw);     // main table w^i
         if (V == V_DIT || V == V_FLAT) {
@@ -177,7 +184,7 @@ cudaError_t run_tile_passes(const MultipassReq& r, bool* ok) {
             } else {
                 a.qmode = TQM_LINEAR; a.in_order = TO_T_FAST; a.out_order = TO_T_FAST;
             }
-            a.vec_in = a.vec_out = al && (1 << (tile_e<T>() - k)) >= VE;
+            a.vec_in = a.vec_out = al && (1 << (tile_e_rt((int)sizeof(T), k) - k)) >= VE;
             if (fac && !last) { a.twist = 3; a.tw_rsel = 0; }
             e = pass_any<A, V_DIF>(k, a, r.stream, r.num_sms, r.launches, &okp);
             done += k;
