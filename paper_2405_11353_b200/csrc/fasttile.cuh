@@ -334,10 +334,12 @@ __global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (
     const int S0t = loc ? 0 : S0;
     const int Lg = loc ? K : L;
     // twist factor w^(Q_t * xr) = twl[t][xr mod 32] * twh[t][xr >> 5] applied to v
-    auto twistv = [&](T v, uint32_t t, uint32_t x) -> T {
-        const uint32_t xr = (a.twist == 2) ? x : brev(x, K);
+    auto twistr = [&](T v, uint32_t t, uint32_t xr) -> T {     // xr = the exponent's local index
         if (K <= 5) return ar.mulc(v, twl[t * TSL + xr]);
         return ar.mulc(ar.mulc(v, twl[t * TSL + (xr & 31)]), twh[t * TSH + (xr >> 5)]);
+    };
+    auto twistv = [&](T v, uint32_t t, uint32_t x) -> T {
+        return twistr(v, t, (a.twist == 2) ? x : brev(x, K));
     };
 
     // network ids of a tile (qmode) -- shared by the prefetch and the tile body
@@ -421,11 +423,15 @@ __global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (
                 *reinterpret_cast<uint4*>(tmp) =
                     PF ? *reinterpret_cast<const uint4*>(stage + i * VE)
                        : __ldg(reinterpret_cast<const uint4*>(a.in + gb + t_gpos_in<A, V, K, LAY>(a, 0u, x)));
+                // one position per vector: local index, its padded offset and the twist index
+                const uint32_t xl = a.rev_local ? brev(x, K) : x;
+                const uint32_t xr = (a.twist == 2) ? xl : brev(xl, K);
+                T* db = bufA + t0 * NP + padpos<T>(xl);
 #pragma unroll
                 for (int e = 0; e < VE; ++e) {
                     T v = tmp[e];
-                    if (TWB && a.twist && a.twist < 3) v = twistv(v, t0 + e, a.rev_local ? brev(x, K) : x);
-                    bufA[(t0 + e) * NP + padpos<T>(a.rev_local ? brev(x, K) : x)] = v;
+                    if (TWB && a.twist && a.twist < 3) v = twistr(v, t0 + e, xr);
+                    db[e * NP] = v;
                 }
             }
         } else if (a.vec_in && a.in_order == TO_C_FAST) {
@@ -436,11 +442,21 @@ __global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (
                 *reinterpret_cast<uint4*>(tmp) =
                     PF ? *reinterpret_cast<const uint4*>(stage + i * VE)
                        : __ldg(reinterpret_cast<const uint4*>(a.in + GinB[pbuf][t] + t_gpos_in<A, V, K, LAY>(a, 0u, x0)));
+                // x0 + e and its K-bit reversal brev(x0) | brev(e) << (K-2) split into a
+                // per-vector part and a compile-time part (disjoint bits: padpos is additive)
+                constexpr int EB = VE == 4 ? 2 : 1;
+                const uint32_t nat0 = x0, rev0 = brev(x0, K);
+                T* db = bufA + t * NP + padpos<T>(a.rev_local ? rev0 : nat0);
 #pragma unroll
                 for (int e = 0; e < VE; ++e) {
+                    const uint32_t ce = (uint32_t)e, cr = brev((uint32_t)e, EB) << (K - EB);
                     T v = tmp[e];
-                    if (TWB && a.twist && a.twist < 3) v = twistv(v, t, a.rev_local ? brev(x0 + e, K) : x0 + e);
-                    bufA[t * NP + padpos<T>(a.rev_local ? brev(x0 + e, K) : x0 + e)] = v;
+                    if (TWB && a.twist && a.twist < 3) {
+                        // twist 1: xr = brev(xl); twist 2: xr = xl
+                        const bool xr_rev = (a.twist == 2) == (a.rev_local != 0);
+                        v = twistr(v, t, xr_rev ? (rev0 | cr) : (nat0 + ce));
+                    }
+                    db[padpos<T>(a.rev_local ? cr : ce)] = v;
                 }
             }
         } else {
