@@ -35,7 +35,11 @@ using fastk::Perm;
 using fastk::plan_lanes;
 using fastk::scatter_bits;
 
-enum TileLayout { TL_VARIANT = 0, TL_SIX_A = 1, TL_SIX_B = 2 };
+// TL_COLS: a DIT pass over the column index j of an [2^L][2^l1] row-major
+// matrix (element (i, j) at i + j*2^l1) for all 2^l1 columns at once; the
+// network id is Q = i | Qj << l1, so consecutive networks of a tile are
+// consecutive columns and both HBM sides move runs of TQ residues
+enum TileLayout { TL_VARIANT = 0, TL_SIX_A = 1, TL_SIX_B = 2, TL_COLS = 3 };
 enum TileQ { TQM_LINEAR = 1, TQM_REV = 2, TQM_2D = 3 };
 enum TileOrder { TO_C_FAST = 0, TO_T_FAST = 1, TO_TB_FAST = 2 };
 
@@ -76,6 +80,7 @@ struct TileArgs {
     const T* cor_lo;
     const T* cor_hi;
     int cor_lb;
+    int cor_on;                // TL_COLS: multiply by w_N^(i * k2) in the scatter (six-step correction)
     unsigned long long* counters;
 };
 
@@ -84,6 +89,12 @@ NTT_D uint64_t t_gpos_in(const TileArgs<A>& a, uint32_t Q, uint32_t x) {
     if (LAY == TL_SIX_A) return ((uint64_t)x << a.l1) | Q;
     if (LAY == TL_SIX_B) return ((uint64_t)x << a.l2) | Q;
     const int L = a.L, S0 = a.S0;
+    if (LAY == TL_COLS) {
+        const uint32_t Qj = Q >> a.l1;
+        uint64_t g = (Qj & ((1u << S0) - 1)) | ((uint64_t)x << S0) | ((uint64_t)(Qj >> S0) << (S0 + K));
+        if (a.rev_in) g = brev((uint32_t)g, L);
+        return (Q & ((1u << a.l1) - 1)) | (g << a.l1);
+    }
     uint64_t g;
     if (V == V_PEASE || V == V_PEASE_NC) g = ((uint64_t)Q << K) | x;
     else if (V == V_STOCKHAM) {
@@ -99,6 +110,11 @@ NTT_D uint64_t t_gpos_out(const TileArgs<A>& a, uint32_t Q, uint32_t x) {
         return (uint64_t)(x >> a.pb) * a.pblk + ((uint64_t)Q << a.pb) + (x & ((1u << a.pb) - 1));
     if (LAY == TL_SIX_B) return ((uint64_t)x << a.l2) | Q;
     const int L = a.L, S0 = a.S0;
+    if (LAY == TL_COLS) {
+        const uint32_t Qj = Q >> a.l1;
+        const uint64_t g = (Qj & ((1u << S0) - 1)) | ((uint64_t)x << S0) | ((uint64_t)(Qj >> S0) << (S0 + K));
+        return (Q & ((1u << a.l1) - 1)) | (g << a.l1);
+    }
     uint64_t g;
     if (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM) {
         if (a.out_trb) return ((uint64_t)x << (L - K)) | brev(Q, L - K);
@@ -277,7 +293,7 @@ constexpr size_t tile_smem_bytes() {
 
 
 template <class A, int V, int K, int TQ, int NT, int LAY, int SMB, int TWB>
-__global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (NT <= 256 ? 3 : 2))) k_tile(TileArgs<A> a) {
+__global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT >= 1024) ? 1 : (NT <= 256 ? 3 : 2))) k_tile(TileArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
     using GG = TileGeo<K, TQ>;
@@ -297,6 +313,7 @@ __global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (
     constexpr bool PF = (LAY == TL_VARIANT) && NTT_TILE_PF_U64 >= (int)sizeof(T) - 4;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint32_t Qs[TQ];
+    __shared__ uint32_t Is[LAY == TL_COLS ? TQ : 1];   // TL_COLS: column index i of each network
     __shared__ uint64_t Rb[TQ];
     // every layout is additive over disjoint bits: gpos(Q, x) = gpos(Q, 0) + gpos(0, x)
     __shared__ uint64_t GinB[2][TQ], Gout[TQ];
@@ -315,8 +332,9 @@ __global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (
     A ar;
     ar.init(a.p);
     const int L = a.L, S0 = a.S0;
-    const int M = (LAY == TL_VARIANT) ? L - K : (LAY == TL_SIX_A ? a.l1 : a.l2);
+    const int M = (LAY == TL_VARIANT) ? L - K : (LAY == TL_SIX_A ? a.l1 : (LAY == TL_SIX_B ? a.l2 : a.l1 + L - K));
     const uint64_t N = 1ull << L;
+    const uint64_t RS = (LAY == TL_COLS) ? (1ull << (L + a.l1)) : N;   // row stride of a batch
     constexpr int LTQ = ilog2c(TQ);
     const int ltpr = M - LTQ;                          // log2 tiles per row
     const uint64_t tiles_per_row = 1ull << ltpr;
@@ -330,7 +348,7 @@ __global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (
     };
     // local mode: six-step sub-transforms, or a late pass factorised into
     // twist + local transform -- stage twiddles from the local table prefix only
-    const bool loc = (LAY != TL_VARIANT) || a.twist;
+    const bool loc = (LAY == TL_SIX_A || LAY == TL_SIX_B) || a.twist;
     const int S0t = loc ? 0 : S0;
     const int Lg = loc ? K : L;
     // twist factor w^(Q_t * xr) = twl[t][xr mod 32] * twh[t][xr >> 5] applied to v
@@ -381,7 +399,7 @@ __global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (
     int pbuf = 0;
     if (threadIdx.x < TQ && (uint64_t)blockIdx.x < ntiles) {
         const uint64_t row = (uint64_t)blockIdx.x >> ltpr;
-        GinB[0][threadIdx.x] = row * N + t_gpos_in<A, V, K, LAY>(a, tileQ(blockIdx.x, threadIdx.x), 0);
+        GinB[0][threadIdx.x] = row * RS + t_gpos_in<A, V, K, LAY>(a, tileQ(blockIdx.x, threadIdx.x), 0);
     }
     __syncthreads();
     if (PF && (uint64_t)blockIdx.x < ntiles) prefetch(blockIdx.x, GinB[0]);
@@ -393,9 +411,10 @@ __global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (
             const int t = threadIdx.x;
             const uint64_t row = tile >> ltpr;
             const uint32_t Q = tileQ(tile, t);
-            Qs[t] = Q;
-            Rb[t] = row * N;
-            Gout[t] = row * N + t_gpos_out<A, V, K, LAY>(a, Q, 0);
+            Qs[t] = (LAY == TL_COLS) ? (Q >> a.l1) : Q;      // twiddle-carrying part
+            if (LAY == TL_COLS) Is[t] = Q & ((1u << a.l1) - 1);
+            Rb[t] = row * RS;
+            Gout[t] = row * RS + t_gpos_out<A, V, K, LAY>(a, Q, 0);
         }
         cp_async_wait_all();
         __syncthreads();                       // staged tile landed (all threads' copies); Qs visible
@@ -477,11 +496,11 @@ __global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (
             if (nxt < ntiles && !PF) {         // direct gather next time: just its bases
                 if (threadIdx.x < TQ)
                     GinB[pbuf ^ 1][threadIdx.x] =
-                        (nxt >> ltpr) * N + t_gpos_in<A, V, K, LAY>(a, tileQ(nxt, threadIdx.x), 0);
+                        (nxt >> ltpr) * RS + t_gpos_in<A, V, K, LAY>(a, tileQ(nxt, threadIdx.x), 0);
             } else if (nxt < ntiles) {
                 if (threadIdx.x < TQ)
                     GinB[pbuf ^ 1][threadIdx.x] =
-                        (nxt >> ltpr) * N + t_gpos_in<A, V, K, LAY>(a, tileQ(nxt, threadIdx.x), 0);
+                        (nxt >> ltpr) * RS + t_gpos_in<A, V, K, LAY>(a, tileQ(nxt, threadIdx.x), 0);
                 __syncthreads();
                 prefetch(nxt, GinB[pbuf ^ 1]);
             }
@@ -605,6 +624,13 @@ __global__ void __launch_bounds__(NT, ((LAY != TL_VARIANT || NT >= 1024) ? 1 : (
                 const T w = ar.mulfull(__ldg(a.cor_hi + (e >> a.cor_lb)), __ldg(a.cor_lo + (e & ((1ull << a.cor_lb) - 1))));
                 r = ar.mulfull(r, w);
             }
+            if (LAY == TL_COLS && a.cor_on) {   // w_N^(i * k2), k2 = the column output index (natural order)
+                const uint32_t Qj = Qs[t];
+                const uint64_t k2 = (Qj & ((1u << a.S0) - 1)) | ((uint64_t)x << a.S0) | ((uint64_t)(Qj >> a.S0) << (a.S0 + K));
+                const uint64_t e = ((uint64_t)Is[t] * k2) & ((1ull << (L + a.l1)) - 1);
+                const T w = ar.mulfull(__ldg(a.cor_hi + (e >> a.cor_lb)), __ldg(a.cor_lo + (e & ((1ull << a.cor_lb) - 1))));
+                r = ar.mulfull(r, w);
+            }
             if (a.scale) r = ar.mulc(r, a.ninv);
             return r;
         };
@@ -661,7 +687,7 @@ cudaError_t launch_tile(const TileArgs<A>& a, cudaStream_t s, int num_sms, int* 
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
-    const int M = LAY == TL_VARIANT ? a.L - K : (LAY == TL_SIX_A ? a.l1 : a.l2);
+    const int M = LAY == TL_VARIANT ? a.L - K : (LAY == TL_SIX_A ? a.l1 : (LAY == TL_SIX_B ? a.l2 : a.l1 + a.L - K));
     const uint64_t ntiles = a.batch * ((1ull << M) / TQ);
     uint64_t grid = (uint64_t)num_sms * occ;
     if (grid > ntiles) grid = ntiles;

@@ -1,6 +1,7 @@
 // Multi-pass tile kernels and the six-step split, Goldilocks (canonical).
 #include "tiles.cuh"
 #include "lazy.cuh"
+#include <cstdlib>
 namespace nttb200 {
 cudaError_t tile_passes_gold(int variant, const MultipassReq& r, bool* ok) {
     using A = Canon<FGold>;
@@ -22,6 +23,13 @@ cudaError_t tile_sixstep_gold(const MultipassReq& r, bool* ok) {
     using A = Canon<FGold>;
     *ok = false;
     if (!r.stw1 || !r.stw2 || !r.cor_lo) return cudaSuccess;
+    // long-run column/row passes + explicit transpose; the column-at-a-time
+    // kernels (TL_SIX_A/B) stay for the distributed steps below
+    static const int legacy = [] { const char* v = getenv("NTT_SIXSTEP_LEGACY"); return v ? atoi(v) : 0; }();
+    if (!legacy) {
+        cudaError_t e = ftile::run_sixstep_cols<A>(r, ok);
+        if (e != cudaSuccess || *ok) return e;
+    }
     *ok = true;
     if (six_match<13, 13>(r)) return ftile::run_sixstep_tiles_k<A, 13, 13>(r);
     if (six_match<7, 7>(r)) return ftile::run_sixstep_tiles_k<A, 7, 7>(r);

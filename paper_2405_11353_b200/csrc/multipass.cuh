@@ -205,6 +205,28 @@ __global__ void __launch_bounds__(256) k_bitrev(const T* in, T* out, uint64_t ba
     }
 }
 
+// Per-row matrix transpose out[c * R + r] = in[r * C + c] (R = 2^rb rows,
+// C = 2^cb columns): the six-step's explicit transpose between its column and
+// row steps (the "six" of six-step), 32 x 32 tiles through shared memory so
+// both HBM sides move 32-residue runs.  rb, cb >= 5.
+template <class T>
+__global__ void __launch_bounds__(256) k_transpose(const T* in, T* out, uint64_t batch, int rb, int cb) {
+    __shared__ T tile[32][33];
+    const uint64_t R = 1ull << rb, C = 1ull << cb;
+    const int pb = rb + cb - 10;                                // log2 tiles per matrix
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;     // 32 x 8
+    for (uint64_t blk = blockIdx.x; blk < (batch << pb); blk += gridDim.x) {
+        const uint64_t row = blk >> pb, b = blk & ((1ull << pb) - 1);
+        const uint64_t br = (b >> (cb - 5)) << 5, bc = (b & ((C >> 5) - 1)) << 5;
+        const T* src = in + (row << (rb + cb));
+        T* dst = out + (row << (rb + cb));
+        for (int k = ty; k < 32; k += 8) tile[k][tx] = src[(br + k) * C + bc + tx];
+        __syncthreads();
+        for (int k = ty; k < 32; k += 8) dst[(bc + k) * R + br + tx] = tile[tx][k];
+        __syncthreads();
+    }
+}
+
 template <class F>
 __global__ void k_pointwise(const typename F::T* a, const typename F::T* b, typename F::T* c, uint64_t n, F f) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)

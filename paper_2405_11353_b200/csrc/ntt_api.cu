@@ -471,7 +471,7 @@ int ntt_plan_info(ntt_plan_t plan, ntt_plan_info_t* info) {
 
 uint64_t ntt_plan_workspace_bytes(ntt_plan_t plan, uint64_t batch) {
     if (!plan) return 0;
-    if (plan->variant == NTT_SIXSTEP) return batch * plan->n * plan->word;
+    if (plan->variant == NTT_SIXSTEP) return 2 * batch * plan->n * plan->word;   // step ping-pong (tiles.cuh)
     if (plan->variant == NTT_NAIVE || plan->L <= smem_max_log2_word(plan->word)) return 0;
     return mp_workspace_bytes(plan->L, plan->word, plan->variant, batch);
 }

@@ -17,7 +17,7 @@ int mp_num_passes(int L, int word, int variant) {
 
 uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch) {
     const uint64_t row = (1ull << L) * (uint64_t)word;
-    if (variant == V_SIXSTEP) return batch * row;
+    if (variant == V_SIXSTEP) return 2 * batch * row;      // column / row passes ping-pong (tiles.cuh)
     if (variant == V_NAIVE || L <= single_pass_max_log2(word)) return 0;
     return 2 * batch * row;
 }

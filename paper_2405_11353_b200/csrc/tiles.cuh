@@ -300,6 +300,110 @@ cudaError_t run_sixstep_tiles_k(const MultipassReq& r) {
     return sixstep_step_b<A, K1, K2>(r, 1, r.ws, r.out);
 }
 
+// ------------------------------------------------------------------------
+// Six-step with long HBM runs (algorithms.py:371-389, x[j*n1 + i]):
+//   step A: DIT over j (length n2) of EVERY column at once -- TL_COLS tiles
+//           hold TQ consecutive columns i, so both HBM sides move TQ-residue
+//           runs (the column-at-a-time layout TL_SIX_A moves 16-byte runs);
+//           bit_reverse_permute(col) fused into the first gather, the
+//           correction w_N^(i*k2) into the last scatter;
+//   the six-step's transpose, as its own 32x32-tiled pass;
+//   step B: DIT over i (length n1) for every k2, TL_COLS again (inner k2),
+//           whose natural-order output IS out[k1*n2 + k2].
+// Each length-2^b step is one pass (b <= 9) or two (b = 12, 13: 6+6, 7+6).
+inline int cols_split(int b, int* K) {
+    if (b >= 6 && b <= 9) { K[0] = b; return 1; }
+    if (b == 12 || b == 13) { K[0] = b - 6; K[1] = 6; return 2; }
+    return 0;
+}
+
+template <class A, int K>
+cudaError_t cols_pass(const TileArgs<A>& a, const MultipassReq& r) {
+    using T = typename A::T;
+    constexpr int TQ = 1 << (tile_e<T, K>() - K);
+    constexpr int NT = (TQ << (K - 4)) < 1024 ? (TQ << (K - 4)) : 1024;
+    return launch_tile<A, V_DIT, K, TQ, NT, TL_COLS, kSmb, 0>(a, r.stream, r.num_sms, r.launches);
+}
+
+template <class A>
+cudaError_t cols_pass_any(int K, const TileArgs<A>& a, const MultipassReq& r) {
+    switch (K) {
+        case 6: return cols_pass<A, 6>(a, r);
+        case 7: return cols_pass<A, 7>(a, r);
+        case 8: return cols_pass<A, 8>(a, r);
+        case 9: return cols_pass<A, 9>(a, r);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <class A>
+cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
+    using T = typename A::T;
+    *ok = false;
+    int K1 = 0, K2 = 0;
+    while ((1ull << K1) < r.n1) ++K1;
+    while ((1ull << K2) < r.n2) ++K2;
+    int KA[2], KB[2];
+    const int PA = cols_split(K2, KA), PB = cols_split(K1, KB);
+    if (!PA || !PB || K1 < 5 || K2 < 5) return cudaSuccess;
+    *ok = true;
+    const uint64_t N = 1ull << (K1 + K2);
+    T* ws0 = static_cast<T*>(r.ws);
+    T* ws1 = ws0 + r.batch * N;
+    const bool al = aligned16(r.in) && aligned16(r.out) && aligned16(r.ws);
+    cudaError_t e = cudaSuccess;
+    // step A: columns (length n2, inner i)
+    const T* cur = static_cast<const T*>(r.in);
+    int done = 0;
+    for (int p = 0; p < PA; ++p) {
+        TileArgs<A> a = tile_base<A>(r);
+        a.L = K2; a.l1 = K1; a.S0 = done;
+        a.qmode = TQM_LINEAR; a.in_order = a.out_order = TO_T_FAST;
+        a.vec_in = a.vec_out = al;
+        a.rev_in = (p == 0);                       // bit_reverse_permute(col) (algorithms.py:374)
+        a.gstw = static_cast<const typename A::Tw*>(r.stw2);
+        a.smb = K2 < kSmb ? K2 : kSmb;
+        a.cor_on = (p == PA - 1);                  // w_N^(i*k2) (algorithms.py:377-379)
+        a.cor_lo = static_cast<const T*>(r.cor_lo);
+        a.cor_hi = static_cast<const T*>(r.cor_hi);
+        a.cor_lb = r.cor_lb;
+        a.in = cur;
+        a.out = (p == PA - 1) ? ws1 : ws0;
+        if ((e = cols_pass_any<A>(KA[p], a, r)) != cudaSuccess) return e;
+        cur = a.out;
+        done += KA[p];
+    }
+    // transpose [n2][n1] -> [n1][n2]
+    {
+        const uint64_t blocks = r.batch << (K1 + K2 - 10);
+        const uint64_t cap = (uint64_t)r.num_sms * 8;
+        k_transpose<T><<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, r.stream>>>(ws1, ws0, r.batch, K2, K1);
+        if (r.launches) ++*r.launches;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    // step B: rows (length n1, inner k2); output = out[k1*n2 + k2]
+    cur = ws0;
+    done = 0;
+    for (int p = 0; p < PB; ++p) {
+        const bool last = (p == PB - 1);
+        TileArgs<A> a = tile_base<A>(r);
+        a.L = K1; a.l1 = K2; a.S0 = done;
+        a.qmode = TQM_LINEAR; a.in_order = a.out_order = TO_T_FAST;
+        a.vec_in = a.vec_out = al;
+        a.rev_in = (p == 0);                       // bit_reverse_permute(row) (algorithms.py:385)
+        a.gstw = static_cast<const typename A::Tw*>(r.stw1);
+        a.smb = K1 < kSmb ? K1 : kSmb;
+        a.count_row = last;
+        a.scale = last ? r.scale : 0;
+        a.in = cur;
+        a.out = last ? static_cast<T*>(r.out) : ws1;
+        if ((e = cols_pass_any<A>(KB[p], a, r)) != cudaSuccess) return e;
+        cur = a.out;
+        done += KB[p];
+    }
+    return cudaSuccess;
+}
+
 }  // namespace ftile
 
 // entry points compiled in kt_f32.cu / kt_gold.cu
