@@ -1,0 +1,328 @@
+// fourstep.cuh -- two-pass four-step transform for large u32 N (2^14..2^20).
+//
+// N = R x C (R = 2^Kr, C = 2^Kc), input x[n1*C + n2] viewed as an R x C
+// row-major matrix, output X[k1 + R*k2]:
+//   pass A (MODE 0): for every column n2, the length-R sub-transform over n1
+//                    -> B[k1][n2], times the twist w_N^(k1*n2) (precomputed
+//                    [k1][n2] Shoup table), written row-major to the workspace;
+//   pass B (MODE 1): for every row k1, the length-C sub-transform over n2,
+//                    written to out[k1 + R*k2].
+// X[k1 + R k2] = sum_n2 w_C^(n2 k2) w_N^(n2 k1) sum_n1 w_R^(n1 k1) x[n1 C + n2],
+// so the output is the transform of the reference (algorithms.py:402-412) for
+// every variant; each sub-transform runs the variant's own dataflow (DIT:
+// algorithms.py:82-121; Pease_nc: constant geometry with the buffers swapping
+// roles, algorithms.py:203-261) with the sub-transform stage twiddles, which
+// are the first 2^K entries of the plan's per-stage table.
+//
+// One CTA owns a tile of TQ networks (pass A: TQ consecutive columns, pass B:
+// TQ consecutive rows) in a padded shared-memory work buffer:
+//   * copy-in with 4-byte cp.async straight into the bit-reversed work layout
+//     (no staging copy); the next tile's copy-in overlaps the current tile's
+//     register groups (two work buffers);
+//   * ceil(K/4) register groups of 16 residues per thread; the first groups
+//     use the network-major thread map (a warp inside one network), the LAST
+//     group the tile-major map (a warp spans the TQ networks), so every global
+//     store of the tile is a full 32-byte sector run of TQ residues;
+//   * pass A multiplies by the twist, pass B by n^-1 (intt) in that last group.
+// Shared-memory maps (all bank-conflict free):
+//   network stride NP = 2^AB (mod 32), AB = 5 - log2 TQ = lane bits above q;
+//   tile-major lane bits land on position bits with padpos residues 0..AB-1.
+#pragma once
+#include <cstdint>
+#include "fasttile.cuh"
+
+namespace nttb200 {
+namespace fstep {
+
+using fastk::padpos;
+using fastk::Perm;
+using fastk::plan_lanes;
+using fastk::scatter_bits;
+using ftile::cp_async_commit;
+using ftile::cp_async_wait_all;
+
+template <class A>
+struct FsArgs {
+    using T = typename A::T;
+    using Tw = typename A::Tw;
+    const T* in;
+    T* out;
+    uint64_t batch;
+    int Kr, Kc;                // R = 2^Kr (pass A length), C = 2^Kc (pass B length)
+    const Tw* stw;             // per-stage table: entries [0, 2^K) = the length-2^K sub-transform's
+    const Tw* twist;           // [k1][n2] = w_N^(k1*n2) with its Shoup word (pass A)
+    uint64_t p;
+    int scale;                 // pass B: n^-1 (intt)
+    Tw ninv;
+    int count_bitrev;
+    unsigned long long* counters;
+};
+
+NTT_D void cp4(uint32_t smem_addr, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr), "l"(g) : "memory");
+}
+
+constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
+
+template <int K, int TQ>
+struct FsGeo {
+    static constexpr int TT = 1 << (K - 4);              // threads per network
+    static constexpr int NT = TQ * TT;
+    static constexpr int G = (K + 3) / 4;
+    static constexpr int K0 = K - 4 * (G - 1);
+    static constexpr int LQ = ilog2c(TQ);
+    static constexpr int AB = LQ >= 5 ? 0 : 5 - LQ;      // lane bits above the network id (tile-major)
+};
+
+template <class T, int K, int TQ>
+constexpr size_t fs_smem_bytes() {
+    using TwT = uint2;
+    return ((size_t)sizeof(TwT) << K) + 2 * (size_t)TQ * ftile::tile_stride<T, K, TQ>() * sizeof(T);
+}
+
+// tile-major last group: sub-network id u from the thread's u' so that the AB
+// in-warp bits of u' hit position bits with padpos residues 0..AB-1
+//   DIT (positions u | c << (K-4)): identity;
+//   Pease (reads u << 4 | c): in-warp bits -> u bits 1..AB (positions 5..)
+template <int V, int K, int AB>
+NTT_D uint32_t last_u(uint32_t up) {
+    if (V == V_DIT || AB == 0) return up;
+    constexpr uint32_t m = (1u << AB) - 1;
+    return ((up & m) << 1) | ((up >> AB) & 1u) | ((up >> (AB + 1)) << (AB + 1));
+}
+
+template <class A, int V, int K, int TQ, int MODE>
+__global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3 : 2)) k_fs(FsArgs<A> a) {
+    using T = typename A::T;
+    using Tw = typename A::Tw;
+    using GG = FsGeo<K, TQ>;
+    constexpr int TT = GG::TT, NT = GG::NT, G = GG::G, K0 = GG::K0, LQ = GG::LQ, AB = GG::AB;
+    constexpr int CW = fastk::lane_bits<T>();
+    constexpr int NP = ftile::tile_stride<T, K, TQ>();
+    constexpr int EPT = 16;                             // residues per thread per tile
+    static_assert(NT * EPT == (TQ << K), "one 16-residue sub-network per thread");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Tw* tws = reinterpret_cast<Tw*>(smem_raw);
+    T* buf0 = reinterpret_cast<T*>(smem_raw + ((size_t)sizeof(Tw) << K));
+    A ar;
+    ar.init(a.p);
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t i = tid; i < (1u << K); i += NT) tws[i] = a.stw[i];
+
+    const int Kr = a.Kr, Kc = a.Kc;
+    const uint64_t N = 1ull << (Kr + Kc);
+    const uint32_t tpp_log = (MODE == 0 ? Kc : Kr) - LQ;   // log2 tiles per polynomial
+    const uint64_t ntiles = a.batch << tpp_log;
+
+    // ---- copy-in geometry (per thread, constant over tiles)
+    // MODE 0 (tile-major): q = tid mod TQ, rest = tid / TQ (K-4 bits);
+    //   row r = rest_lo << (K-AB) | rest_hi << 4 | j, placed at brev_K(r)
+    // MODE 1 (contiguous): element e = tid + j*NT of the TQ x C tile block
+    uint32_t cin_soff;          // shared offset (elements) of register j = 0
+    uint64_t cin_goff;          // global offset within the tile's base
+    if (MODE == 0) {
+        const uint32_t q = tid & (TQ - 1), rest = tid >> LQ;
+        const uint32_t rlo = rest & ((1u << AB) - 1), rhi = rest >> AB;
+        const uint32_t r0 = (rlo << (K - AB)) | (rhi << 4);
+        cin_soff = q * NP + padpos<T>(brev(r0, K));
+        cin_goff = ((uint64_t)r0 << Kc) + q;
+    } else {
+        const uint32_t x0 = tid & ((1u << K) - 1), q0 = tid >> K;
+        cin_soff = q0 * NP + padpos<T>(brev(x0, K));
+        cin_goff = tid;
+    }
+    auto tile_gbase = [&](uint64_t tl) -> uint64_t {      // global element of the tile's (q=0, r/x=0)
+        const uint64_t b = tl >> tpp_log;
+        const uint64_t g = tl & ((1ull << tpp_log) - 1);
+        return b * N + (MODE == 0 ? g * TQ : (g * TQ) << Kc);
+    };
+    auto copy_in = [&](uint64_t tl, T* dst) {
+        const T* src = a.in + tile_gbase(tl) + cin_goff;
+        const uint32_t sb = fastk::smem_u32(dst + cin_soff);
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+            uint32_t so;
+            uint64_t go;
+            if (MODE == 0) {
+                so = padpos<T>(brev((uint32_t)j, K));            // r bits 0..3 -> positions K-4..K-1
+                go = (uint64_t)j << Kc;
+            } else {
+                // e = tid + j*NT: x = e mod 2^K, q = e >> K (NT = TQ*2^(K-4))
+                constexpr uint32_t NTc = NT;
+                const uint32_t ej = (uint32_t)j * NTc;
+                so = (ej >> K) * NP + padpos<T>(brev(ej & ((1u << K) - 1), K));
+                go = ej;
+            }
+            cp4(sb + so * sizeof(T), src + go);
+        }
+    };
+
+    if ((uint64_t)blockIdx.x < ntiles) copy_in(blockIdx.x, buf0);
+    cp_async_commit();
+    int it = 0;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        T* X = buf0 + (it & 1) * (TQ * NP);
+        T* Y = buf0 + ((it + 1) & 1) * (TQ * NP);
+        cp_async_wait_all();
+        __syncthreads();                     // X landed for every thread; Y free (previous tile done)
+        {
+            const uint64_t nxt = tile + gridDim.x;
+            if (nxt < ntiles) copy_in(nxt, Y);
+            cp_async_commit();
+        }
+        // ---- register groups 0 .. G-2: network-major thread map
+#pragma unroll
+        for (int g = 0; g < G - 1; ++g) {
+            T v[16];
+            const uint32_t t = tid >> (K - 4), u = tid & (TT - 1);
+            T* sb = X + t * NP;
+            if (V == V_DIT) {
+                const int B = g == 0 ? 0 : K0 + 4 * (g - 1);
+                const int kg = g == 0 ? K0 : 4;
+                uint32_t pbase = 0;
+#define NTT_FSMAP(BB)                                  \
+    if (B == BB) {                                     \
+        constexpr Perm PM = plan_lanes(K, BB, CW);     \
+        pbase = scatter_bits<K - 4>(u, PM);            \
+    }
+                NTT_FSMAP(0) NTT_FSMAP(1) NTT_FSMAP(2) NTT_FSMAP(3) NTT_FSMAP(4) NTT_FSMAP(5)
+#undef NTT_FSMAP
+                T* wb = sb + padpos<T>(pbase);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) v[c] = wb[padpos<T>((uint32_t)c << B)];
+#define NTT_FSBW(BB, kgv) \
+    if (B == BB && kg == kgv) ftile::t_bitwin<A, K, BB, BB, kgv, false, false>(ar, v, pbase, 0u, 0, tws);
+                if (g == 0) { NTT_FSBW(0, 1) NTT_FSBW(0, 2) NTT_FSBW(0, 3) NTT_FSBW(0, 4) }
+                else { NTT_FSBW(1, 4) NTT_FSBW(2, 4) NTT_FSBW(3, 4) NTT_FSBW(4, 4) NTT_FSBW(5, 4) }
+#undef NTT_FSBW
+#pragma unroll
+                for (int c = 0; c < 16; ++c) wb[padpos<T>((uint32_t)c << B)] = v[c];
+            } else {   // Pease / Pease_nc: constant geometry, one buffer (roles swap through the registers)
+                const int sg = g == 0 ? 0 : K0 + 4 * (g - 1);
+                const int kg = g == 0 ? K0 : 4;
+                const T* rb = sb + padpos<T>(u << 4);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) v[c] = rb[padpos<T>((uint32_t)c)];
+#define NTT_FSPE(SG, KGV) \
+    if (sg == SG && kg == KGV) ftile::t_pease<A, K, SG, KGV, false>(ar, v, u, 0u, 0, tws);
+                if (g == 0) { NTT_FSPE(0, 1) NTT_FSPE(0, 2) NTT_FSPE(0, 3) NTT_FSPE(0, 4) }
+                else { NTT_FSPE(1, 4) NTT_FSPE(2, 4) NTT_FSPE(3, 4) NTT_FSPE(4, 4) NTT_FSPE(5, 4) }
+#undef NTT_FSPE
+                __syncthreads();             // every read of the (single) work buffer done
+                T* wbo = sb + padpos<T>(u << (4 - kg));
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const uint32_t n = c >> kg, Rb = c & ((1u << kg) - 1);
+                    wbo[padpos<T>(n | (Rb << (K - kg)))] = v[c];
+                }
+            }
+            __syncthreads();
+        }
+        // ---- last group: tile-major thread map, stores straight to HBM
+        {
+            T v[16];
+            const uint32_t t = tid & (TQ - 1);
+            const uint32_t u = last_u<V, K, AB>(tid >> LQ);
+            const T* sb = X + t * NP;
+            constexpr int sgL = K - 4;
+            if (V == V_DIT) {
+                const T* wb = sb + padpos<T>(u);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) v[c] = wb[padpos<T>((uint32_t)c << sgL)];
+                ftile::t_bitwin<A, K, sgL, sgL, 4, false, false>(ar, v, u, 0u, 0, tws);
+            } else {
+                const T* rb = sb + padpos<T>(u << 4);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) v[c] = rb[padpos<T>((uint32_t)c)];
+                ftile::t_pease<A, K, sgL, 4, false>(ar, v, u, 0u, 0, tws);
+            }
+            // output index of register c: u | c << (K-4) (natural order, both dataflows)
+            const uint64_t gb = tile_gbase(tile);
+            if (MODE == 0) {
+                // B[k1][n2] * w_N^(k1 n2) -> ws[k1*C + n2], n2 = tile column t
+                const uint64_t col = (tile & ((1ull << tpp_log) - 1)) * TQ + t;
+                T* dst = a.out + gb + t + ((uint64_t)u << Kc);
+                const Tw* tw = a.twist + col + ((uint64_t)u << Kc);
+                // Shoup with x < 4p < 2^32 is exact and canonicalising: no separate fin
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const uint64_t ro = (uint64_t)c << (K - 4 + Kc);
+                    dst[ro] = ar.mulc(v[c], __ldg(tw + ro));
+                }
+            } else {
+                // out[k1 + R*k2]: k1 = tile row t, k2 = u | c << (K-4)
+                const uint64_t k1 = (tile & ((1ull << tpp_log) - 1)) * TQ + t;
+                T* dst = a.out + (tile >> tpp_log) * N + k1 + ((uint64_t)u << Kr);
+                if (a.scale) {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) dst[(uint64_t)c << (K - 4 + Kr)] = ar.mulc(v[c], a.ninv);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) dst[(uint64_t)c << (K - 4 + Kr)] = ar.fin(v[c]);
+                }
+            }
+        }
+        if (a.counters && tid == 0 && (tile & ((1ull << tpp_log) - 1)) == 0) {
+            atomicAdd(a.counters + C_HBM, 1ull);
+            if (MODE == 1) atomicAdd(a.counters + C_TRANSFORMS, 1ull);
+            if (MODE == 0 && a.count_bitrev) atomicAdd(a.counters + C_BITREV, (unsigned long long)a.count_bitrev);
+        }
+    }
+}
+
+template <int K>
+constexpr int fs_tq() { return K >= 9 ? 8 : (K == 8 ? 16 : 32); }
+
+template <class A, int V, int K, int MODE>
+cudaError_t fs_launch(const FsArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {
+    using T = typename A::T;
+    constexpr int TQ = fs_tq<K>();
+    constexpr int NT = FsGeo<K, TQ>::NT;
+    constexpr size_t smem = fs_smem_bytes<T, K, TQ>();
+    auto kern = k_fs<A, V, K, TQ, MODE>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    const int lq = ilog2c(TQ);
+    const uint64_t ntiles = a.batch << ((MODE == 0 ? a.Kc : a.Kr) - lq);
+    uint64_t grid = (uint64_t)num_sms * occ;
+    if (grid > ntiles) grid = ntiles;
+    if (grid == 0) return cudaSuccess;
+    kern<<<(unsigned)grid, NT, smem, s>>>(a);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+template <class A, int V, int K>
+cudaError_t fs_pass(int mode, const FsArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {
+    return mode == 0 ? fs_launch<A, V, K, 0>(a, s, num_sms, launches) : fs_launch<A, V, K, 1>(a, s, num_sms, launches);
+}
+
+template <class A, int V>
+cudaError_t fs_pass_any(int K, int mode, const FsArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {
+    switch (K) {
+        case 7: return fs_pass<A, V, 7>(mode, a, s, num_sms, launches);
+        case 8: return fs_pass<A, V, 8>(mode, a, s, num_sms, launches);
+        case 9: return fs_pass<A, V, 9>(mode, a, s, num_sms, launches);
+        case 10: return fs_pass<A, V, 10>(mode, a, s, num_sms, launches);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// Builds the pass-A twist table tw4[k1*C + n2] = w^(k1*n2) from the plan's
+// main table (w^i with its Shoup word, i < N; k1*n2 < N needs no reduction).
+template <class Tw>
+__global__ void k_fs_twist_table(const Tw* tw, Tw* out, int Kr, int Kc) {
+    const uint64_t n = 1ull << (Kr + Kc);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k1 = i >> Kc, n2 = i & ((1ull << Kc) - 1);
+        out[i] = tw[k1 * n2];
+    }
+}
+
+}  // namespace fstep
+
+}  // namespace nttb200

@@ -138,7 +138,11 @@ cudaError_t run_variant(const MultipassReq& r) {
     {
         bool ok = false;
         cudaError_t te = cudaSuccess;
-        if constexpr (std::is_same<F, F32S>::value) te = tile_passes_f32(V, r.p < (1ull << 30), r, &ok);
+        if constexpr (std::is_same<F, F32S>::value) {
+            te = fourstep_f32(r, &ok);
+            if (te != cudaSuccess || ok) return te;
+            te = tile_passes_f32(V, r.p < (1ull << 30), r, &ok);
+        }
         else if constexpr (std::is_same<F, FGold>::value) te = tile_passes_gold(V, r, &ok);
         if (te != cudaSuccess || ok) return te;
     }

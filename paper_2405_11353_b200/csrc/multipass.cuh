@@ -289,11 +289,20 @@ struct MultipassReq {
     int num_sms;
     int* launches;
     void* ws;                  // workspace: 2 x batch x N residues
+    const void* fst;           // four-step twist table [k1][n2] = w^(k1*n2) (fourstep.cuh), or null
 };
 
 int mp_num_passes(int L, int word, int variant);
 uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch);
 cudaError_t mp_launch_f32s(const MultipassReq& r);
+// two-pass four-step for large u32 N (fourstep.cuh, kfs_f32.cu); *ok = false when it does not apply
+cudaError_t fourstep_f32(const MultipassReq& r, bool* ok);
+// four-step is used for LazyF32 fields (p < 2^30), DIT / Pease_nc, 14 <= L <= 20
+inline bool fourstep_applies(int L, int variant, uint64_t p, int word) {
+    return word == 4 && p < (1ull << 30) && L >= 14 && L <= 20 && (variant == V_DIT || variant == V_PEASE_NC);
+}
+inline int fourstep_kr(int L) { return (L + 1) / 2; }
+cudaError_t fourstep_twist_build(const void* tw, void* out, int L, cudaStream_t s);
 cudaError_t mp_launch_f32w(const MultipassReq& r);
 cudaError_t mp_launch_gold(const MultipassReq& r);
 cudaError_t mp_launch_f64(const MultipassReq& r);

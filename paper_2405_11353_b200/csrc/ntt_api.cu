@@ -237,6 +237,8 @@ struct ntt_plan_s {
     // four-step twist hi table (u32 multi-pass): w^(j * 2^twh_bits) + Shoup word
     void* twh = nullptr;
     int twh_bits = 0;
+    // four-step twist table (fourstep.cuh): [k1][n2] = w^(k1*n2) + Shoup word
+    void* fst = nullptr;
     int num_sms = 148;
     // workspace for multi-pass plans and host-buffer execution
     void* ws = nullptr;
@@ -262,6 +264,7 @@ struct ntt_plan_s {
         if (cor_lo) cudaFree(cor_lo);
         if (cor_hi) cudaFree(cor_hi);
         if (twh) cudaFree(twh);
+        if (fst) cudaFree(fst);
         cudaSetDevice(cur);
     }
 };
@@ -441,6 +444,16 @@ int ntt_plan_create(uint64_t p, uint64_t g, int w_bits, uint64_t n, int variant,
         if (e != cudaSuccess) { pl->twh = nullptr; return cuda_fail(e, "twist table upload"); }
         pl->twh_bits = th;
     }
+    if (fourstep_applies(L, variant, p, word_bytes)) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        cudaError_t e = cudaMalloc(&pl->fst, n * 8);
+        if (e == cudaSuccess) e = fourstep_twist_build(pl->table->tw, pl->fst, L, 0);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        cudaSetDevice(cur);
+        if (e != cudaSuccess) { if (pl->fst) cudaFree(pl->fst); pl->fst = nullptr; return cuda_fail(e, "four-step twist table"); }
+    }
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
         pl->num_sms = sms;
@@ -498,6 +511,7 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
     r.ws = plan->ws;
     r.twh = plan->twh;
     r.twh_bits = plan->twh_bits;
+    r.fst = plan->fst;
     if (plan->variant == NTT_SIXSTEP) {
         r.n1 = plan->n1; r.n2 = plan->n2;
         r.tw1 = plan->table1 ? plan->table1->tw : nullptr;

@@ -163,6 +163,21 @@ def test_list_api_and_bench_checksum(golden):
             assert isinstance(out, list) and out[0] == rec["checksum"] == (467606314 if n == "1024" else out[0])
 
 
+@pytest.mark.parametrize("variant", ["dit", "pease_nc"])
+@pytest.mark.parametrize("L", [14, 15, 16, 17, 18, 19, 20])
+def test_fourstep_sizes_vs_oracle(variant, L):
+    """Two-pass four-step kernels (fourstep.cuh; every R x C split 7..10):
+    forward, unscaled inverse and intt against the oracle, odd batch."""
+    p, g = 998244353, 3
+    B = 3 if L <= 18 else 1
+    x = rand(p, B, L, np.uint32, 4000 + L)
+    assert np.array_equal(gpu_ntt(x, p, g, 32, variant), O.ntt(x, p, g, 32, variant)), (variant, L)
+    assert np.array_equal(gpu_ntt(x, p, g, 32, variant, inverse=True),
+                          O.ntt(x, p, g, 32, variant, inverse=True)), (variant, L)
+    assert np.array_equal(gpu_ntt(x, p, g, 32, variant, inverse=True, scale=True),
+                          O.ntt(x, p, g, 32, variant, inverse=True, scale=True)), (variant, L)
+
+
 @pytest.mark.parametrize("cfg", [1, 2, 3])
 def test_config_golden_hash_full(cfg):
     w = CONFIGS[cfg]
