@@ -192,7 +192,7 @@ NTT_D void t_pease(const A& ar, typename A::T (&v)[16], uint32_t u, uint32_t qto
 #pragma unroll
     for (int n = 0; n < NB; ++n) {
         const uint32_t q = (u << (4 - kg)) | n;                   // local network id (K-kg bits)
-        const uint32_t bprev = sg ? (q >> (K - kg - sg)) : 0u;     // output bits of earlier groups
+        const uint32_t bprev = sg ? (q >> ((K - kg - sg) > 0 ? (K - kg - sg) : 0)) : 0u;     // output bits of earlier groups
 #pragma unroll
         for (int m = 0; m < kg; ++m) {
             const int s = S0 + sg + m + 1;

@@ -31,6 +31,28 @@
 #include <cstdint>
 #include "fasttile.cuh"
 
+// experiment knobs (defaults = measured best)
+#ifndef NTT_FS_CIN_LATE
+#define NTT_FS_CIN_LATE 0       // issue the next tile's copy-in after the first group instead of before it
+#endif
+#ifndef NTT_FS_DIAG
+#define NTT_FS_DIAG 0           // diagnostics only: 1 = skip the butterflies (data movement alone), 3 = also skip the stores, 4 = skip butterflies + copy-in
+#endif
+#ifndef NTT_FS_L2PF
+#define NTT_FS_L2PF 0           // prefetch the input this many polynomials ahead into L2 (0 = off)
+#endif
+#ifndef NTT_FS_L2PF_ALL
+#define NTT_FS_L2PF_ALL 0       // also in pass B (contiguous tiles)
+#endif
+#ifndef NTT_FS_TWIST_TAB
+#define NTT_FS_TWIST_TAB 1      // pass A twist from the precomputed [k1][n2] table (1) or factored (0):
+                                // w^(n2 k1) = w^(n2 u) * w^(n2 c 2^(K-4)), one main-table load per
+                                // thread + a 16 x TQ shared table per tile instead of 8 L2 bytes per residue
+#endif
+#ifndef NTT_FS_TW_EARLY
+#define NTT_FS_TW_EARLY 1       // pass A: load the 16 twist factors before the last group's butterflies
+#endif
+
 namespace nttb200 {
 namespace fstep {
 
@@ -50,7 +72,8 @@ struct FsArgs {
     uint64_t batch;
     int Kr, Kc;                // R = 2^Kr (pass A length), C = 2^Kc (pass B length)
     const Tw* stw;             // per-stage table: entries [0, 2^K) = the length-2^K sub-transform's
-    const Tw* twist;           // [k1][n2] = w_N^(k1*n2) with its Shoup word (pass A)
+    const Tw* twist;           // [k1][n2] = w_N^(k1*n2) with its Shoup word (pass A, NTT_FS_TWIST_TAB)
+    const Tw* tw_main;         // the plan's main table w_N^i, i < N (factored twist)
     uint64_t p;
     int scale;                 // pass B: n^-1 (intt)
     Tw ninv;
@@ -77,7 +100,7 @@ struct FsGeo {
 template <class T, int K, int TQ>
 constexpr size_t fs_smem_bytes() {
     using TwT = uint2;
-    return ((size_t)sizeof(TwT) << K) + 2 * (size_t)TQ * ftile::tile_stride<T, K, TQ>() * sizeof(T);
+    return ((size_t)sizeof(TwT) << K) + (size_t)sizeof(TwT) * 16 * TQ + 2 * (size_t)TQ * ftile::tile_stride<T, K, TQ>() * sizeof(T);
 }
 
 // tile-major last group: sub-network id u from the thread's u' so that the AB
@@ -92,7 +115,7 @@ NTT_D uint32_t last_u(uint32_t up) {
 }
 
 template <class A, int V, int K, int TQ, int MODE>
-__global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3 : 2)) k_fs(FsArgs<A> a) {
+__global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3 : (FsGeo<K, TQ>::NT <= 512 ? 2 : 1))) k_fs(FsArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
     using GG = FsGeo<K, TQ>;
@@ -103,7 +126,8 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
     static_assert(NT * EPT == (TQ << K), "one 16-residue sub-network per thread");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Tw* tws = reinterpret_cast<Tw*>(smem_raw);
-    T* buf0 = reinterpret_cast<T*>(smem_raw + ((size_t)sizeof(Tw) << K));
+    Tw* twB = tws + (1 << K);                           // factored twist: [c][t] = w^(n2_t c 2^(K-4))
+    T* buf0 = reinterpret_cast<T*>(twB + 16 * TQ);
     A ar;
     ar.init(a.p);
     const uint32_t tid = threadIdx.x;
@@ -137,6 +161,7 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
         return b * N + (MODE == 0 ? g * TQ : (g * TQ) << Kc);
     };
     auto copy_in = [&](uint64_t tl, T* dst) {
+        if (NTT_FS_DIAG == 4) return;
         const T* src = a.in + tile_gbase(tl) + cin_goff;
         const uint32_t sb = fastk::smem_u32(dst + cin_soff);
 #pragma unroll
@@ -157,6 +182,18 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
         }
     };
 
+    // L2 prefetch of the input NTT_FS_L2PF polynomials ahead: tile g of
+    // polynomial b pulls the contiguous 1/(tiles per polynomial) slice g of
+    // polynomial b + NTT_FS_L2PF, so the strided gathers of pass A find their
+    // 32-byte runs in L2 (DRAM sees whole contiguous slices)
+    auto l2_prefetch = [&](uint64_t tl) {
+        if (NTT_FS_L2PF == 0 || tid != 0) return;
+        const uint64_t b = (tl >> tpp_log) + NTT_FS_L2PF;
+        if (b >= a.batch) return;
+        const uint64_t slice = N >> tpp_log;                     // elements per slice
+        const T* src = a.in + b * N + (tl & ((1ull << tpp_log) - 1)) * slice;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((uint32_t)(slice * sizeof(T))) : "memory");
+    };
     if ((uint64_t)blockIdx.x < ntiles) copy_in(blockIdx.x, buf0);
     cp_async_commit();
     int it = 0;
@@ -165,14 +202,28 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
         T* Y = buf0 + ((it + 1) & 1) * (TQ * NP);
         cp_async_wait_all();
         __syncthreads();                     // X landed for every thread; Y free (previous tile done)
-        {
+        auto prefetch_next = [&]() {
             const uint64_t nxt = tile + gridDim.x;
             if (nxt < ntiles) copy_in(nxt, Y);
             cp_async_commit();
+            if (NTT_FS_L2PF_ALL || MODE == 0) l2_prefetch(tile);
+        };
+        if (!NTT_FS_CIN_LATE) prefetch_next();
+        // factored pass-A twist: the tile's [c][t] table and this thread's w^(n2 u)
+        Tw twA;
+        if (MODE == 0 && !NTT_FS_TWIST_TAB) {
+            const uint64_t col0 = (tile & ((1ull << tpp_log) - 1)) * TQ;
+            if (tid < 16 * TQ) {
+                const uint32_t c = tid / TQ, t = tid % TQ;
+                twB[tid] = __ldg(a.tw_main + (((col0 + t) * c) << (K - 4)));
+            }
+            twA = __ldg(a.tw_main + (col0 + (tid & (TQ - 1))) * last_u<V, K, AB>(tid >> LQ));
         }
         // ---- register groups 0 .. G-2: network-major thread map
 #pragma unroll
         for (int g = 0; g < G - 1; ++g) {
+            if (NTT_FS_DIAG >= 1) break;
+            if (NTT_FS_CIN_LATE && g == 1) prefetch_next();   // after the first group's loads
             T v[16];
             const uint32_t t = tid >> (K - 4), u = tid & (TT - 1);
             T* sb = X + t * NP;
@@ -218,6 +269,7 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
             }
             __syncthreads();
         }
+        if (NTT_FS_CIN_LATE && G == 2) prefetch_next();
         // ---- last group: tile-major thread map, stores straight to HBM
         {
             T v[16];
@@ -225,29 +277,49 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
             const uint32_t u = last_u<V, K, AB>(tid >> LQ);
             const T* sb = X + t * NP;
             constexpr int sgL = K - 4;
+            // pass A: the twist factors of this thread's 16 outputs, loaded before the
+            // butterflies so their L2 latency overlaps the last group's arithmetic
+            Tw twv[(MODE == 0 && NTT_FS_TW_EARLY && NTT_FS_TWIST_TAB) ? 16 : 1];
+            if (MODE == 0 && NTT_FS_TW_EARLY && NTT_FS_TWIST_TAB) {
+                const uint64_t col = (tile & ((1ull << tpp_log) - 1)) * TQ + t;
+                const Tw* tw = a.twist + col + ((uint64_t)u << Kc);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) twv[(MODE == 0 && NTT_FS_TW_EARLY && NTT_FS_TWIST_TAB) ? c : 0] = __ldg(tw + ((uint64_t)c << (K - 4 + Kc)));
+            }
             if (V == V_DIT) {
                 const T* wb = sb + padpos<T>(u);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) v[c] = wb[padpos<T>((uint32_t)c << sgL)];
-                ftile::t_bitwin<A, K, sgL, sgL, 4, false, false>(ar, v, u, 0u, 0, tws);
+                if (NTT_FS_DIAG == 0) ftile::t_bitwin<A, K, sgL, sgL, 4, false, false>(ar, v, u, 0u, 0, tws);
             } else {
                 const T* rb = sb + padpos<T>(u << 4);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) v[c] = rb[padpos<T>((uint32_t)c)];
-                ftile::t_pease<A, K, sgL, 4, false>(ar, v, u, 0u, 0, tws);
+                if (NTT_FS_DIAG == 0) ftile::t_pease<A, K, sgL, 4, false>(ar, v, u, 0u, 0, tws);
             }
             // output index of register c: u | c << (K-4) (natural order, both dataflows)
             const uint64_t gb = tile_gbase(tile);
-            if (MODE == 0) {
+            if (NTT_FS_DIAG == 3) {
+                if (a.count_bitrev == 77) a.out[tid] = v[0] ^ v[5] ^ v[15];   // never: keeps the loads
+            } else if (MODE == 0) {
                 // B[k1][n2] * w_N^(k1 n2) -> ws[k1*C + n2], n2 = tile column t
                 const uint64_t col = (tile & ((1ull << tpp_log) - 1)) * TQ + t;
                 T* dst = a.out + gb + t + ((uint64_t)u << Kc);
                 const Tw* tw = a.twist + col + ((uint64_t)u << Kc);
                 // Shoup with x < 4p < 2^32 is exact and canonicalising: no separate fin
+                if (NTT_FS_TWIST_TAB) {
 #pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    const uint64_t ro = (uint64_t)c << (K - 4 + Kc);
-                    dst[ro] = ar.mulc(v[c], __ldg(tw + ro));
+                    for (int c = 0; c < 16; ++c) {
+                        const uint64_t ro = (uint64_t)c << (K - 4 + Kc);
+                        dst[ro] = ar.mulc(v[c], NTT_FS_TW_EARLY ? twv[NTT_FS_TW_EARLY ? c : 0] : __ldg(tw + ro));
+                    }
+                } else {
+                    // [0,2p) results: pass B's first stage takes lazy inputs
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const uint64_t ro = (uint64_t)c << (K - 4 + Kc);
+                        dst[ro] = ar.mull(ar.mull(v[c], ftile::lds_tw(&twB[c * TQ + t])), twA);
+                    }
                 }
             } else {
                 // out[k1 + R*k2]: k1 = tile row t, k2 = u | c << (K-4)
@@ -270,8 +342,11 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
     }
 }
 
+#ifndef NTT_FS_TQ10
+#define NTT_FS_TQ10 8
+#endif
 template <int K>
-constexpr int fs_tq() { return K >= 9 ? 8 : (K == 8 ? 16 : 32); }
+constexpr int fs_tq() { return K == 10 ? NTT_FS_TQ10 : (K == 9 ? 8 : (K == 8 ? 16 : 32)); }
 
 template <class A, int V, int K, int MODE>
 cudaError_t fs_launch(const FsArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {

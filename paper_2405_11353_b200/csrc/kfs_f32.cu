@@ -20,6 +20,7 @@ static cudaError_t fs_run(const MultipassReq& r, int Kr, int Kc) {
     a.Kc = Kc;
     a.stw = static_cast<const uint2*>(r.stw);
     a.twist = static_cast<const uint2*>(r.fst);
+    a.tw_main = static_cast<const uint2*>(r.tw);
     a.p = r.p;
     a.ninv = make_uint2((uint32_t)r.ninv, (uint32_t)r.ninv_shoup);
     a.counters = r.counters;

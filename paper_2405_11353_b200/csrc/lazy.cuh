@@ -83,6 +83,10 @@ struct LazyF32 {
         return umin32(z, z - p);
     }
     NTT_D T mulfull(T a, T b) const { return (T)(((uint64_t)a * b) % p); }
+    NTT_D T mull(T x, Tw w) const {           // lazy x*w in [0,2p) for any x < 2^32
+        const T q = __umulhi(x, w.y);
+        return x * w.x - q * p;
+    }
 };
 
 template <class F>

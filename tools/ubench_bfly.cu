@@ -138,11 +138,17 @@ void run(const char* name, uint64_t p, typename A::Tw w0, typename A::Tw w1, int
     cudaFree(out);
 }
 
+// the four-mul.wide product (previous default) for comparison
+struct FGoldOld : FGoldC {
+    NTT_D T mul(T x, Tw w) const { return mul_c(x, w); }
+};
+
 __global__ void k_goldcheck(const uint64_t* a, const uint64_t* b, int n, int* bad) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     uint64_t x = a[i], y = b[i];
     if (FGoldC::mul_c(x, y) != FGold::reduce128(x * y, __umul64hi(x, y))) atomicAdd(bad, 1);
+    if (FGoldC::mul_m(x, y) != FGold::reduce128(x * y, __umul64hi(x, y))) atomicAdd(bad, 1);
     { uint64_t s_ = x + y; if (s_ < x) s_ += FGold::EPS; if (FGoldC::add_c(x, y) != FGold::canon(s_)) atomicAdd(bad + 1, 1); }
     if (FGoldC::sub_c(x, y) != (x < y ? x - y - FGold::EPS : x - y)) atomicAdd(bad + 2, 1);
 }
@@ -184,6 +190,8 @@ int main() {
     run<Canon<FGold>>("goldilocks", G, 7ull, 49ull, 512);
     run<Canon<FGoldC>>("gold-carry", G, 7ull, 49ull, 256);
     run<Canon<FGoldC>>("gold-carry", G, 7ull, 49ull, 512);
+    run<Canon<FGoldOld>>("gold-mulc", G, 7ull, 49ull, 256);
+    run<Canon<FGoldOld>>("gold-mulc", G, 7ull, 49ull, 512);
     // exactness check of FGoldC vs FGold on random operands
     check_gold();
     return 0;
