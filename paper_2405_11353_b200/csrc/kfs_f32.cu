@@ -1,6 +1,9 @@
 // Four-step two-pass kernels for large u32 N (fourstep.cuh), LazyF32 fields.
 #include <cstdlib>
+#include <cstring>
+#include <cudaTypedefs.h>
 #include "fourstep.cuh"
+#include "fourstep_tma.cuh"
 #include "multipass.cuh"
 #include "lazy.cuh"
 namespace nttb200 {
@@ -9,6 +12,81 @@ namespace nttb200 {
 static bool fourstep_enabled() {
     static const bool on = [] { const char* e = getenv("NTT_FOURSTEP"); return !(e && e[0] == '0'); }();
     return on;
+}
+
+#ifndef NTT_FSA_L2PROMO
+#define NTT_FSA_L2PROMO 0     // TMA L2 promotion of the 32-byte box rows: 0 none, 1 64B, 2 128B, 3 256B
+#endif
+// NTT_FS_TMA=0 keeps pass A on cp.async copy-in (A/B experiments)
+static bool fs_tma_enabled() {
+    static const bool on = [] { const char* e = getenv("NTT_FS_TMA"); return !(e && e[0] == '0'); }();
+    return on;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// a pass of length 2^10 with TMA / bulk-copy tile loads (fourstep_tma.cuh): true when it ran
+template <int V, int MODE>
+static bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err) {
+    using A = LazyF32;
+    *err = cudaSuccess;
+    const void* src = MODE == 0 ? r.in : r.ws;
+    if (!fs_tma_enabled() || (reinterpret_cast<uintptr_t>(src) & 15)) return false;
+    CUtensorMap map;
+    memset(&map, 0, sizeof(map));
+    if (MODE == 0) {
+        auto enc = tensor_map_encoder();
+        if (!enc) return false;
+        cuuint64_t dims[2] = {(cuuint64_t)1 << Kc, (cuuint64_t)r.batch << Kr};
+        cuuint64_t strides[1] = {((cuuint64_t)1 << Kc) * 4};
+        cuuint32_t box[2] = {8, 256};
+        cuuint32_t es[2] = {1, 1};
+        if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(src), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                NTT_FSA_L2PROMO == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : NTT_FSA_L2PROMO == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                : NTT_FSA_L2PROMO == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    fstep::FsTmaArgs<A> a{};
+    a.in = static_cast<const uint32_t*>(src);
+    a.out = static_cast<uint32_t*>(MODE == 0 ? r.ws : r.out);
+    a.batch = r.batch;
+    a.Kr = Kr;
+    a.Kc = Kc;
+    a.stw = static_cast<const uint2*>(r.stw);
+    a.twist = static_cast<const uint2*>(r.fst);
+    a.tw_main = static_cast<const uint2*>(r.tw);
+    a.p = r.p;
+    a.scale = MODE == 1 ? r.scale : 0;
+    a.ninv = make_uint2((uint32_t)r.ninv, (uint32_t)r.ninv_shoup);
+    a.count_bitrev = MODE == 0 ? 1 : 0;
+    a.counters = r.counters;
+    constexpr size_t smem = fstep::fsa_smem_bytes(fstep::TmaGeo<V>::NP);
+    auto kern = fstep::k_fs_tma<A, V, MODE>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 512, smem);
+    if (e != cudaSuccess) { *err = e; return true; }
+    if (occ < 1) occ = 1;
+    const uint64_t ntiles = r.batch << ((MODE == 0 ? Kc : Kr) - 3);
+    uint64_t grid = (uint64_t)r.num_sms * occ;
+    if (grid > ntiles) grid = ntiles;
+    kern<<<(unsigned)grid, 512, smem, r.stream>>>(map, a);
+    if (r.launches) ++*r.launches;
+    *err = cudaGetLastError();
+    return true;
 }
 
 template <int V>
@@ -29,13 +107,15 @@ static cudaError_t fs_run(const MultipassReq& r, int Kr, int Kc) {
     a.out = static_cast<uint32_t*>(r.ws);
     a.scale = 0;
     a.count_bitrev = 1;          // DIT / Pease_nc sub-transforms bit-reverse their inputs
-    cudaError_t e = fstep::fs_pass_any<A, V>(Kr, 0, a, r.stream, r.num_sms, r.launches);
+    cudaError_t e = cudaSuccess;
+    if (!(Kr == 10 && fs_pass_tma<V, 0>(r, Kr, Kc, &e))) e = fstep::fs_pass_any<A, V>(Kr, 0, a, r.stream, r.num_sms, r.launches);
     if (e != cudaSuccess) return e;
     // pass B: row sub-transforms -> out[k1 + R*k2]
     a.in = static_cast<const uint32_t*>(r.ws);
     a.out = static_cast<uint32_t*>(r.out);
     a.scale = r.scale;
     a.count_bitrev = 0;
+    if (Kc == 10 && fs_pass_tma<V, 1>(r, Kr, Kc, &e)) return e;
     return fstep::fs_pass_any<A, V>(Kc, 1, a, r.stream, r.num_sms, r.launches);
 }
 
