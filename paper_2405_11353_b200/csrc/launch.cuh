@@ -113,6 +113,11 @@ cudaError_t run_variant(const MultipassReq& r) {
     const int L = r.L;
     const uint64_t N = 1ull << L;
     constexpr int elog = tile_elems_log2<T>();
+    if constexpr (std::is_same<F, F32S>::value) {       // four-step (incl. 2^14, otherwise single-pass)
+        bool ok = false;
+        cudaError_t fe = fourstep_f32(r, &ok);
+        if (fe != cudaSuccess || ok) return fe;
+    }
     if (L <= single_pass_max_log2(sizeof(T))) {
         bool ok = false;
         cudaError_t fe = try_fast<F, V>(r, &ok);
@@ -138,11 +143,7 @@ cudaError_t run_variant(const MultipassReq& r) {
     {
         bool ok = false;
         cudaError_t te = cudaSuccess;
-        if constexpr (std::is_same<F, F32S>::value) {
-            te = fourstep_f32(r, &ok);
-            if (te != cudaSuccess || ok) return te;
-            te = tile_passes_f32(V, r.p < (1ull << 30), r, &ok);
-        }
+        if constexpr (std::is_same<F, F32S>::value) te = tile_passes_f32(V, r.p < (1ull << 30), r, &ok);
         else if constexpr (std::is_same<F, FGold>::value) te = tile_passes_gold(V, r, &ok);
         if (te != cudaSuccess || ok) return te;
     }

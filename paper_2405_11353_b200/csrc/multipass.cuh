@@ -292,8 +292,9 @@ struct MultipassReq {
     const void* fst;           // four-step twist table [k1][n2] = w^(k1*n2) (fourstep.cuh), or null
 };
 
-int mp_num_passes(int L, int word, int variant);
-uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch);
+// pass count / workspace of a plan (single pass: shared-memory resident, no workspace)
+int mp_num_passes(int L, int word, int variant, uint64_t p);
+uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch, uint64_t p);
 cudaError_t mp_launch_f32s(const MultipassReq& r);
 // two-pass four-step for large u32 N (fourstep.cuh, kfs_f32.cu); *ok = false when it does not apply
 cudaError_t fourstep_f32(const MultipassReq& r, bool* ok);

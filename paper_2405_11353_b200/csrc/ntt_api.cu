@@ -473,8 +473,7 @@ int ntt_plan_info(ntt_plan_t plan, ntt_plan_info_t* info) {
     info->w_bits = plan->w; info->variant = plan->variant; info->direction = plan->dir;
     info->word_bytes = plan->word; info->device = plan->device; info->field_kind = plan->kind;
     if (plan->variant == NTT_SIXSTEP) info->passes = 2;
-    else if (plan->variant == NTT_NAIVE || plan->L <= smem_max_log2_word(plan->word)) info->passes = 1;
-    else info->passes = mp_num_passes(plan->L, plan->word, plan->variant);
+    else info->passes = mp_num_passes(plan->L, plan->word, plan->variant, plan->p);
     info->n_inv = plan->table->n_inv;
     info->n_inv_shoup = plan->dir == NTT_INVERSE ? shoup_word(plan->table->n_inv, plan->p, plan->w) : 0;
     info->device_table_bytes = plan->table->bytes + (plan->table1 ? plan->table1->bytes : 0) +
@@ -485,8 +484,7 @@ int ntt_plan_info(ntt_plan_t plan, ntt_plan_info_t* info) {
 uint64_t ntt_plan_workspace_bytes(ntt_plan_t plan, uint64_t batch) {
     if (!plan) return 0;
     if (plan->variant == NTT_SIXSTEP) return 2 * batch * plan->n * plan->word;   // step ping-pong (tiles.cuh)
-    if (plan->variant == NTT_NAIVE || plan->L <= smem_max_log2_word(plan->word)) return 0;
-    return mp_workspace_bytes(plan->L, plan->word, plan->variant, batch);
+    return mp_workspace_bytes(plan->L, plan->word, plan->variant, batch, plan->p);
 }
 
 static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t batch, unsigned flags,
