@@ -100,6 +100,13 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
 
 
+def plan_passes_of(dp) -> int | None:
+    try:
+        return int(dp.info.passes)
+    except Exception:
+        return None
+
+
 def cpu_oracle_rate(w, variant: str, seconds: float, rows_cap: int | None = None):
     """Rows/s of the CPU restatement on all host threads (bounded sample)."""
     from oracle import oracle as O
@@ -155,6 +162,7 @@ def main() -> None:
     ap.add_argument("--variant", default="pease_nc")
     ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the N = 2^9..2^20 u32 sweep")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -308,6 +316,46 @@ def main() -> None:
             except Exception as exc:  # report, do not hide
                 extra[f"config{cfg}_{var}"] = {"error": repr(exc)[:300]}
 
+    sweep = {}
+    if not args.no_extra and not args.no_sweep:
+        # batched u32 transforms N = 2^9 .. 2^20 at 256 MiB of residues per step (P = 998244353,
+        # pease_nc): the N range BASELINE.json's metric names; graph replay, CUDA events
+        p = 998244353
+        for L in range(9, 21):
+            n = 1 << L
+            B = (1 << 26) // n
+            try:
+                plan = P.make_plan(P.FieldParams(p, 3), args.variant, n)
+                dp = P.algorithms.device_plan_for(plan, 4, local_rank)
+                xa = torch.randint(0, p, (2, B, n), dtype=torch.int64, device=dev).to(torch.int32).view(torch.uint32)
+                ya = torch.empty_like(xa)
+                sp = stream.cuda_stream
+                reps = 6
+                with torch.cuda.stream(stream):
+                    for i in range(3):
+                        dp.exec_device(xa[i % 2].data_ptr(), ya[i % 2].data_ptr(), B, False, sp)
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=stream):
+                        for i in range(reps):
+                            dp.exec_device(xa[i % 2].data_ptr(), ya[i % 2].data_ptr(), B, False, sp)
+                    g.replay()
+                    barrier()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    g.replay()
+                    e1.record(stream)
+                    stream.synchronize()
+                t = max_over_ranks(e0.elapsed_time(e1)) / 1e3 / reps
+                gbs = 2 * B * n * 4 / t / 1e9
+                sweep[f"2^{L}"] = {"batch": B, "ms": round(1e3 * t, 4), "ntt_per_s": world * B / t,
+                                   "gbfly_per_s": round(world * B * (n // 2) * L / t / 1e9, 1),
+                                   "roofline_frac": round(gbs / peak, 3),
+                                   "passes": plan_passes_of(dp)}
+                del xa, ya, g
+                torch.cuda.empty_cache()
+            except Exception as exc:
+                sweep[f"2^{L}"] = {"error": repr(exc)[:200]}
+
     if world > 1 and not args.no_extra:
         # config 5 as ONE transform split four-step across the ranks (strong
         # scaling, one NCCL all-to-all per step); slab layout per distributed.py
@@ -370,6 +418,7 @@ def main() -> None:
                     "roofline_frac": alg_bytes / (dit["per_step_ms"] / 1e3) / 1e9 / peak,
                     "sha256_parity": dit["parity"]},
             "configs": extra,
+            "sweep_u32_pease_nc": sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
