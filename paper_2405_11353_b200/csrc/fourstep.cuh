@@ -81,8 +81,10 @@ struct FsArgs {
     unsigned long long* counters;
 };
 
-NTT_D void cp4(uint32_t smem_addr, const void* g) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr), "l"(g) : "memory");
+template <class T>
+NTT_D void cpe(uint32_t smem_addr, const void* g) {      // one residue (4 or 8 bytes)
+    if (sizeof(T) == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr), "l"(g) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr), "l"(g) : "memory");
 }
 
 constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
@@ -97,9 +99,8 @@ struct FsGeo {
     static constexpr int AB = LQ >= 5 ? 0 : 5 - LQ;      // lane bits above the network id (tile-major)
 };
 
-template <class T, int K, int TQ>
+template <class T, class TwT, int K, int TQ>
 constexpr size_t fs_smem_bytes() {
-    using TwT = uint2;
     return ((size_t)sizeof(TwT) << K) + (size_t)sizeof(TwT) * 16 * TQ + 2 * (size_t)TQ * ftile::tile_stride<T, K, TQ>() * sizeof(T);
 }
 
@@ -109,7 +110,7 @@ constexpr size_t fs_smem_bytes() {
 //   Pease (reads u << 4 | c): in-warp bits -> u bits 1..AB (positions 5..)
 template <int V, int K, int AB>
 NTT_D uint32_t last_u(uint32_t up) {
-    if (V == V_DIT || AB == 0) return up;
+    if (V == V_DIT || V == V_DIF || AB == 0) return up;
     constexpr uint32_t m = (1u << AB) - 1;
     return ((up & m) << 1) | ((up >> AB) & 1u) | ((up >> (AB + 1)) << (AB + 1));
 }
@@ -123,6 +124,10 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
     constexpr int CW = fastk::lane_bits<T>();
     constexpr int NP = ftile::tile_stride<T, K, TQ>();
     constexpr int EPT = 16;                             // residues per thread per tile
+    // DIT / Pease gather their input bit-reversed (algorithms.py:119,238,255); DIF
+    // reads it in natural order and bit-reverses its output (algorithms.py:158)
+    constexpr bool BRIN = (V != V_DIF);
+    constexpr bool TWE = NTT_FS_TW_EARLY && sizeof(T) == 4;
     static_assert(NT * EPT == (TQ << K), "one 16-residue sub-network per thread");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Tw* tws = reinterpret_cast<Tw*>(smem_raw);
@@ -148,11 +153,11 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
         const uint32_t q = tid & (TQ - 1), rest = tid >> LQ;
         const uint32_t rlo = rest & ((1u << AB) - 1), rhi = rest >> AB;
         const uint32_t r0 = (rlo << (K - AB)) | (rhi << 4);
-        cin_soff = q * NP + padpos<T>(brev(r0, K));
+        cin_soff = q * NP + padpos<T>(BRIN ? brev(r0, K) : r0);
         cin_goff = ((uint64_t)r0 << Kc) + q;
     } else {
         const uint32_t x0 = tid & ((1u << K) - 1), q0 = tid >> K;
-        cin_soff = q0 * NP + padpos<T>(brev(x0, K));
+        cin_soff = q0 * NP + padpos<T>(BRIN ? brev(x0, K) : x0);
         cin_goff = tid;
     }
     auto tile_gbase = [&](uint64_t tl) -> uint64_t {      // global element of the tile's (q=0, r/x=0)
@@ -169,16 +174,16 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
             uint32_t so;
             uint64_t go;
             if (MODE == 0) {
-                so = padpos<T>(brev((uint32_t)j, K));            // r bits 0..3 -> positions K-4..K-1
+                so = padpos<T>(BRIN ? brev((uint32_t)j, K) : (uint32_t)j);   // r bits 0..3 (bit-reversed: positions K-4..K-1)
                 go = (uint64_t)j << Kc;
             } else {
                 // e = tid + j*NT: x = e mod 2^K, q = e >> K (NT = TQ*2^(K-4))
                 constexpr uint32_t NTc = NT;
                 const uint32_t ej = (uint32_t)j * NTc;
-                so = (ej >> K) * NP + padpos<T>(brev(ej & ((1u << K) - 1), K));
+                so = (ej >> K) * NP + padpos<T>(BRIN ? brev(ej & ((1u << K) - 1), K) : (ej & ((1u << K) - 1)));
                 go = ej;
             }
-            cp4(sb + so * sizeof(T), src + go);
+            cpe<T>(sb + so * sizeof(T), src + go);
         }
     };
 
@@ -227,23 +232,25 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
             T v[16];
             const uint32_t t = tid >> (K - 4), u = tid & (TT - 1);
             T* sb = X + t * NP;
-            if (V == V_DIT) {
-                const int B = g == 0 ? 0 : K0 + 4 * (g - 1);
-                const int kg = g == 0 ? K0 : 4;
+            if (V == V_DIT || V == V_DIF) {
+                // DIT: windows from bit 0 up (first short); DIF: from the top bit down (short window last)
+                const int B = (V == V_DIT) ? (g == 0 ? 0 : K0 + 4 * (g - 1)) : K - 4 * (g + 1);
+                const int kg = (V == V_DIT) ? (g == 0 ? K0 : 4) : 4;
                 uint32_t pbase = 0;
 #define NTT_FSMAP(BB)                                  \
     if (B == BB) {                                     \
         constexpr Perm PM = plan_lanes(K, BB, CW);     \
         pbase = scatter_bits<K - 4>(u, PM);            \
     }
-                NTT_FSMAP(0) NTT_FSMAP(1) NTT_FSMAP(2) NTT_FSMAP(3) NTT_FSMAP(4) NTT_FSMAP(5)
+                NTT_FSMAP(0) NTT_FSMAP(1) NTT_FSMAP(2) NTT_FSMAP(3) NTT_FSMAP(4) NTT_FSMAP(5) NTT_FSMAP(6)
 #undef NTT_FSMAP
                 T* wb = sb + padpos<T>(pbase);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) v[c] = wb[padpos<T>((uint32_t)c << B)];
 #define NTT_FSBW(BB, kgv) \
-    if (B == BB && kg == kgv) ftile::t_bitwin<A, K, BB, BB, kgv, false, false>(ar, v, pbase, 0u, 0, tws);
-                if (g == 0) { NTT_FSBW(0, 1) NTT_FSBW(0, 2) NTT_FSBW(0, 3) NTT_FSBW(0, 4) }
+    if (B == BB && kg == kgv) ftile::t_bitwin<A, K, BB, BB, kgv, V == V_DIF, false>(ar, v, pbase, 0u, 0, tws);
+                if (V == V_DIF) { NTT_FSBW(1, 4) NTT_FSBW(2, 4) NTT_FSBW(3, 4) NTT_FSBW(4, 4) NTT_FSBW(5, 4) NTT_FSBW(6, 4) }
+                else if (g == 0) { NTT_FSBW(0, 1) NTT_FSBW(0, 2) NTT_FSBW(0, 3) NTT_FSBW(0, 4) }
                 else { NTT_FSBW(1, 4) NTT_FSBW(2, 4) NTT_FSBW(3, 4) NTT_FSBW(4, 4) NTT_FSBW(5, 4) }
 #undef NTT_FSBW
 #pragma unroll
@@ -279,14 +286,25 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
             constexpr int sgL = K - 4;
             // pass A: the twist factors of this thread's 16 outputs, loaded before the
             // butterflies so their L2 latency overlaps the last group's arithmetic
-            Tw twv[(MODE == 0 && NTT_FS_TW_EARLY && NTT_FS_TWIST_TAB) ? 16 : 1];
-            if (MODE == 0 && NTT_FS_TW_EARLY && NTT_FS_TWIST_TAB) {
+            // output index of register c: DIT / Pease u | c << (K-4) (natural order);
+            // DIF block [0,4) at u << 4, output brev_K(position)
+            auto xo = [&](int c) -> uint32_t {
+                if (V == V_DIF) return brev((u << 4) | (uint32_t)c, K);
+                return u | ((uint32_t)c << (K - 4));
+            };
+            Tw twv[(MODE == 0 && TWE && NTT_FS_TWIST_TAB) ? 16 : 1];
+            if (MODE == 0 && TWE && NTT_FS_TWIST_TAB) {
                 const uint64_t col = (tile & ((1ull << tpp_log) - 1)) * TQ + t;
-                const Tw* tw = a.twist + col + ((uint64_t)u << Kc);
 #pragma unroll
-                for (int c = 0; c < 16; ++c) twv[(MODE == 0 && NTT_FS_TW_EARLY && NTT_FS_TWIST_TAB) ? c : 0] = __ldg(tw + ((uint64_t)c << (K - 4 + Kc)));
+                for (int c = 0; c < 16; ++c)
+                    twv[(MODE == 0 && TWE && NTT_FS_TWIST_TAB) ? c : 0] = __ldg(a.twist + col + ((uint64_t)xo(c) << Kc));
             }
-            if (V == V_DIT) {
+            if (V == V_DIF) {
+                const T* wb = sb + padpos<T>(u << 4);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) v[c] = wb[padpos<T>((uint32_t)c)];
+                if (NTT_FS_DIAG == 0) ftile::t_bitwin<A, K, 0, 0, 4, true, false>(ar, v, u << 4, 0u, 0, tws);
+            } else if (V == V_DIT) {
                 const T* wb = sb + padpos<T>(u);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) v[c] = wb[padpos<T>((uint32_t)c << sgL)];
@@ -297,40 +315,38 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
                 for (int c = 0; c < 16; ++c) v[c] = rb[padpos<T>((uint32_t)c)];
                 if (NTT_FS_DIAG == 0) ftile::t_pease<A, K, sgL, 4, false>(ar, v, u, 0u, 0, tws);
             }
-            // output index of register c: u | c << (K-4) (natural order, both dataflows)
             const uint64_t gb = tile_gbase(tile);
             if (NTT_FS_DIAG == 3) {
                 if (a.count_bitrev == 77) a.out[tid] = v[0] ^ v[5] ^ v[15];   // never: keeps the loads
             } else if (MODE == 0) {
                 // B[k1][n2] * w_N^(k1 n2) -> ws[k1*C + n2], n2 = tile column t
                 const uint64_t col = (tile & ((1ull << tpp_log) - 1)) * TQ + t;
-                T* dst = a.out + gb + t + ((uint64_t)u << Kc);
-                const Tw* tw = a.twist + col + ((uint64_t)u << Kc);
-                // Shoup with x < 4p < 2^32 is exact and canonicalising: no separate fin
-                if (NTT_FS_TWIST_TAB) {
+                T* dst = a.out + gb + t;
+                if (NTT_FS_TWIST_TAB || V == V_DIF) {
+                    // (u32) Shoup with x < 4p < 2^32 is exact and canonicalising: no separate fin
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
-                        const uint64_t ro = (uint64_t)c << (K - 4 + Kc);
-                        dst[ro] = ar.mulc(v[c], NTT_FS_TW_EARLY ? twv[NTT_FS_TW_EARLY ? c : 0] : __ldg(tw + ro));
+                        const uint64_t ro = (uint64_t)xo(c) << Kc;
+                        dst[ro] = ar.mulc(v[c], TWE ? twv[TWE ? c : 0] : __ldg(a.twist + col + ro));
                     }
                 } else {
                     // [0,2p) results: pass B's first stage takes lazy inputs
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
                         const uint64_t ro = (uint64_t)c << (K - 4 + Kc);
-                        dst[ro] = ar.mull(ar.mull(v[c], ftile::lds_tw(&twB[c * TQ + t])), twA);
+                        dst[ro + ((uint64_t)u << Kc)] = ar.mull(ar.mull(v[c], ftile::lds_tw(&twB[c * TQ + t])), twA);
                     }
                 }
             } else {
-                // out[k1 + R*k2]: k1 = tile row t, k2 = u | c << (K-4)
+                // out[k1 + R*k2]: k1 = tile row t, k2 = xo(c)
                 const uint64_t k1 = (tile & ((1ull << tpp_log) - 1)) * TQ + t;
-                T* dst = a.out + (tile >> tpp_log) * N + k1 + ((uint64_t)u << Kr);
+                T* dst = a.out + (tile >> tpp_log) * N + k1;
                 if (a.scale) {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) dst[(uint64_t)c << (K - 4 + Kr)] = ar.mulc(v[c], a.ninv);
+                    for (int c = 0; c < 16; ++c) dst[(uint64_t)xo(c) << Kr] = ar.mulc(v[c], a.ninv);
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) dst[(uint64_t)c << (K - 4 + Kr)] = ar.fin(v[c]);
+                    for (int c = 0; c < 16; ++c) dst[(uint64_t)xo(c) << Kr] = ar.fin(v[c]);
                 }
             }
         }
@@ -345,15 +361,18 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
 #ifndef NTT_FS_TQ10
 #define NTT_FS_TQ10 8
 #endif
-template <int K>
-constexpr int fs_tq() { return K == 10 ? NTT_FS_TQ10 : (K == 9 ? 8 : (K == 8 ? 16 : 32)); }
+template <class T, int K>
+constexpr int fs_tq() {
+    if (sizeof(T) == 8) return K == 8 ? 16 : (K == 9 ? 8 : 32);
+    return K == 10 ? NTT_FS_TQ10 : (K == 9 ? 8 : (K == 8 ? 16 : 32));
+}
 
 template <class A, int V, int K, int MODE>
 cudaError_t fs_launch(const FsArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {
     using T = typename A::T;
-    constexpr int TQ = fs_tq<K>();
+    constexpr int TQ = fs_tq<T, K>();
     constexpr int NT = FsGeo<K, TQ>::NT;
-    constexpr size_t smem = fs_smem_bytes<T, K, TQ>();
+    constexpr size_t smem = fs_smem_bytes<T, typename A::Tw, K, TQ>();
     auto kern = k_fs<A, V, K, TQ, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -129,9 +129,12 @@ cudaError_t fourstep_f32(const MultipassReq& r, bool* ok) {
     return fs_run<V_PEASE_NC>(r, Kr, Kc);
 }
 
-cudaError_t fourstep_twist_build(const void* tw, void* out, int L, cudaStream_t s) {
+cudaError_t fourstep_twist_build(const void* tw, void* out, int L, int word, cudaStream_t s) {
     const int Kr = fourstep_kr(L), Kc = L - Kr;
-    fstep::k_fs_twist_table<uint2><<<1024, 256, 0, s>>>(static_cast<const uint2*>(tw), static_cast<uint2*>(out), Kr, Kc);
+    if (word == 4)   // (w, Shoup word) pairs
+        fstep::k_fs_twist_table<uint2><<<1024, 256, 0, s>>>(static_cast<const uint2*>(tw), static_cast<uint2*>(out), Kr, Kc);
+    else             // Goldilocks: values
+        fstep::k_fs_twist_table<uint64_t><<<1024, 256, 0, s>>>(static_cast<const uint64_t*>(tw), static_cast<uint64_t*>(out), Kr, Kc);
     return cudaGetLastError();
 }
 

@@ -113,9 +113,9 @@ cudaError_t run_variant(const MultipassReq& r) {
     const int L = r.L;
     const uint64_t N = 1ull << L;
     constexpr int elog = tile_elems_log2<T>();
-    if constexpr (std::is_same<F, F32S>::value) {       // four-step (incl. 2^14, otherwise single-pass)
+    if constexpr (std::is_same<F, F32S>::value || std::is_same<F, FGold>::value) {   // four-step (fourstep.cuh)
         bool ok = false;
-        cudaError_t fe = fourstep_f32(r, &ok);
+        cudaError_t fe = std::is_same<F, F32S>::value ? fourstep_f32(r, &ok) : fourstep_gold(r, &ok);
         if (fe != cudaSuccess || ok) return fe;
     }
     if (L <= single_pass_max_log2(sizeof(T))) {

@@ -124,6 +124,7 @@ struct Canon {
     }
     NTT_D T fin(T x) const { return x; }
     NTT_D T mulc(T x, Tw w) const { return f.mul(x, w); }
+    NTT_D T mull(T x, Tw w) const { return f.mul(x, w); }
     NTT_D T mulfull(T a, T b) const { return f.mul_full(a, b); }
 };
 

@@ -298,12 +298,17 @@ uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch, uint64
 cudaError_t mp_launch_f32s(const MultipassReq& r);
 // two-pass four-step for large u32 N (fourstep.cuh, kfs_f32.cu); *ok = false when it does not apply
 cudaError_t fourstep_f32(const MultipassReq& r, bool* ok);
-// four-step is used for LazyF32 fields (p < 2^30), DIT / Pease_nc, 14 <= L <= 20
+// four-step: LazyF32 fields (p < 2^30) DIT / Pease_nc 14 <= L <= 20, Goldilocks 2^16
 inline bool fourstep_applies(int L, int variant, uint64_t p, int word) {
-    return word == 4 && p < (1ull << 30) && L >= 14 && L <= 20 && (variant == V_DIT || variant == V_PEASE_NC);
+    if (word == 4)
+        return p < (1ull << 30) && L >= 14 && L <= 20 && (variant == V_DIT || variant == V_PEASE_NC);
+    // Goldilocks 2^16 = 256 x 256 (config 3): DIT, DIF, Pease_nc sub-transforms
+    return word == 8 && p == 0xFFFFFFFF00000001ull && L == 16 &&
+           (variant == V_DIT || variant == V_DIF || variant == V_PEASE_NC);
 }
 inline int fourstep_kr(int L) { return (L + 1) / 2; }
-cudaError_t fourstep_twist_build(const void* tw, void* out, int L, cudaStream_t s);
+cudaError_t fourstep_twist_build(const void* tw, void* out, int L, int word, cudaStream_t s);
+cudaError_t fourstep_gold(const MultipassReq& r, bool* ok);
 cudaError_t mp_launch_f32w(const MultipassReq& r);
 cudaError_t mp_launch_gold(const MultipassReq& r);
 cudaError_t mp_launch_f64(const MultipassReq& r);

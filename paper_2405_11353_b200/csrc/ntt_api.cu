@@ -449,7 +449,7 @@ int ntt_plan_create(uint64_t p, uint64_t g, int w_bits, uint64_t n, int variant,
         cudaGetDevice(&cur);
         cudaSetDevice(device);
         cudaError_t e = cudaMalloc(&pl->fst, n * 8);
-        if (e == cudaSuccess) e = fourstep_twist_build(pl->table->tw, pl->fst, L, 0);
+        if (e == cudaSuccess) e = fourstep_twist_build(pl->table->tw, pl->fst, L, word_bytes, 0);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         cudaSetDevice(cur);
         if (e != cudaSuccess) { if (pl->fst) cudaFree(pl->fst); pl->fst = nullptr; return cuda_fail(e, "four-step twist table"); }

@@ -178,6 +178,18 @@ def test_fourstep_sizes_vs_oracle(variant, L):
                           O.ntt(x, p, g, 32, variant, inverse=True, scale=True)), (variant, L)
 
 
+@pytest.mark.parametrize("variant", ["dit", "dif", "pease_nc"])
+def test_fourstep_goldilocks_2_16(variant):
+    """Goldilocks 256 x 256 four-step (config 3's size): forward, unscaled
+    inverse and intt against the oracle."""
+    p, g = (1 << 64) - (1 << 32) + 1, 7
+    x = rand(p, 3, 16, np.uint64, 4116)
+    assert np.array_equal(gpu_ntt(x, p, g, 64, variant), O.ntt(x, p, g, 64, variant))
+    assert np.array_equal(gpu_ntt(x, p, g, 64, variant, inverse=True), O.ntt(x, p, g, 64, variant, inverse=True))
+    assert np.array_equal(gpu_ntt(x, p, g, 64, variant, inverse=True, scale=True),
+                          O.ntt(x, p, g, 64, variant, inverse=True, scale=True))
+
+
 @pytest.mark.parametrize("cfg", [1, 2, 3])
 def test_config_golden_hash_full(cfg):
     w = CONFIGS[cfg]
