@@ -19,6 +19,8 @@
 //    thread->sub-network map is chosen so warp accesses are bank-conflict free.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include "engine.cuh"
 #include "lazy.cuh"
 
@@ -50,6 +52,32 @@ NTT_D void mbar_wait(uint64_t* bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
+// programmatic dependent launch (PDL): griddepcontrol is a no-op without the
+// launch attribute, so every kernel that calls these stays correct when
+// launched plainly
+NTT_D void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+NTT_D void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// launch with the PDL attribute (NTT_PDL=0 in the environment: plain launch)
+inline bool pdl_enabled() {
+    static const bool on = [] { const char* e = getenv("NTT_PDL"); return !(e && e[0] == '0'); }();
+    return on;
+}
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 NTT_D void team_sync(int id, int nthreads) {
     if (nthreads == 32) __syncwarp();
     else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -298,6 +326,10 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     if (t == 0) mbar_init(&mbar[team], 1);
     fence_mbar_init();
     __syncthreads();
+    // programmatic dependent launch: the prologue above (plan-owned tables only)
+    // overlaps the previous launch's tail; its outputs are visible after the wait
+    pdl_trigger();
+    pdl_wait();
 
     const uint64_t stride = (uint64_t)gridDim.x * TEAMS;
     uint64_t poly = (uint64_t)blockIdx.x * TEAMS + team;
@@ -553,9 +585,9 @@ cudaError_t launch_fast_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int
         uint64_t grid = ctas < (uint64_t)num_sms ? ctas : (uint64_t)num_sms;
         *ok = true;
         if (grid == 0) return cudaSuccess;
-        kern<<<(unsigned)grid, C::TEAMS * C::TT, C::smem, s>>>(a);
+        cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(C::TEAMS * C::TT), C::smem, s, a);
         if (launches) ++*launches;
-        return cudaGetLastError();
+        return le != cudaSuccess ? le : cudaGetLastError();
     }
 }
 

@@ -199,6 +199,9 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
         const T* src = a.in + b * N + (tl & ((1ull << tpp_log) - 1)) * slice;
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((uint32_t)(slice * sizeof(T))) : "memory");
     };
+    __syncthreads();                         // twiddle table in place (before the PDL wait)
+    fastk::pdl_trigger();
+    fastk::pdl_wait();
     if ((uint64_t)blockIdx.x < ntiles) copy_in(blockIdx.x, buf0);
     cp_async_commit();
     int it = 0;
@@ -385,9 +388,9 @@ cudaError_t fs_launch(const FsArgs<A>& a, cudaStream_t s, int num_sms, int* laun
     uint64_t grid = (uint64_t)num_sms * occ;
     if (grid > ntiles) grid = ntiles;
     if (grid == 0) return cudaSuccess;
-    kern<<<(unsigned)grid, NT, smem, s>>>(a);
+    cudaError_t le = fastk::launch_pdl(kern, dim3((unsigned)grid), dim3(NT), smem, s, a);
     if (launches) ++*launches;
-    return cudaGetLastError();
+    return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 template <class A, int V, int K>

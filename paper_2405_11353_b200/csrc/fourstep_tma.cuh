@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
         fastk::fence_mbar_init();
     }
     __syncthreads();
+    fastk::pdl_trigger();
+    fastk::pdl_wait();                       // the previous launch's output (our input) is visible
     if (tid == 0) {
         if ((uint64_t)blockIdx.x < ntiles) issue(blockIdx.x, 0);
         if ((uint64_t)blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);

@@ -83,9 +83,9 @@ static bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err)
     const uint64_t ntiles = r.batch << ((MODE == 0 ? Kc : Kr) - 3);
     uint64_t grid = (uint64_t)r.num_sms * occ;
     if (grid > ntiles) grid = ntiles;
-    kern<<<(unsigned)grid, 512, smem, r.stream>>>(map, a);
+    *err = fastk::launch_pdl(kern, dim3((unsigned)grid), dim3(512), smem, r.stream, map, a);
     if (r.launches) ++*r.launches;
-    *err = cudaGetLastError();
+    if (*err == cudaSuccess) *err = cudaGetLastError();
     return true;
 }
 
