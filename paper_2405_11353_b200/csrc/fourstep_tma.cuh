@@ -92,7 +92,9 @@ NTT_D void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) 
 
 // MODE 0: pass A (columns, tensor-map box loads, twist, rows k1 of the workspace)
 // MODE 1: pass B (rows of the workspace by 1-D bulk copies, out[k1 + R*k2])
-template <class A, int V, int MODE>
+// KO = log2 of the other dimension (C for MODE 0, R for MODE 1), compile time so
+// every strided store / twist offset is an immediate
+template <class A, int V, int MODE, int KO>
 __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUtensorMap tmap, FsTmaArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
@@ -110,9 +112,9 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
     ar.init(a.p);
     const uint32_t tid = threadIdx.x;
     for (uint32_t i = tid; i < 1024; i += NT) tws[i] = a.stw[i];
-    const int Kr = a.Kr, Kc = a.Kc;
-    const uint64_t N = 1ull << (Kr + Kc);
-    const int tpp_log = (MODE == 0 ? Kc : Kr) - 3;   // tiles per polynomial = (C or R) / 8
+    constexpr int Kr = MODE == 0 ? 10 : KO, Kc = MODE == 0 ? KO : 10;
+    constexpr uint64_t N = 1ull << (Kr + Kc);
+    constexpr int tpp_log = (MODE == 0 ? Kc : Kr) - 3;   // tiles per polynomial = (C or R) / 8
     const uint64_t ntiles = a.batch << tpp_log;
     constexpr uint32_t TILE_BYTES = 8 * 1024 * 4;
     auto issue = [&](uint64_t tl, int s) {
@@ -146,7 +148,9 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
         const int s = it & 1;
         const T* S = stg + s * STG;
         // staging element (input index x, network q)
-        auto sidx = [&](uint32_t x) -> uint32_t { return MODE == 0 ? x * 8 + q : q * kStgRow + x; };
+        // staging base of this thread's network (the position part added as an immediate)
+        const T* Sq = S + (MODE == 0 ? q : q * kStgRow);
+        auto sidx = [&](uint32_t x) -> uint32_t { return MODE == 0 ? x * 8 : x; };
         T v[16];
         // ---- group 0 (tile-major): read the dense staging, write the work buffer
         uint32_t u0;
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
             const uint32_t pbase = u0 << 4;
             const uint32_t rb = brev(pbase, K);
 #pragma unroll
-            for (int c = 0; c < 16; ++c) v[c] = S[sidx(rb | (brev((uint32_t)c, 4) << 6))];
+            for (int c = 0; c < 16; ++c) v[c] = Sq[sidx(rb) + sidx(brev((uint32_t)c, 4) << 6)];
             ftile::t_bitwin<A, K, 0, 0, GG::KG0, false, false>(ar, v, pbase, 0u, 0, tws);
             __syncthreads();                  // staging consumed; previous tile's last group done with W
             T* wb = W + q * NP + padpos<T>(pbase);
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
         } else {
             const uint32_t rb = brev(u0 << 4, K);
 #pragma unroll
-            for (int c = 0; c < 16; ++c) v[c] = S[sidx(rb | (brev((uint32_t)c, 4) << 6))];
+            for (int c = 0; c < 16; ++c) v[c] = Sq[sidx(rb) + sidx(brev((uint32_t)c, 4) << 6)];
             ftile::t_pease<A, K, 0, GG::KG0, false>(ar, v, u0, 0u, 0, tws);
             __syncthreads();
             T* wbo = W + q * NP + padpos<T>(u0 << (4 - GG::KG0));

@@ -74,7 +74,7 @@ static bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err)
     a.count_bitrev = MODE == 0 ? 1 : 0;
     a.counters = r.counters;
     constexpr size_t smem = fstep::fsa_smem_bytes(fstep::TmaGeo<V>::NP);
-    auto kern = fstep::k_fs_tma<A, V, MODE>;
+    auto kern = (MODE == 0 ? Kc : Kr) == 10 ? fstep::k_fs_tma<A, V, MODE, 10> : fstep::k_fs_tma<A, V, MODE, 9>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ = 0;
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 512, smem);
