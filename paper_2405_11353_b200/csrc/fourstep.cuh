@@ -115,7 +115,7 @@ NTT_D uint32_t last_u(uint32_t up) {
     return ((up & m) << 1) | ((up >> AB) & 1u) | ((up >> (AB + 1)) << (AB + 1));
 }
 
-template <class A, int V, int K, int TQ, int MODE>
+template <class A, int V, int K, int TQ, int MODE, int KO>
 __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3 : (FsGeo<K, TQ>::NT <= 512 ? 2 : 1))) k_fs(FsArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
@@ -138,9 +138,10 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
     const uint32_t tid = threadIdx.x;
     for (uint32_t i = tid; i < (1u << K); i += NT) tws[i] = a.stw[i];
 
-    const int Kr = a.Kr, Kc = a.Kc;
-    const uint64_t N = 1ull << (Kr + Kc);
-    const uint32_t tpp_log = (MODE == 0 ? Kc : Kr) - LQ;   // log2 tiles per polynomial
+    // KO = log2 of the other dimension, compile time: every strided offset is an immediate
+    constexpr int Kr = MODE == 0 ? K : KO, Kc = MODE == 0 ? KO : K;
+    constexpr uint64_t N = 1ull << (Kr + Kc);
+    constexpr uint32_t tpp_log = (MODE == 0 ? Kc : Kr) - LQ;   // log2 tiles per polynomial
     const uint64_t ntiles = a.batch << tpp_log;
 
     // ---- copy-in geometry (per thread, constant over tiles)
@@ -370,13 +371,13 @@ constexpr int fs_tq() {
     return K == 10 ? NTT_FS_TQ10 : (K == 9 ? 8 : (K == 8 ? 16 : 32));
 }
 
-template <class A, int V, int K, int MODE>
+template <class A, int V, int K, int MODE, int KO>
 cudaError_t fs_launch(const FsArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {
     using T = typename A::T;
     constexpr int TQ = fs_tq<T, K>();
     constexpr int NT = FsGeo<K, TQ>::NT;
     constexpr size_t smem = fs_smem_bytes<T, typename A::Tw, K, TQ>();
-    auto kern = k_fs<A, V, K, TQ, MODE>;
+    auto kern = k_fs<A, V, K, TQ, MODE, KO>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0;
@@ -384,7 +385,7 @@ cudaError_t fs_launch(const FsArgs<A>& a, cudaStream_t s, int num_sms, int* laun
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
     const int lq = ilog2c(TQ);
-    const uint64_t ntiles = a.batch << ((MODE == 0 ? a.Kc : a.Kr) - lq);
+    const uint64_t ntiles = a.batch << (KO - lq);
     uint64_t grid = (uint64_t)num_sms * occ;
     if (grid > ntiles) grid = ntiles;
     if (grid == 0) return cudaSuccess;
@@ -393,18 +394,24 @@ cudaError_t fs_launch(const FsArgs<A>& a, cudaStream_t s, int num_sms, int* laun
     return le != cudaSuccess ? le : cudaGetLastError();
 }
 
-template <class A, int V, int K>
-cudaError_t fs_pass(int mode, const FsArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {
-    return mode == 0 ? fs_launch<A, V, K, 0>(a, s, num_sms, launches) : fs_launch<A, V, K, 1>(a, s, num_sms, launches);
+// pass `mode` of a transform of size 2^L (Kr = ceil(L/2), Kc = floor(L/2))
+template <class A, int V, int L>
+cudaError_t fs_pass_l(int mode, const FsArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {
+    constexpr int KR = (L + 1) / 2, KC = L - KR;
+    return mode == 0 ? fs_launch<A, V, KR, 0, KC>(a, s, num_sms, launches)
+                     : fs_launch<A, V, KC, 1, KR>(a, s, num_sms, launches);
 }
 
 template <class A, int V>
-cudaError_t fs_pass_any(int K, int mode, const FsArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {
-    switch (K) {
-        case 7: return fs_pass<A, V, 7>(mode, a, s, num_sms, launches);
-        case 8: return fs_pass<A, V, 8>(mode, a, s, num_sms, launches);
-        case 9: return fs_pass<A, V, 9>(mode, a, s, num_sms, launches);
-        case 10: return fs_pass<A, V, 10>(mode, a, s, num_sms, launches);
+cudaError_t fs_pass_any(int L, int mode, const FsArgs<A>& a, cudaStream_t s, int num_sms, int* launches) {
+    switch (L) {
+        case 14: return fs_pass_l<A, V, 14>(mode, a, s, num_sms, launches);
+        case 15: return fs_pass_l<A, V, 15>(mode, a, s, num_sms, launches);
+        case 16: return fs_pass_l<A, V, 16>(mode, a, s, num_sms, launches);
+        case 17: return fs_pass_l<A, V, 17>(mode, a, s, num_sms, launches);
+        case 18: return fs_pass_l<A, V, 18>(mode, a, s, num_sms, launches);
+        case 19: return fs_pass_l<A, V, 19>(mode, a, s, num_sms, launches);
+        case 20: return fs_pass_l<A, V, 20>(mode, a, s, num_sms, launches);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -108,7 +108,7 @@ static cudaError_t fs_run(const MultipassReq& r, int Kr, int Kc) {
     a.scale = 0;
     a.count_bitrev = 1;          // DIT / Pease_nc sub-transforms bit-reverse their inputs
     cudaError_t e = cudaSuccess;
-    if (!(Kr == 10 && fs_pass_tma<V, 0>(r, Kr, Kc, &e))) e = fstep::fs_pass_any<A, V>(Kr, 0, a, r.stream, r.num_sms, r.launches);
+    if (!(Kr == 10 && fs_pass_tma<V, 0>(r, Kr, Kc, &e))) e = fstep::fs_pass_any<A, V>(Kr + Kc, 0, a, r.stream, r.num_sms, r.launches);
     if (e != cudaSuccess) return e;
     // pass B: row sub-transforms -> out[k1 + R*k2]
     a.in = static_cast<const uint32_t*>(r.ws);
@@ -116,7 +116,7 @@ static cudaError_t fs_run(const MultipassReq& r, int Kr, int Kc) {
     a.scale = r.scale;
     a.count_bitrev = 0;
     if (Kc == 10 && fs_pass_tma<V, 1>(r, Kr, Kc, &e)) return e;
-    return fstep::fs_pass_any<A, V>(Kc, 1, a, r.stream, r.num_sms, r.launches);
+    return fstep::fs_pass_any<A, V>(Kr + Kc, 1, a, r.stream, r.num_sms, r.launches);
 }
 
 cudaError_t fourstep_f32(const MultipassReq& r, bool* ok) {

@@ -27,13 +27,13 @@ static cudaError_t fsg_run(const MultipassReq& r) {
     a.out = static_cast<uint64_t*>(r.ws);
     a.scale = 0;
     a.count_bitrev = 1;          // every variant here bit-reverses (DIT/Pease on input, DIF on output)
-    cudaError_t e = fstep::fs_launch<A, V, 8, 0>(a, r.stream, r.num_sms, r.launches);
+    cudaError_t e = fstep::fs_launch<A, V, 8, 0, 8>(a, r.stream, r.num_sms, r.launches);
     if (e != cudaSuccess) return e;
     a.in = static_cast<const uint64_t*>(r.ws);
     a.out = static_cast<uint64_t*>(r.out);
     a.scale = r.scale;
     a.count_bitrev = 0;
-    return fstep::fs_launch<A, V, 8, 1>(a, r.stream, r.num_sms, r.launches);
+    return fstep::fs_launch<A, V, 8, 1, 8>(a, r.stream, r.num_sms, r.launches);
 }
 
 cudaError_t fourstep_gold(const MultipassReq& r, bool* ok) {
