@@ -48,26 +48,44 @@ NTT_D void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t
         : "memory");
 }
 
-template <int V>
+// Geometry per (variant, sub-transform length 2^K), NT = 512 threads:
+//   TQ = 2^(13-K) networks per tile (every tile holds 8192 residues), AB =
+//   in-warp thread bits above the network id.  Group splits: DIT (K0, 4, ...),
+//   Pease (4, ..., K0).  NP / in-warp bit placements from the exhaustive bank
+//   model:
+//     K = 10 (AB = 2): DIT NP = 1, group-0 lanes -> u bits 4,5, last -> 3,4;
+//                      Pease NP = 2, group 0 -> 4,5, last -> 0,1;
+//     K = 9  (AB = 1): DIT NP = 1 with network base + 8*(q >> 3), group 0 -> u4, last -> u3;
+//                      Pease NP = 1, group 0 -> u4, last -> u0;
+//     K <= 8 (AB = 0): a warp is 32 networks: NP = 1.
+template <int V, int K>
 struct TmaGeo {
-    static constexpr int K = 10, TQ = 8, NT = 512, TT = 64;
-    static constexpr int NPM = (V == V_DIT) ? 1 : 2;                  // network stride mod 32
-    static constexpr int NP = ((fastk::padded_len<uint32_t, K>() + 31) / 32) * 32 + NPM;
-    // group split: DIT (2,4,4), Pease (4,4,2)
-    static constexpr int KG0 = (V == V_DIT) ? 2 : 4;
-    static constexpr int KGL = (V == V_DIT) ? 4 : 2;
-    static constexpr int I0a = 4, I0b = 5;                            // group-0 in-warp bits -> u bits
-    static constexpr int ILa = (V == V_DIT) ? 3 : 0, ILb = (V == V_DIT) ? 4 : 1;   // last group
+    static constexpr int TQ = 1 << (13 - K), NT = 512, TT = 1 << (K - 4);
+    static constexpr int LQ = 13 - K;
+    static constexpr int AB = LQ >= 5 ? 0 : 5 - LQ;
+    static constexpr int G = (K + 3) / 4;
+    static constexpr int K0 = K - 4 * (G - 1);
+    static constexpr int KG0 = (V == V_DIT) ? K0 : 4;
+    static constexpr int KGL = (V == V_DIT) ? 4 : K0;
+    static constexpr int NPM = (K == 10 && V != V_DIT) ? 2 : 1;       // network stride mod 32
+    static constexpr int NP = ((fastk::padded_len<uint32_t, K>() + 8 + 31) / 32) * 32 + NPM;
+    static constexpr bool NLIN = (K == 9 && V == V_DIT);              // base(q) = q*NP + 8*(q >> 3)
+    static constexpr int I0a = 4, I0b = 5;                            // group-0 in-warp -> u bits
+    static constexpr int ILa = (V == V_DIT) ? (K == 10 ? 3 : 3) : 0;  // last group
+    static constexpr int ILb = (V == V_DIT) ? 4 : 1;
+    static NTT_HD constexpr uint32_t base(uint32_t q) { return q * NP + (NLIN ? 8 * (q >> 3) : 0); }
 };
 
-// u (6 bits) from w = tid >> 3 with w bits 0,1 (in-warp) on u bits ia, ib
-template <int ia, int ib>
-NTT_D uint32_t place2(uint32_t w) {
-    uint32_t u = ((w & 1u) << ia) | (((w >> 1) & 1u) << ib);
-    uint32_t rest = w >> 2;
+// u (K-4 bits) from w = tid >> LQ: w's AB low (in-warp) bits on u bits ia (, ib), the rest in order
+template <int UB, int AB, int ia, int ib>
+NTT_D uint32_t placeN(uint32_t w) {
+    if (AB == 0) return w;
+    uint32_t u = (w & 1u) << ia;
+    if (AB == 2) u |= ((w >> 1) & 1u) << ib;
+    uint32_t rest = w >> AB;
 #pragma unroll
-    for (int b = 0; b < 6; ++b) {
-        if (b == ia || b == ib) continue;
+    for (int b = 0; b < UB; ++b) {
+        if (b == ia || (AB == 2 && b == ib)) continue;
         u |= (rest & 1u) << b;
         rest >>= 1;
     }
@@ -79,8 +97,11 @@ NTT_D uint32_t place2(uint32_t w) {
 #endif
 // MODE 1 staging rows are skewed by 4 words (tile-major reads: 8 rows x 4 residues hit 32 banks)
 constexpr int kStgRow = 1024 + 4;
-constexpr size_t fsa_smem_bytes(int NP) {
-    return (size_t)8 * 1024 + 2 * (size_t)8 * kStgRow * 4 + (size_t)8 * NP * 4 + 16 * 8 * 8;
+template <int V, int K, int MODE>
+constexpr size_t fsa_smem_bytes() {
+    using GG = TmaGeo<V, K>;
+    return ((size_t)8 << K) + 2 * (size_t)(MODE == 0 ? 8192 : 8 * kStgRow) * 4 + (size_t)GG::base(GG::TQ) * 4 + 8 +
+           16 * (size_t)GG::TQ * 8;
 }
 
 NTT_D void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -90,40 +111,44 @@ NTT_D void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) 
                  : "memory");
 }
 
-// MODE 0: pass A (columns, tensor-map box loads, twist, rows k1 of the workspace)
-// MODE 1: pass B (rows of the workspace by 1-D bulk copies, out[k1 + R*k2])
+// MODE 0: pass A (columns, tensor-map box loads, twist, rows k1 of the workspace), 7 <= K <= 10
+// MODE 1: pass B (rows of the workspace by 1-D bulk copies, out[k1 + R*k2]), K = 10
 // KO = log2 of the other dimension (C for MODE 0, R for MODE 1), compile time so
 // every strided store / twist offset is an immediate
-template <class A, int V, int MODE, int KO>
+template <class A, int V, int MODE, int K, int KO>
 __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUtensorMap tmap, FsTmaArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
-    using GG = TmaGeo<V>;
-    constexpr int K = GG::K, TQ = GG::TQ, NT = GG::NT, TT = GG::TT, NP = GG::NP;
+    using GG = TmaGeo<V, K>;
+    static_assert(MODE == 0 || K == 10, "bulk-row pass B: 2^10 rows");
+    constexpr int TQ = GG::TQ, NT = GG::NT, TT = GG::TT, LQ = GG::LQ, AB = GG::AB, G = GG::G, K0 = GG::K0;
+    constexpr int UB = K - 4;
     constexpr int CW = fastk::lane_bits<T>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t mbar[2];
-    Tw* tws = reinterpret_cast<Tw*>(smem_raw);                           // 2^10 stage twiddles
-    T* stg = reinterpret_cast<T*>(smem_raw + 8 * 1024);                  // 2 staging tiles
-    constexpr int STG = MODE == 0 ? 8 * 1024 : 8 * kStgRow;              // MODE 0 [1024][8], MODE 1 [8][kStgRow]
-    T* W = stg + 2 * STG;                                                // [8][NP] work buffer
-    Tw* twB = reinterpret_cast<Tw*>(W + 8 * NP);                          // factored twist [c][q] (8 * NP * 4 bytes: 8-aligned)
+    Tw* tws = reinterpret_cast<Tw*>(smem_raw);                           // 2^K stage twiddles
+    T* stg = reinterpret_cast<T*>(smem_raw + ((size_t)8 << K));          // 2 staging tiles
+    constexpr int STG = MODE == 0 ? 8192 : 8 * kStgRow;                  // MODE 0 [2^K][TQ], MODE 1 [8][kStgRow]
+    T* W = stg + 2 * STG;                                                // TQ networks at GG::base(q)
+    Tw* twB = reinterpret_cast<Tw*>(W + ((GG::base(TQ) + 1) & ~1u));     // factored twist [c][q]
     A ar;
     ar.init(a.p);
     const uint32_t tid = threadIdx.x;
-    for (uint32_t i = tid; i < 1024; i += NT) tws[i] = a.stw[i];
-    constexpr int Kr = MODE == 0 ? 10 : KO, Kc = MODE == 0 ? KO : 10;
+    for (uint32_t i = tid; i < (1u << K); i += NT) tws[i] = a.stw[i];
+    constexpr int Kr = MODE == 0 ? K : KO, Kc = MODE == 0 ? KO : K;
     constexpr uint64_t N = 1ull << (Kr + Kc);
-    constexpr int tpp_log = (MODE == 0 ? Kc : Kr) - 3;   // tiles per polynomial = (C or R) / 8
+    constexpr int tpp_log = (MODE == 0 ? Kc : Kr) - LQ;   // tiles per polynomial = (C or R) / TQ
     const uint64_t ntiles = a.batch << tpp_log;
-    constexpr uint32_t TILE_BYTES = 8 * 1024 * 4;
+    constexpr uint32_t TILE_BYTES = 8192 * 4;
+    constexpr int BROWS = K >= 8 ? 256 : (1 << K);        // rows per tensor box
     auto issue = [&](uint64_t tl, int s) {
         fastk::mbar_expect_tx(&mbar[s], TILE_BYTES);
-        if (MODE == 0) {                             // 4 boxes of [256 rows][8 cols]
-            const int x = (int)((tl & ((1ull << tpp_log) - 1)) * 8);
-            const int y = (int)((tl >> tpp_log) << 10);
+        if (MODE == 0) {                             // boxes of [BROWS rows][TQ cols]
+            const int x = (int)((tl & ((1ull << tpp_log) - 1)) * TQ);
+            const int y = (int)((tl >> tpp_log) << K);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) tma_load_2d(stg + s * STG + j * 2048, &tmap, x, y + 256 * j, &mbar[s]);
+            for (int j = 0; j < (1 << K) / BROWS; ++j)
+                tma_load_2d(stg + s * STG + j * BROWS * TQ, &tmap, x, y + BROWS * j, &mbar[s]);
         } else {                                     // 8 rows of 4 KiB
             const T* src = a.in + (tl >> tpp_log) * N + (((tl & ((1ull << tpp_log) - 1)) * 8) << 10);
 #pragma unroll
@@ -142,57 +167,56 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
         if ((uint64_t)blockIdx.x < ntiles) issue(blockIdx.x, 0);
         if ((uint64_t)blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
     }
-    const uint32_t q = tid & 7, w = tid >> 3;
+    const uint32_t q = tid & (TQ - 1), w = tid >> LQ;
+    // output position of last-group register c (natural order): a(u) + b(c)
+    auto bpart = [](int c) -> uint32_t {
+        if (V == V_DIT) return (uint32_t)c << (K - 4);
+        return ((uint32_t)c >> GG::KGL) | (((uint32_t)c & ((1u << GG::KGL) - 1)) << (K - GG::KGL));
+    };
+    auto apart = [](uint32_t u) -> uint32_t { return V == V_DIT ? u : (u << (4 - GG::KGL)); };
     int it = 0;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int s = it & 1;
         const T* S = stg + s * STG;
-        // staging element (input index x, network q)
         // staging base of this thread's network (the position part added as an immediate)
         const T* Sq = S + (MODE == 0 ? q : q * kStgRow);
-        auto sidx = [&](uint32_t x) -> uint32_t { return MODE == 0 ? x * 8 : x; };
+        auto sidx = [&](uint32_t x) -> uint32_t { return MODE == 0 ? x * TQ : x; };
         T v[16];
         // ---- group 0 (tile-major): read the dense staging, write the work buffer
-        uint32_t u0;
-        if (V == V_DIT) u0 = place2<GG::I0a, GG::I0b>(w);
-        else u0 = place2<GG::I0a, GG::I0b>(w);
+        const uint32_t u0 = placeN<UB, AB, GG::I0a, GG::I0b>(w);
+        const uint32_t rb = brev(u0 << 4, K);                 // input index of position u0 << 4
         fastk::mbar_wait(&mbar[s], (it >> 1) & 1);
-        if (V == V_DIT) {
-            // block [0,4): positions u0 << 4 | c, input row brev10(position)
-            const uint32_t pbase = u0 << 4;
-            const uint32_t rb = brev(pbase, K);
 #pragma unroll
-            for (int c = 0; c < 16; ++c) v[c] = Sq[sidx(rb) + sidx(brev((uint32_t)c, 4) << 6)];
+        for (int c = 0; c < 16; ++c) v[c] = Sq[sidx(rb) + sidx(brev((uint32_t)c, 4) << (K - 4))];
+        if (V == V_DIT) {
+            // block [0,4): positions u0 << 4 | c
+            const uint32_t pbase = u0 << 4;
             ftile::t_bitwin<A, K, 0, 0, GG::KG0, false, false>(ar, v, pbase, 0u, 0, tws);
             __syncthreads();                  // staging consumed; previous tile's last group done with W
-            T* wb = W + q * NP + padpos<T>(pbase);
+            T* wb = W + GG::base(q) + padpos<T>(pbase);
 #pragma unroll
             for (int c = 0; c < 16; ++c) wb[padpos<T>((uint32_t)c)] = v[c];
         } else {
-            const uint32_t rb = brev(u0 << 4, K);
-#pragma unroll
-            for (int c = 0; c < 16; ++c) v[c] = Sq[sidx(rb) + sidx(brev((uint32_t)c, 4) << 6)];
             ftile::t_pease<A, K, 0, GG::KG0, false>(ar, v, u0, 0u, 0, tws);
             __syncthreads();
-            T* wbo = W + q * NP + padpos<T>(u0 << (4 - GG::KG0));
+            T* wbo = W + GG::base(q) + padpos<T>(u0 << (4 - GG::KG0));
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
                 const uint32_t n = c >> GG::KG0, Rb = c & ((1u << GG::KG0) - 1);
                 wbo[padpos<T>(n | (Rb << (K - GG::KG0)))] = v[c];
             }
         }
-        // factored twist of the last group: w^(k1 n2) = w^(n2 * a(u)) * w^(n2 * b(c)), k1 = a(u) + b(c)
+        // factored twist of the last group: w^(k1 n2) = w^(n2 a(u)) * w^(n2 b(c)), k1 = a(u) + b(c)
         Tw twA;
+        const uint32_t uL = placeN<UB, AB, GG::ILa, GG::ILb>(w);
         if (MODE == 0 && NTT_FSA_TWF) {
-            const uint64_t col0 = (tile & ((1ull << tpp_log) - 1)) * 8;
-            if (tid < 128) {
-                const uint32_t c = tid >> 3, t = tid & 7;
-                const uint32_t bc = (V == V_DIT) ? (c << 6) : ((c >> 2) | ((c & 3u) << 8));
-                twB[tid] = __ldg(a.tw_main + (col0 + t) * bc);
+            const uint64_t col0 = (tile & ((1ull << tpp_log) - 1)) * TQ;
+#pragma unroll
+            for (uint32_t i = tid; i < 16 * TQ; i += NT) {
+                const uint32_t c = i / TQ, t = i % TQ;
+                twB[i] = __ldg(a.tw_main + (col0 + t) * bpart((int)c));
             }
-            const uint32_t uL = place2<GG::ILa, GG::ILb>(w);
-            const uint32_t au = (V == V_DIT) ? uL : (uL << 2);
-            twA = __ldg(a.tw_main + (col0 + q) * au);
+            twA = __ldg(a.tw_main + (col0 + q) * apart(uL));
         }
         if (tid == 0) {                       // staging s is free: the tile after next
             const uint64_t nn = tile + 2 * (uint64_t)gridDim.x;
@@ -202,67 +226,77 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
             }
         }
         __syncthreads();
-        // ---- middle group (network-major)
-        {
-            const uint32_t t = tid >> 6, u = tid & (TT - 1);
-            T* sb = W + t * NP;
+        // ---- middle groups (network-major)
+#pragma unroll
+        for (int g = 1; g < G - 1; ++g) {
+            const uint32_t t = tid >> (K - 4), u = tid & (TT - 1);
+            T* sb = W + GG::base(t);
             if (V == V_DIT) {
-                constexpr int B = 2;
-                constexpr Perm PM = plan_lanes(K, B, CW);
-                const uint32_t pbase = scatter_bits<K - 4>(u, PM);
+                const int B = K0 + 4 * (g - 1);
+                uint32_t pbase = 0;
+#define NTT_TMAP(BB)                                \
+    if (B == BB) {                                  \
+        constexpr Perm PM = plan_lanes(K, BB, CW);  \
+        pbase = scatter_bits<K - 4>(u, PM);         \
+    }
+                NTT_TMAP(1) NTT_TMAP(2) NTT_TMAP(3) NTT_TMAP(4) NTT_TMAP(5)
+#undef NTT_TMAP
                 T* wb = sb + padpos<T>(pbase);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) v[c] = wb[padpos<T>((uint32_t)c << B)];
-                ftile::t_bitwin<A, K, B, B, 4, false, false>(ar, v, pbase, 0u, 0, tws);
+#define NTT_TBWM(BB) \
+    if (B == BB) ftile::t_bitwin<A, K, BB, BB, 4, false, false>(ar, v, pbase, 0u, 0, tws);
+                NTT_TBWM(1) NTT_TBWM(2) NTT_TBWM(3) NTT_TBWM(4) NTT_TBWM(5)
+#undef NTT_TBWM
 #pragma unroll
                 for (int c = 0; c < 16; ++c) wb[padpos<T>((uint32_t)c << B)] = v[c];
             } else {
-                constexpr int sg = 4;
-                const T* rb = sb + padpos<T>(u << 4);
+                const int sg = 4 * g;
+                const T* rbp = sb + padpos<T>(u << 4);
 #pragma unroll
-                for (int c = 0; c < 16; ++c) v[c] = rb[padpos<T>((uint32_t)c)];
-                ftile::t_pease<A, K, sg, 4, false>(ar, v, u, 0u, 0, tws);
+                for (int c = 0; c < 16; ++c) v[c] = rbp[padpos<T>((uint32_t)c)];
+#define NTT_TPEM(SG) \
+    if (sg == SG) ftile::t_pease<A, K, SG, 4, false>(ar, v, u, 0u, 0, tws);
+                NTT_TPEM(4) NTT_TPEM(8)
+#undef NTT_TPEM
                 __syncthreads();              // every read of the single work buffer done
                 T* wbo = sb + padpos<T>(u);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) wbo[padpos<T>((uint32_t)c << (K - 4))] = v[c];
             }
+            __syncthreads();
         }
-        __syncthreads();
-        // ---- last group (tile-major) -> twist -> workspace rows k1
+        // ---- last group (tile-major) -> twist -> workspace rows k1 / outputs
         {
-            const uint32_t u = place2<GG::ILa, GG::ILb>(w);
-            const T* sb = W + q * NP;
-            // output row of register c
-            auto xout = [&](int c) -> uint32_t {
-                if (V == V_DIT) return u | ((uint32_t)c << 6);
-                return (u << 2) | ((uint32_t)c >> 2) | (((uint32_t)c & 3u) << 8);
-            };
-            const uint64_t col = (tile & ((1ull << tpp_log) - 1)) * 8 + q;
+            const uint32_t u = uL;
+            const T* sb = W + GG::base(q);
+            const uint64_t col = (tile & ((1ull << tpp_log) - 1)) * TQ + q;
             if (V == V_DIT) {
                 const T* wb = sb + padpos<T>(u);
 #pragma unroll
-                for (int c = 0; c < 16; ++c) v[c] = wb[padpos<T>((uint32_t)c << 6)];
-                ftile::t_bitwin<A, K, 6, 6, 4, false, false>(ar, v, u, 0u, 0, tws);
+                for (int c = 0; c < 16; ++c) v[c] = wb[padpos<T>((uint32_t)c << (K - 4))];
+                ftile::t_bitwin<A, K, K - 4, K - 4, 4, false, false>(ar, v, u, 0u, 0, tws);
             } else {
-                const T* rb = sb + padpos<T>(u << 4);
+                const T* rbp = sb + padpos<T>(u << 4);
 #pragma unroll
-                for (int c = 0; c < 16; ++c) v[c] = rb[padpos<T>((uint32_t)c)];
-                ftile::t_pease<A, K, 8, GG::KGL, false>(ar, v, u, 0u, 0, tws);
+                for (int c = 0; c < 16; ++c) v[c] = rbp[padpos<T>((uint32_t)c)];
+                ftile::t_pease<A, K, K - GG::KGL, GG::KGL, false>(ar, v, u, 0u, 0, tws);
             }
+            const uint32_t au = apart(u);
             T* dst = a.out + (tile >> tpp_log) * N + col;    // MODE 0: column n2; MODE 1: row k1
             if (MODE == 0) {
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
-                    if (NTT_FSA_TWF) dst[(uint64_t)xout(c) << Kc] = ar.mull(ar.mull(v[c], ftile::lds_tw(&twB[c * 8 + q])), twA);
-                    else dst[(uint64_t)xout(c) << Kc] = ar.mulc(v[c], __ldg(a.twist + col + ((uint64_t)xout(c) << Kc)));
+                    const uint64_t ro = (uint64_t)(au + bpart(c)) << Kc;
+                    if (NTT_FSA_TWF) dst[ro] = ar.mull(ar.mull(v[c], ftile::lds_tw(&twB[c * TQ + q])), twA);
+                    else dst[ro] = ar.mulc(v[c], __ldg(a.twist + col + ro));
                 }
             } else if (a.scale) {
 #pragma unroll
-                for (int c = 0; c < 16; ++c) dst[(uint64_t)xout(c) << Kr] = ar.mulc(v[c], a.ninv);
+                for (int c = 0; c < 16; ++c) dst[(uint64_t)(au + bpart(c)) << Kr] = ar.mulc(v[c], a.ninv);
             } else {
 #pragma unroll
-                for (int c = 0; c < 16; ++c) dst[(uint64_t)xout(c) << Kr] = ar.fin(v[c]);
+                for (int c = 0; c < 16; ++c) dst[(uint64_t)(au + bpart(c)) << Kr] = ar.fin(v[c]);
             }
         }
         if (a.counters && tid == 0 && (tile & ((1ull << tpp_log) - 1)) == 0) {

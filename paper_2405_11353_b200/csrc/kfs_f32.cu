@@ -35,32 +35,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-// a pass of length 2^10 with TMA / bulk-copy tile loads (fourstep_tma.cuh): true when it ran
-template <int V, int MODE>
-static bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err) {
+// a pass with TMA / bulk-copy tile loads (fourstep_tma.cuh): K = the pass's
+// sub-transform length, KO = the other dimension
+template <int V, int MODE, int K, int KO>
+static cudaError_t fs_pass_tma_k(const MultipassReq& r, const CUtensorMap& map) {
     using A = LazyF32;
-    *err = cudaSuccess;
-    const void* src = MODE == 0 ? r.in : r.ws;
-    if (!fs_tma_enabled() || (reinterpret_cast<uintptr_t>(src) & 15)) return false;
-    CUtensorMap map;
-    memset(&map, 0, sizeof(map));
-    if (MODE == 0) {
-        auto enc = tensor_map_encoder();
-        if (!enc) return false;
-        cuuint64_t dims[2] = {(cuuint64_t)1 << Kc, (cuuint64_t)r.batch << Kr};
-        cuuint64_t strides[1] = {((cuuint64_t)1 << Kc) * 4};
-        cuuint32_t box[2] = {8, 256};
-        cuuint32_t es[2] = {1, 1};
-        if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(src), dims, strides, box, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                NTT_FSA_L2PROMO == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                : NTT_FSA_L2PROMO == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                : NTT_FSA_L2PROMO == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return false;
-    }
+    using GG = fstep::TmaGeo<V, K>;
+    constexpr int Kr = MODE == 0 ? K : KO, Kc = MODE == 0 ? KO : K;
     fstep::FsTmaArgs<A> a{};
-    a.in = static_cast<const uint32_t*>(src);
+    a.in = static_cast<const uint32_t*>(MODE == 0 ? r.in : r.ws);
     a.out = static_cast<uint32_t*>(MODE == 0 ? r.ws : r.out);
     a.batch = r.batch;
     a.Kr = Kr;
@@ -73,20 +56,58 @@ static bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err)
     a.ninv = make_uint2((uint32_t)r.ninv, (uint32_t)r.ninv_shoup);
     a.count_bitrev = MODE == 0 ? 1 : 0;
     a.counters = r.counters;
-    constexpr size_t smem = fstep::fsa_smem_bytes(fstep::TmaGeo<V>::NP);
-    auto kern = (MODE == 0 ? Kc : Kr) == 10 ? fstep::k_fs_tma<A, V, MODE, 10> : fstep::k_fs_tma<A, V, MODE, 9>;
+    constexpr size_t smem = fstep::fsa_smem_bytes<V, K, MODE>();
+    auto kern = fstep::k_fs_tma<A, V, MODE, K, KO>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ = 0;
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 512, smem);
-    if (e != cudaSuccess) { *err = e; return true; }
+    if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
-    const uint64_t ntiles = r.batch << ((MODE == 0 ? Kc : Kr) - 3);
+    const uint64_t ntiles = r.batch << ((MODE == 0 ? Kc : Kr) - GG::LQ);
     uint64_t grid = (uint64_t)r.num_sms * occ;
     if (grid > ntiles) grid = ntiles;
-    *err = fastk::launch_pdl(kern, dim3((unsigned)grid), dim3(512), smem, r.stream, map, a);
+    e = fastk::launch_pdl(kern, dim3((unsigned)grid), dim3(512), smem, r.stream, map, a);
     if (r.launches) ++*r.launches;
-    if (*err == cudaSuccess) *err = cudaGetLastError();
-    return true;
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// true when the pass ran through the TMA kernel (*err its status)
+template <int V, int MODE>
+static bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err) {
+    *err = cudaSuccess;
+    const void* src = MODE == 0 ? r.in : r.ws;
+    const int K = MODE == 0 ? Kr : Kc;
+    if (!fs_tma_enabled() || (reinterpret_cast<uintptr_t>(src) & 15)) return false;
+    if (MODE == 1 && K != 10) return false;
+    if (K < 7 || K > 10) return false;
+    CUtensorMap map;
+    memset(&map, 0, sizeof(map));
+    if (MODE == 0) {
+        auto enc = tensor_map_encoder();
+        if (!enc) return false;
+        const int tq = 1 << (13 - K);
+        cuuint64_t dims[2] = {(cuuint64_t)1 << Kc, (cuuint64_t)r.batch << Kr};
+        cuuint64_t strides[1] = {((cuuint64_t)1 << Kc) * 4};
+        cuuint32_t box[2] = {(cuuint32_t)tq, (cuuint32_t)(K >= 8 ? 256 : (1 << K))};
+        cuuint32_t es[2] = {1, 1};
+        if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(src), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                NTT_FSA_L2PROMO == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : NTT_FSA_L2PROMO == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                : NTT_FSA_L2PROMO == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    // (K, other dimension) pairs of 2^14 .. 2^20 (Kr = ceil(L/2), Kc = floor(L/2))
+#define NTT_FSTK(KK, KOO) \
+    if (K == KK && (MODE == 0 ? Kc : Kr) == KOO) { *err = fs_pass_tma_k<V, MODE, KK, KOO>(r, map); return true; }
+    if constexpr (MODE == 0) {
+        NTT_FSTK(7, 7) NTT_FSTK(8, 7) NTT_FSTK(8, 8) NTT_FSTK(9, 8) NTT_FSTK(9, 9) NTT_FSTK(10, 9) NTT_FSTK(10, 10)
+    } else {
+        NTT_FSTK(10, 10)
+    }
+#undef NTT_FSTK
+    return false;
 }
 
 template <int V>
@@ -108,14 +129,14 @@ static cudaError_t fs_run(const MultipassReq& r, int Kr, int Kc) {
     a.scale = 0;
     a.count_bitrev = 1;          // DIT / Pease_nc sub-transforms bit-reverse their inputs
     cudaError_t e = cudaSuccess;
-    if (!(Kr == 10 && fs_pass_tma<V, 0>(r, Kr, Kc, &e))) e = fstep::fs_pass_any<A, V>(Kr + Kc, 0, a, r.stream, r.num_sms, r.launches);
+    if (!fs_pass_tma<V, 0>(r, Kr, Kc, &e)) e = fstep::fs_pass_any<A, V>(Kr + Kc, 0, a, r.stream, r.num_sms, r.launches);
     if (e != cudaSuccess) return e;
     // pass B: row sub-transforms -> out[k1 + R*k2]
     a.in = static_cast<const uint32_t*>(r.ws);
     a.out = static_cast<uint32_t*>(r.out);
     a.scale = r.scale;
     a.count_bitrev = 0;
-    if (Kc == 10 && fs_pass_tma<V, 1>(r, Kr, Kc, &e)) return e;
+    if (fs_pass_tma<V, 1>(r, Kr, Kc, &e)) return e;
     return fstep::fs_pass_any<A, V>(Kr + Kc, 1, a, r.stream, r.num_sms, r.launches);
 }
 
