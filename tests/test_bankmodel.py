@@ -51,3 +51,12 @@ def test_small_networks_conflict_as_documented():
     best = min(bk.score("dit", 8, 32, 512, NP, 4, bk.SHAPES["dit"])[0] for NP in range(264, 297))
     _, ideal = bk.score("dit", 8, 32, 512, 265, 4, bk.SHAPES["dit"])
     assert best / ideal > 1.5
+
+
+@pytest.mark.parametrize("V", ["dit", "pease"])
+@pytest.mark.parametrize("K", [7, 8, 9, 10])
+def test_tma_fourstep_column_pass_is_conflict_free(V, K):
+    """fourstep_tma.cuh TmaGeo<V, K>: the tile-major groups (dense TMA staging
+    reads, padded work-buffer writes, last-group reads) of the shipped geometry"""
+    import bank_fs
+    assert bank_fs.worst_conflict(V, K) == 1
