@@ -402,6 +402,8 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
         GinB[0][threadIdx.x] = row * RS + t_gpos_in<A, V, K, LAY>(a, tileQ(blockIdx.x, threadIdx.x), 0);
     }
     __syncthreads();
+    fastk::pdl_trigger();                      // PDL: prologue (plan tables, indices) overlapped;
+    fastk::pdl_wait();                         // the previous launch's output visible from here on
     if (PF && (uint64_t)blockIdx.x < ntiles) prefetch(blockIdx.x, GinB[0]);
     cp_async_commit();
 
@@ -692,9 +694,9 @@ cudaError_t launch_tile(const TileArgs<A>& a, cudaStream_t s, int num_sms, int* 
     uint64_t grid = (uint64_t)num_sms * occ;
     if (grid > ntiles) grid = ntiles;
     if (grid == 0) return cudaSuccess;
-    kern<<<(unsigned)grid, NT, smem, s>>>(a);
+    cudaError_t le = fastk::launch_pdl(kern, dim3((unsigned)grid), dim3(NT), smem, s, a);
     if (launches) ++*launches;
-    return cudaGetLastError();
+    return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 }  // namespace ftile

@@ -215,6 +215,8 @@ __global__ void __launch_bounds__(256) k_transpose(const T* in, T* out, uint64_t
     const uint64_t R = 1ull << rb, C = 1ull << cb;
     const int pb = rb + cb - 10;                                // log2 tiles per matrix
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;     // 32 x 8
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // PDL (no-op without the attribute)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (uint64_t blk = blockIdx.x; blk < (batch << pb); blk += gridDim.x) {
         const uint64_t row = blk >> pb, b = blk & ((1ull << pb) - 1);
         const uint64_t br = (b >> (cb - 5)) << 5, bc = (b & ((C >> 5) - 1)) << 5;

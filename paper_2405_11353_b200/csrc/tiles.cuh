@@ -377,9 +377,10 @@ cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
     {
         const uint64_t blocks = r.batch << (K1 + K2 - 10);
         const uint64_t cap = (uint64_t)r.num_sms * 8;
-        k_transpose<T><<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, r.stream>>>(ws1, ws0, r.batch, K2, K1);
+        e = fastk::launch_pdl(k_transpose<T>, dim3((unsigned)(blocks < cap ? blocks : cap)), dim3(256), 0, r.stream,
+                              static_cast<const T*>(ws1), ws0, r.batch, K2, K1);
         if (r.launches) ++*r.launches;
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return e;
     }
     // step B: rows (length n1, inner k2); output = out[k1*n2 + k2]
     cur = ws0;
