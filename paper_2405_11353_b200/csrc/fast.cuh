@@ -288,7 +288,7 @@ NTT_D void stockham_regs(const A& ar, typename A::T (&v)[RN], uint32_t hi, const
 // -------------------------------------------------------------- kernel ----
 // SC: n^-1 scaling compiled in (a runtime flag would leave the predicated-off
 // multiply in the store loop: 5 issue slots per residue)
-template <class A, int V, int L, int TEAMS, bool SC, int RB>
+template <class A, int V, int L, int TEAMS, bool SC, int RB, bool DS>
 __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
@@ -309,21 +309,23 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     constexpr bool STG_ = (RB == 4);
     constexpr int NBUF = TWO ? 3 : 2;      // staging + work (+ second work buffer for Pease)
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ uint64_t mbar[TEAMS];
+    // DS: two staging buffers per team, the polynomial after next in flight
+    constexpr int NSTG = STG_ ? (DS ? 2 : 1) : 0;
+    __shared__ uint64_t mbar[TEAMS * 2];
 
     Tw* stw = reinterpret_cast<Tw*>(smem_raw);
     const int team = threadIdx.x / TT;
     const uint32_t t = threadIdx.x % TT;
     constexpr int NP = padded_len<T, L>();
-    T* S = reinterpret_cast<T*>(smem_raw + (size_t)N * sizeof(Tw)) + (size_t)team * ((STG_ ? N : 0) + (NBUF - 1) * NP);
-    T* W0 = S + (STG_ ? N : 0);
+    T* S = reinterpret_cast<T*>(smem_raw + (size_t)N * sizeof(Tw)) + (size_t)team * (NSTG * N + (NBUF - 1) * NP);
+    T* W0 = S + NSTG * N;
     T* W1 = TWO ? W0 + NP : W0;
     A ar;
     ar.init(a.p);
 
     // twiddle table once per CTA; barriers
     for (int i = threadIdx.x; i < N; i += blockDim.x) stw[i] = a.stw[i];
-    if (t == 0) mbar_init(&mbar[team], 1);
+    if (t == 0) { mbar_init(&mbar[2 * team], 1); mbar_init(&mbar[2 * team + 1], 1); }
     fence_mbar_init();
     __syncthreads();
     // programmatic dependent launch: the prologue above (plan-owned tables only)
@@ -335,22 +337,26 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     uint64_t poly = (uint64_t)blockIdx.x * TEAMS + team;
     const uint32_t bytes = N * sizeof(T);
     if (STG_ && t == 0 && poly < a.batch) {
-        mbar_expect_tx(&mbar[team], bytes);
-        tma_load_1d(S, a.in + poly * N, bytes, &mbar[team]);
+        mbar_expect_tx(&mbar[2 * team], bytes);
+        tma_load_1d(S, a.in + poly * N, bytes, &mbar[2 * team]);
+        if (DS && poly + stride < a.batch) {
+            mbar_expect_tx(&mbar[2 * team + 1], bytes);
+            tma_load_1d(S + N, a.in + (poly + stride) * N, bytes, &mbar[2 * team + 1]);
+        }
     }
-    uint32_t phase = 0;
+    uint32_t it = 0;
     int copies = 0;
     const int bar_id = 1 + team;
 
     for (; poly < a.batch; poly += stride) {
         T v[RV];
-        if (STG_) {
-            mbar_wait(&mbar[team], phase);
-            phase ^= 1;
-        }
-        const T* S0 = STG_ ? S : a.in + poly * N;   // first-group source
+        const uint32_t sb_ = DS ? (it & 1) : 0;     // staging buffer of this polynomial
+        if (STG_) mbar_wait(&mbar[2 * team + sb_], DS ? ((it >> 1) & 1) : (it & 1));
+        ++it;
+        T* Sb = S + sb_ * N;
+        const T* S0 = STG_ ? Sb : a.in + poly * N;   // first-group source
         T* gout = a.out + poly * N;
-        const uint64_t next = poly + stride;
+        const uint64_t next = poly + (DS ? 2 : 1) * stride;   // the polynomial this buffer loads next
 
         if (V == V_DIT || V == V_DIF) {
 #pragma unroll
@@ -387,8 +393,8 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                     if (STG_) team_sync(bar_id, TT);      // staging consumed: prefetch the next row
                     if (STG_ && t == 0 && next < a.batch) {
                         fence_proxy_async();
-                        mbar_expect_tx(&mbar[team], bytes);
-                        tma_load_1d(S, a.in + next * N, bytes, &mbar[team]);
+                        mbar_expect_tx(&mbar[2 * team + sb_], bytes);
+                        tma_load_1d(Sb, a.in + next * N, bytes, &mbar[2 * team + sb_]);
                     }
                 }
                 // ---- stages
@@ -452,8 +458,8 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                         if (STG_) team_sync(bar_id, TT);
                         if (STG_ && t == 0 && next < a.batch) {
                             fence_proxy_async();
-                            mbar_expect_tx(&mbar[team], bytes);
-                            tma_load_1d(S, a.in + next * N, bytes, &mbar[team]);
+                            mbar_expect_tx(&mbar[2 * team + sb_], bytes);
+                            tma_load_1d(Sb, a.in + next * N, bytes, &mbar[2 * team + sb_]);
                         }
                     }
 #define NTT_PE(SG, KGV) \
@@ -494,8 +500,8 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                         if (STG_) team_sync(bar_id, TT);
                         if (STG_ && t == 0 && next < a.batch) {
                             fence_proxy_async();
-                            mbar_expect_tx(&mbar[team], bytes);
-                            tma_load_1d(S, a.in + next * N, bytes, &mbar[team]);
+                            mbar_expect_tx(&mbar[2 * team + sb_], bytes);
+                            tma_load_1d(Sb, a.in + next * N, bytes, &mbar[2 * team + sb_]);
                         }
                     }
 #define NTT_ST(SG, KGV) \
@@ -548,6 +554,9 @@ constexpr int kFastMaxThreads = NTT_FAST_MAX_THREADS;
 // butterfly from 10.3 to 7.8 but caps a CTA at 512 threads (128 registers):
 // measured 48 us vs 38 us for RB = 4 on config 2 (4 warps/SMSP cannot hide the
 // dependency latency; profiles/r1/summary.md).  Kept selectable for study.
+#ifndef NTT_FAST_DS
+#define NTT_FAST_DS 1     // double staging where the shared memory allows it without losing a team
+#endif
 #ifndef NTT_FAST_WIDE_RB
 #define NTT_FAST_WIDE_RB 4
 #endif
@@ -561,13 +570,22 @@ struct FastCfg {
     static constexpr int RB = (sizeof(T) == 4 && (L == 11 || L == 12)) ? NTT_FAST_WIDE_RB : 4;
     static constexpr int TT = 1 << (L - RB);
     static constexpr int NBUF = (V == V_PEASE) ? 3 : 2;
-    static constexpr long kSmemCap = 227 * 1024 - 1024;
+    // opt-in limit per block (227 KiB, static shared memory included) minus the mbarriers
+    static constexpr long kSmemCap = 227 * 1024 - 256;
     static constexpr long table = (long)N * sizeof(Tw);
-    static constexpr long team_bytes = ((RB == 4 ? (long)N : 0L) + (long)(NBUF - 1) * padded_len<T, L>()) * sizeof(T);
-    static constexpr int by_smem = (int)((kSmemCap - table) / team_bytes);
-    static constexpr int by_thr = kFastMaxThreads / TT;
-    static constexpr int t0 = by_smem < by_thr ? by_smem : by_thr;
-    static constexpr int TEAMS = t0 > 8 ? 8 : (t0 < 0 ? 0 : t0);
+    static constexpr long team_bytes_n(int nstg) {
+        return ((RB == 4 ? (long)N * nstg : 0L) + (long)(NBUF - 1) * padded_len<T, L>()) * sizeof(T);
+    }
+    static constexpr int teams_n(int nstg) {
+        const int by_smem = (int)((kSmemCap - table) / team_bytes_n(nstg));
+        const int by_thr = kFastMaxThreads / TT;
+        const int t0 = by_smem < by_thr ? by_smem : by_thr;
+        return t0 > 8 ? 8 : (t0 < 0 ? 0 : t0);
+    }
+    // double staging (two polynomials in flight per team) where it costs no team
+    static constexpr bool DS = NTT_FAST_DS && RB == 4 && teams_n(2) == teams_n(1);
+    static constexpr int TEAMS = teams_n(DS ? 2 : 1);
+    static constexpr long team_bytes = team_bytes_n(DS ? 2 : 1);
     static constexpr long smem = table + (long)TEAMS * team_bytes;
 };
 
@@ -578,7 +596,7 @@ cudaError_t launch_fast_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int
         *ok = false;
         return cudaSuccess;
     } else {
-        auto kern = a.scale ? k_fast<A, V, L, C::TEAMS, true, C::RB> : k_fast<A, V, L, C::TEAMS, false, C::RB>;
+        auto kern = a.scale ? k_fast<A, V, L, C::TEAMS, true, C::RB, C::DS> : k_fast<A, V, L, C::TEAMS, false, C::RB, C::DS>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
         if (e != cudaSuccess) return e;
         uint64_t ctas = (a.batch + C::TEAMS - 1) / C::TEAMS;
