@@ -256,6 +256,28 @@ NTT_HD constexpr int tile_stride() {
     return n;
 }
 
+// Network base of a tile: t * NP, except the u64 column-layout tiles with 4-8
+// threads per network (config 5's 2^6 / 2^7 passes), where a warp spans 4-8
+// networks and no linear stride keeps both the vector copies and the DIT
+// register groups conflict-free; there base(t) = t * NP + (t >> XS) with the
+// NP / XS an exhaustive bank search chose (tools/bankcheck.py replays it).
+template <class T, int K, int TQ, int LAY>
+NTT_HD constexpr int tile_np() {
+    if (sizeof(T) == 8 && LAY == 3 && K == 7 && TQ == 32) return (padded_len<T, K>() + 16 + 15) / 16 * 16 + 4;
+    if (sizeof(T) == 8 && LAY == 3 && K == 6 && TQ == 64) return (padded_len<T, K>() + 16 + 15) / 16 * 16 + 2;
+    return tile_stride<T, K, TQ>();
+}
+template <class T, int K, int TQ, int LAY>
+NTT_HD constexpr int tile_xs() {
+    if (sizeof(T) == 8 && LAY == 3 && K == 7 && TQ == 32) return 2;
+    if (sizeof(T) == 8 && LAY == 3 && K == 6 && TQ == 64) return 3;
+    return 0;
+}
+template <class T, int K, int TQ, int LAY>
+NTT_HD constexpr uint32_t tile_nbase(uint32_t t) {
+    return t * (uint32_t)tile_np<T, K, TQ, LAY>() + (tile_xs<T, K, TQ, LAY>() ? (t >> tile_xs<T, K, TQ, LAY>()) : 0u);
+}
+
 template <int K, int TQ>
 struct TileGeo {
     static constexpr int TT = 1 << (K - 4);       // threads per network
@@ -286,7 +308,7 @@ constexpr size_t tile_smem_bytes() {
     constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);
     constexpr int TT = 1 << (K - 4);
     constexpr bool ONEBUF = (TQ * TT) / NT == 1;
-    const size_t bufs = (PP && !ONEBUF ? 2 : 1) * (size_t)TQ * tile_stride<T, K, TQ>() * sizeof(T);
+    const size_t bufs = (PP && !ONEBUF ? 2 : 1) * (size_t)tile_nbase<T, K, TQ, LAY>(TQ) * sizeof(T);
     const size_t head = ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * tw_row<K>() : 0);
     return ((head + bufs + 15) & ~(size_t)15) + ((LAY == 0 && NTT_TILE_PF_U64 >= (int)sizeof(T) - 4) ? ((size_t)TQ << K) * sizeof(T) : 0);
 }
@@ -299,7 +321,8 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
     using GG = TileGeo<K, TQ>;
     constexpr int TT = GG::TT, G = GG::G, K0 = GG::K0;
     constexpr int CW = fastk::lane_bits<T>();
-    constexpr int NP = tile_stride<T, K, TQ>();
+    constexpr int NP = tile_np<T, K, TQ, LAY>();
+    auto nb = [](uint32_t t) -> uint32_t { return tile_nbase<T, K, TQ, LAY>(t); };
     constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);
     constexpr int REP = (TQ * TT) / NT;             // sub-networks per thread per group
     constexpr int VE = 16 / sizeof(T);              // residues per 16-byte vector
@@ -324,11 +347,11 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
     Tw* twl = tws + (1 << SMB);
     Tw* twh = twl + TQ * TSL;
     T* bufA = reinterpret_cast<T*>(smem_raw + ((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * tw_row<K>() : 0));
-    T* bufB = (PP && !ONEBUF) ? bufA + TQ * NP : bufA;
+    T* bufB = (PP && !ONEBUF) ? bufA + nb(TQ) : bufA;
     // staging buffer: the next tile's input, raw gather order, filled by
     // cp.async while the current tile runs its register groups
     T* stage = !PF ? nullptr : reinterpret_cast<T*>(
-        (reinterpret_cast<uintptr_t>(bufA + ((PP && !ONEBUF) ? 2 : 1) * TQ * NP) + 15) & ~(uintptr_t)15);
+        (reinterpret_cast<uintptr_t>(bufA + ((PP && !ONEBUF) ? 2 : 1) * nb(TQ)) + 15) & ~(uintptr_t)15);
     A ar;
     ar.init(a.p);
     const int L = a.L, S0 = a.S0;
@@ -447,7 +470,7 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
                 // one position per vector: local index, its padded offset and the twist index
                 const uint32_t xl = a.rev_local ? brev(x, K) : x;
                 const uint32_t xr = (a.twist == 2) ? xl : brev(xl, K);
-                T* db = bufA + t0 * NP + padpos<T>(xl);
+                T* db = bufA + nb(t0) + padpos<T>(xl);       // t0 + e stays in t0's (t >> XS) class
 #pragma unroll
                 for (int e = 0; e < VE; ++e) {
                     T v = tmp[e];
@@ -467,7 +490,7 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
                 // per-vector part and a compile-time part (disjoint bits: padpos is additive)
                 constexpr int EB = VE == 4 ? 2 : 1;
                 const uint32_t nat0 = x0, rev0 = brev(x0, K);
-                T* db = bufA + t * NP + padpos<T>(a.rev_local ? rev0 : nat0);
+                T* db = bufA + nb(t) + padpos<T>(a.rev_local ? rev0 : nat0);
 #pragma unroll
                 for (int e = 0; e < VE; ++e) {
                     const uint32_t ce = (uint32_t)e, cr = brev((uint32_t)e, EB) << (K - EB);
@@ -489,7 +512,7 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
                 else { const int lb = LTQ - a.la; const uint32_t tb = i & ((1u << lb) - 1), ta = (i >> lb) & (a.TA - 1); t = ta + (tb << a.la); x = i / TQ; }
                 T v = PF ? stage[i] : __ldg(a.in + GinB[pbuf][t] + t_gpos_in<A, V, K, LAY>(a, 0u, x));
                 if (TWB && a.twist && a.twist < 3) v = twistv(v, t, a.rev_local ? brev(x, K) : x);
-                bufA[t * NP + padpos<T>(a.rev_local ? brev(x, K) : x)] = v;
+                bufA[nb(t) + padpos<T>(a.rev_local ? brev(x, K) : x)] = v;
             }
         }
         __syncthreads();                       // staging consumed, tile in the work buffer
@@ -522,8 +545,8 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
                 const uint32_t tid = threadIdx.x + r * NT;
                 const uint32_t t = tid / TT, u = tid % TT;
                 const uint32_t Q = loc ? 0u : Qs[t];
-                T* sb = src + t * NP;
-                T* db = dst + t * NP;
+                T* sb = src + nb(t);
+                T* db = dst + nb(t);
                 if (V == V_DIT || V == V_DIF) {
                     const int B = (V == V_DIT) ? (g == 0 ? 0 : K0 + 4 * (g - 1)) : (g == G - 1 ? 0 : K - 4 * (g + 1));
                     const int kg = (V == V_DIT) ? (g == 0 ? K0 : 4) : (g == G - 1 ? K0 : 4);
@@ -644,7 +667,7 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
                 const uint32_t t0 = (i % (TQ / VE)) * VE, x = i / (TQ / VE);
                 T tmp[VE];
 #pragma unroll
-                for (int e = 0; e < VE; ++e) tmp[e] = finish(t0 + e, x, res[(t0 + e) * NP + padpos<T>(x)]);
+                for (int e = 0; e < VE; ++e) tmp[e] = finish(t0 + e, x, res[nb(t0 + e) + padpos<T>(x)]);
                 *reinterpret_cast<uint4*>(a.out + gb + t_gpos_out<A, V, K, LAY>(a, 0u, x)) =
                     *reinterpret_cast<uint4*>(tmp);
             }
@@ -654,7 +677,7 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
                 const uint32_t t = i / ((1u << K) / VE), x0 = (i % ((1u << K) / VE)) * VE;
                 T tmp[VE];
 #pragma unroll
-                for (int e = 0; e < VE; ++e) tmp[e] = finish(t, x0 + e, res[t * NP + padpos<T>(x0 + e)]);
+                for (int e = 0; e < VE; ++e) tmp[e] = finish(t, x0 + e, res[nb(t) + padpos<T>(x0 + e)]);
                 *reinterpret_cast<uint4*>(a.out + Gout[t] + t_gpos_out<A, V, K, LAY>(a, 0u, x0)) =
                     *reinterpret_cast<uint4*>(tmp);
             }
@@ -664,7 +687,7 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
                 if (a.out_order == TO_C_FAST) { t = i >> K; x = i & ((1u << K) - 1); }
                 else if (a.out_order == TO_T_FAST) { t = i % TQ; x = i / TQ; }
                 else { const int lb = LTQ - a.la; const uint32_t tb = i & ((1u << lb) - 1), ta = (i >> lb) & (a.TA - 1); t = ta + (tb << a.la); x = i / TQ; }
-                a.out[Gout[t] + t_gpos_out<A, V, K, LAY>(a, 0u, x)] = finish(t, x, res[t * NP + padpos<T>(x)]);
+                a.out[Gout[t] + t_gpos_out<A, V, K, LAY>(a, 0u, x)] = finish(t, x, res[nb(t) + padpos<T>(x)]);
             }
         }
         if (a.counters && threadIdx.x == 0 && tile % tiles_per_row == 0) {

@@ -60,3 +60,13 @@ def test_tma_fourstep_column_pass_is_conflict_free(V, K):
     reads, padded work-buffer writes, last-group reads) of the shipped geometry"""
     import bank_fs
     assert bank_fs.worst_conflict(V, K) == 1
+
+
+@pytest.mark.parametrize("K,TQ", [(7, 32), (6, 64)])
+def test_u64_column_tiles_nonlinear_base(K, TQ):
+    """config 5's column/row passes: the shipped base(t) = t*NP + (t >> XS) is
+    conflict-free (2 wavefronts = one 256-byte warp access) where the linear
+    tile_stride was 2-way conflicted"""
+    NP, XS = bk.cols_u64_nbase(K, TQ)
+    assert bk.cols_u64_worst(K, TQ, NP, XS) == 2
+    assert bk.cols_u64_worst(K, TQ, tile_stride(K, TQ, 8), 0) > 2

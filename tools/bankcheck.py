@@ -220,3 +220,30 @@ def breakdown(V, K, TQ, NP, word=4, passes=None):
             a[0] += wavefronts(lanes, word)
             a[1] += 1
     return {k: round(v[0] / v[1], 2) for k, v in out.items()}
+
+
+# ---- u64 column-layout tiles (config 5's 2^6 / 2^7 passes): non-linear network base
+def cols_u64_nbase(K, TQ):
+    """csrc/fasttile.cuh tile_nbase<uint64_t, K, TQ, TL_COLS>: (NP, XS)"""
+    npb = (padded_len(K, 8) + 16 + 15) // 16 * 16
+    return {(7, 32): (npb + 4, 2), (6, 64): (npb + 2, 3)}[(K, TQ)]
+
+
+def cols_u64_worst(K, TQ, NP, XS):
+    """worst wavefronts per warp access (2 = ideal for 8-byte lanes) of the T-fast
+    vector copies and the DIT register groups (plan_lanes maps) of one tile"""
+    base = lambda t: t * NP + (t >> XS if XS else 0)
+    TT, G, K0 = geo(K)
+    worst = 0
+    for e in range(2):                                   # 16-byte vector copies, lane i -> (t0 + e, x)
+        for x in range(4):
+            lanes = [base((i % (TQ // 2)) * 2 + e) + padpos(i // (TQ // 2) + x * (32 // (TQ // 2)), 8) for i in range(32)]
+            worst = max(worst, wavefronts(lanes, 8))
+    for g in range(G):
+        B = 0 if g == 0 else K0 + 4 * (g - 1)
+        bits = plan_lanes(K, B, 4)
+        for w0 in range(0, TQ * TT, 32):
+            for c in range(16):
+                lanes = [base(tid // TT) + padpos(scatter_bits(tid % TT, bits) | (c << B), 8) for tid in range(w0, w0 + 32)]
+                worst = max(worst, wavefronts(lanes, 8))
+    return worst
