@@ -241,8 +241,9 @@ struct ntt_plan_s {
     void* fst = nullptr;
     int num_sms = 148;
     // workspace for multi-pass plans and host-buffer execution
-    void* ws = nullptr;
-    uint64_t ws_bytes = 0;
+    // multi-pass workspace, one per CUDA stream: a plan is immutable and may run
+    // concurrently on several streams (each stream's passes are stream-ordered)
+    std::map<cudaStream_t, std::pair<void*, uint64_t>> ws;
     void* hbuf = nullptr;
     uint64_t hbuf_bytes = 0;
     // host-exec pipeline: hs[0] H2D copies, hs[1] transforms, hs[2] D2H copies,
@@ -250,12 +251,14 @@ struct ntt_plan_s {
     static constexpr int kMaxChunks = 64;
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t hev[2 * kMaxChunks] = {};
-    std::mutex mu;
+    std::mutex mu;        // guards ws / hbuf / stream + event creation
+    std::mutex host_mu;   // serialises ntt_exec_host calls (one host pipeline per plan)
     ~ntt_plan_s() {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(device);
-        if (ws) cudaFree(ws);
+        for (auto& kv : ws)
+            if (kv.second.first) cudaFree(kv.second.first);
         if (hbuf) cudaFree(hbuf);
         for (auto st : hs)
             if (st) cudaStreamDestroy(st);
@@ -495,10 +498,13 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
     if (!d_in || !d_out) return fail(NTT_E_INVALID, "NULL buffer");
     unsigned long long* ctr = dev_counters(plan->device);
     uint64_t need = ntt_plan_workspace_bytes(plan, batch);
+    void* ws = nullptr;
     if (need) {
         std::lock_guard<std::mutex> lk(plan->mu);
-        int st = grow(plan->ws, plan->ws_bytes, need);
+        auto& slot = plan->ws[stream];
+        int st = grow(slot.first, slot.second, need);
         if (st) return st;
+        ws = slot.first;
     }
     int launches = 0;
     MultipassReq r{};
@@ -506,7 +512,7 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
     r.tw = plan->table->tw; r.stw = plan->table->stw; r.p = plan->p; r.scale = scale;
     r.ninv = plan->table->n_inv; r.ninv_shoup = plan->table->n_inv_dev_shoup;
     r.counters = ctr; r.stream = stream; r.num_sms = plan->num_sms; r.launches = &launches;
-    r.ws = plan->ws;
+    r.ws = ws;
     r.twh = plan->twh;
     r.twh_bits = plan->twh_bits;
     r.fst = plan->fst;
@@ -543,6 +549,7 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     const uint64_t row_bytes = plan->n * plan->word;
     const uint64_t bytes = batch * row_bytes;
     int st = NTT_OK;
+    std::lock_guard<std::mutex> host_lk(plan->host_mu);
     {
         std::lock_guard<std::mutex> lk(plan->mu);
         st = grow(plan->hbuf, plan->hbuf_bytes, bytes);
