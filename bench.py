@@ -316,6 +316,48 @@ def main() -> None:
             except Exception as exc:  # report, do not hide
                 extra[f"config{cfg}_{var}"] = {"error": repr(exc)[:300]}
 
+    if not args.no_extra:
+        # polymul.cyclic_mul_ntt on config 2's shape: 4096 products
+        # c = a * b mod (x^4096 - 1): forward of both operands in one launch, then
+        # ntt_exec_pointwise_inverse (product fused into the inverse's first group)
+        try:
+            p, L, B = 998244353, 12, 4096
+            n = 1 << L
+            pf = P.algorithms._device_plan(P.FieldParams(p, 3), n, args.variant, P.FORWARD, None, None, 4, local_rank)
+            pi = P.algorithms._device_plan(P.FieldParams(p, 3), n, args.variant, P.INVERSE, None, None, 4, local_rank)
+            nset = 4
+            ab = torch.randint(0, p, (nset, 2, B, n), dtype=torch.int64, device=dev).to(torch.int32).view(torch.uint32)
+            spec = torch.empty_like(ab[0])
+            cc = torch.empty_like(ab[:, 0])
+            sp = stream.cuda_stream
+            reps = max(3, min(args.steps, 20))
+            def pm(i):
+                pf.exec_device(ab[i % nset].data_ptr(), spec.data_ptr(), 2 * B, False, sp)
+                pi.pointwise_inverse(spec[0].data_ptr(), spec[1].data_ptr(), cc[i % nset].data_ptr(), B, sp)
+            with torch.cuda.stream(stream):
+                for i in range(3):
+                    pm(i)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for i in range(reps):
+                        pm(i)
+                g.replay()
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                g.replay()
+                e1.record(stream)
+                stream.synchronize()
+            t = max_over_ranks(e0.elapsed_time(e1)) / 1e3 / reps
+            extra["polymul_4096x2^12"] = {
+                "products_per_s": world * B / t, "ms_per_step": 1e3 * t, "launches_per_step": 2,
+                "hbm_alg_gbs": 3 * B * n * 4 / t / 1e9, "roofline_frac": 3 * B * n * 4 / t / 1e9 / peak,
+                "workload": "4096 cyclic products of N=2^12, P=998244353 (forward x2 in one launch + fused pointwise-inverse)"}
+            del ab, spec, cc, g
+            torch.cuda.empty_cache()
+        except Exception as exc:
+            extra["polymul_4096x2^12"] = {"error": repr(exc)[:300]}
+
     sweep = {}
     if not args.no_extra and not args.no_sweep:
         # batched u32 transforms N = 2^9 .. 2^20 at 256 MiB of residues per step (P = 998244353,

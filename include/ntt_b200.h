@@ -123,6 +123,16 @@ uint64_t ntt_plan_workspace_bytes(ntt_plan_t plan, uint64_t batch);
 int ntt_sixstep_dist_step(ntt_plan_t plan, int step, int rank, int world, const void* d_in, void* d_out,
                           void* stream);
 
+/* The second half of polymul.cyclic_mul_ntt (polymul.py:61-63, intt of the
+ * pointwise product) as ONE call: d_out = intt(d_a .* d_b) for `batch` rows,
+ * d_a / d_b the forward transforms of the operands.  `plan` must be an
+ * inverse-direction plan.  Shared-memory-resident u32 plans (p < 2^30, N =
+ * 2^9..2^13) run one fused kernel: the product is taken (Montgomery) as the
+ * inverse's first group loads its input and n^-1 (times 2^32) is applied in
+ * its last group's stores; every other plan runs the pointwise kernel + intt. */
+int ntt_exec_pointwise_inverse(ntt_plan_t plan, const void* d_a, const void* d_b, void* d_out, uint64_t batch,
+                               void* stream);
+
 /* polymul.pointwise_mul -- polymul.py:45-49: c[i] = a[i]*b[i] mod p over
  * `count` residues (device pointers, plan's field/word). */
 int ntt_pointwise_mul(ntt_plan_t plan, const void* d_a, const void* d_b, void* d_c,

@@ -40,7 +40,7 @@ NTT_FLAG_SCALE = 1
 EXPORTS = (
     "ntt_field_check", "ntt_find_primitive_root", "ntt_root_of_unity", "ntt_table_build",
     "ntt_plan_create", "ntt_plan_destroy", "ntt_plan_info", "ntt_exec", "ntt_exec_host",
-    "ntt_plan_workspace_bytes", "ntt_pointwise_mul", "ntt_sixstep_dist_step", "ntt_counters_enable", "ntt_counters_read",
+    "ntt_plan_workspace_bytes", "ntt_pointwise_mul", "ntt_exec_pointwise_inverse", "ntt_sixstep_dist_step", "ntt_counters_enable", "ntt_counters_read",
     "ntt_counters_reset", "ntt_last_error", "ntt_abi_version", "ntt_device_count",
 )
 
@@ -95,6 +95,7 @@ def load():
         L.ntt_plan_workspace_bytes.argtypes = [_vp, _u64]
         L.ntt_plan_workspace_bytes.restype = _u64
         L.ntt_pointwise_mul.argtypes = [_vp, _vp, _vp, _vp, _u64, _vp]
+        L.ntt_exec_pointwise_inverse.argtypes = [_vp, _vp, _vp, _vp, _u64, _vp]
         L.ntt_sixstep_dist_step.argtypes = [_vp, _int, _int, _int, _vp, _vp, _vp]
         L.ntt_counters_enable.argtypes = [_int]
         L.ntt_counters_read.argtypes = [ctypes.POINTER(Counters)]
@@ -146,6 +147,10 @@ class DevicePlan:
 
     def exec_host(self, in_ptr: int, out_ptr: int, batch: int, scale: bool, stream: int = 0) -> None:
         check(load().ntt_exec_host(self._h, in_ptr, out_ptr, batch, NTT_FLAG_SCALE if scale else 0, stream))
+
+    def pointwise_inverse(self, a_ptr: int, b_ptr: int, out_ptr: int, batch: int, stream: int) -> None:
+        """out = intt(a .* b) (fused on shared-memory-resident u32 plans)"""
+        check(load().ntt_exec_pointwise_inverse(self._h, a_ptr, b_ptr, out_ptr, batch, stream))
 
     def pointwise(self, a_ptr: int, b_ptr: int, c_ptr: int, count: int, stream: int) -> None:
         check(load().ntt_pointwise_mul(self._h, a_ptr, b_ptr, c_ptr, count, stream))

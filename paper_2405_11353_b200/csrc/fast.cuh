@@ -156,6 +156,7 @@ struct Geo {
 template <class A>
 struct FastArgs {
     using T = typename A::T;
+    const T* in2 = nullptr;   // PW kernels: the second operand (the product in*in2 is transformed)
     using Tw = typename A::Tw;
     const T* in;
     T* out;
@@ -288,7 +289,7 @@ NTT_D void stockham_regs(const A& ar, typename A::T (&v)[RN], uint32_t hi, const
 // -------------------------------------------------------------- kernel ----
 // SC: n^-1 scaling compiled in (a runtime flag would leave the predicated-off
 // multiply in the store loop: 5 issue slots per residue)
-template <class A, int V, int L, int TEAMS, bool SC, int RB, bool DS>
+template <class A, int V, int L, int TEAMS, bool SC, int RB, bool DS, bool PW = false>
 __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
@@ -310,7 +311,10 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     constexpr int NBUF = TWO ? 3 : 2;      // staging + work (+ second work buffer for Pease)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // DS: two staging buffers per team, the polynomial after next in flight
-    constexpr int NSTG = STG_ ? (DS ? 2 : 1) : 0;
+    // PW: the two staging buffers hold the two operands of a pointwise product
+    // that is taken as the first group reads its input (polymul.py:61-63 fused)
+    constexpr int NSTG = STG_ ? ((DS || PW) ? 2 : 1) : 0;
+    static_assert(!PW || (STG_ && !DS), "pointwise-fused kernels stage both operands");
     __shared__ uint64_t mbar[TEAMS * 2];
 
     Tw* stw = reinterpret_cast<Tw*>(smem_raw);
@@ -337,8 +341,9 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     uint64_t poly = (uint64_t)blockIdx.x * TEAMS + team;
     const uint32_t bytes = N * sizeof(T);
     if (STG_ && t == 0 && poly < a.batch) {
-        mbar_expect_tx(&mbar[2 * team], bytes);
+        mbar_expect_tx(&mbar[2 * team], PW ? 2 * bytes : bytes);
         tma_load_1d(S, a.in + poly * N, bytes, &mbar[2 * team]);
+        if (PW) tma_load_1d(S + N, a.in2 + poly * N, bytes, &mbar[2 * team]);
         if (DS && poly + stride < a.batch) {
             mbar_expect_tx(&mbar[2 * team + 1], bytes);
             tma_load_1d(S + N, a.in + (poly + stride) * N, bytes, &mbar[2 * team + 1]);
@@ -355,6 +360,11 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
         ++it;
         T* Sb = S + sb_ * N;
         const T* S0 = STG_ ? Sb : a.in + poly * N;   // first-group source
+        // first-group load (PW: the pointwise product of the two staged operands)
+        auto ld0 = [&](uint32_t idx) -> T {
+            if constexpr (PW) return ar.pwmul(S0[idx], S0[N + idx]);
+            else return ldsrc<STG_>(S0 + idx);
+        };
         T* gout = a.out + poly * N;
         const uint64_t next = poly + (DS ? 2 : 1) * stride;   // the polynomial this buffer loads next
 
@@ -386,15 +396,16 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                 for (int c = 0; c < RV; ++c) {
                     const uint32_t pos = pbase | ((uint32_t)c << B);
                     // DIT: pbase = brev(t) << 4, so brev(pos) = brev(c) << (L-4) | t (no per-residue BREV)
-                    if (first) v[c] = ldsrc<STG_>(S0 + (V == V_DIT ? ((brev((uint32_t)c, RB) << (L - RB)) | t) : pos));
+                    if (first) v[c] = ld0(V == V_DIT ? ((brev((uint32_t)c, RB) << (L - RB)) | t) : pos);
                     else v[c] = wb[padpos<T>((uint32_t)c << B)];
                 }
                 if (first) {
                     if (STG_) team_sync(bar_id, TT);      // staging consumed: prefetch the next row
                     if (STG_ && t == 0 && next < a.batch) {
                         fence_proxy_async();
-                        mbar_expect_tx(&mbar[2 * team + sb_], bytes);
+                        mbar_expect_tx(&mbar[2 * team + sb_], PW ? 2 * bytes : bytes);
                         tma_load_1d(Sb, a.in + next * N, bytes, &mbar[2 * team + sb_]);
+                        if (PW) tma_load_1d(Sb + N, a.in2 + next * N, bytes, &mbar[2 * team + sb_]);
                     }
                 }
                 // ---- stages
@@ -452,14 +463,15 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                     const T* sb = src + padpos<T>(u << RB);
 #pragma unroll
                     for (int c = 0; c < RV; ++c) {
-                        v[c] = first ? ldsrc<STG_>(S0 + ((brev((uint32_t)c, RB) << (L - RB)) | t)) : sb[padpos<T>((uint32_t)c)];   // u = brev(t)
+                        v[c] = first ? ld0((brev((uint32_t)c, RB) << (L - RB)) | t) : sb[padpos<T>((uint32_t)c)];   // u = brev(t)
                     }
                     if (first) {
                         if (STG_) team_sync(bar_id, TT);
                         if (STG_ && t == 0 && next < a.batch) {
                             fence_proxy_async();
-                            mbar_expect_tx(&mbar[2 * team + sb_], bytes);
+                            mbar_expect_tx(&mbar[2 * team + sb_], PW ? 2 * bytes : bytes);
                             tma_load_1d(Sb, a.in + next * N, bytes, &mbar[2 * team + sb_]);
+                            if (PW) tma_load_1d(Sb + N, a.in2 + next * N, bytes, &mbar[2 * team + sb_]);
                         }
                     }
 #define NTT_PE(SG, KGV) \
@@ -494,14 +506,15 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                     for (int c = 0; c < RV; ++c) {
                         // register c = (w << (RB-kg)) | x; position = hi | w | x | lo
                         const uint32_t pos = (hi << (L - sg)) | ((uint32_t)c << (lob - (RB - kg))) | lo;
-                        v[c] = first ? ldsrc<STG_>(S0 + pos) : sb[padpos<T>((uint32_t)c << (lob - (RB - kg)))];
+                        v[c] = first ? ld0(pos) : sb[padpos<T>((uint32_t)c << (lob - (RB - kg)))];
                     }
                     if (first) {
                         if (STG_) team_sync(bar_id, TT);
                         if (STG_ && t == 0 && next < a.batch) {
                             fence_proxy_async();
-                            mbar_expect_tx(&mbar[2 * team + sb_], bytes);
+                            mbar_expect_tx(&mbar[2 * team + sb_], PW ? 2 * bytes : bytes);
                             tma_load_1d(Sb, a.in + next * N, bytes, &mbar[2 * team + sb_]);
+                            if (PW) tma_load_1d(Sb + N, a.in2 + next * N, bytes, &mbar[2 * team + sb_]);
                         }
                     }
 #define NTT_ST(SG, KGV) \
@@ -561,7 +574,7 @@ constexpr int kFastMaxThreads = NTT_FAST_MAX_THREADS;
 #define NTT_FAST_WIDE_RB 4
 #endif
 
-template <class A, int V, int L>
+template <class A, int V, int L, bool PW = false>
 struct FastCfg {
     using T = typename A::T;
     using Tw = typename A::Tw;
@@ -583,9 +596,9 @@ struct FastCfg {
         return t0 > 8 ? 8 : (t0 < 0 ? 0 : t0);
     }
     // double staging (two polynomials in flight per team) where it costs no team
-    static constexpr bool DS = NTT_FAST_DS && RB == 4 && teams_n(2) == teams_n(1);
-    static constexpr int TEAMS = teams_n(DS ? 2 : 1);
-    static constexpr long team_bytes = team_bytes_n(DS ? 2 : 1);
+    static constexpr bool DS = !PW && NTT_FAST_DS && RB == 4 && teams_n(2) == teams_n(1);
+    static constexpr int TEAMS = (PW && RB != 4) ? 0 : teams_n((DS || PW) ? 2 : 1);
+    static constexpr long team_bytes = team_bytes_n((DS || PW) ? 2 : 1);
     static constexpr long smem = table + (long)TEAMS * team_bytes;
 };
 
@@ -606,6 +619,41 @@ cudaError_t launch_fast_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int
         cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(C::TEAMS * C::TT), C::smem, s, a);
         if (launches) ++*launches;
         return le != cudaSuccess ? le : cudaGetLastError();
+    }
+}
+
+// d_out = intt(in .* in2): pointwise product fused into the first group's
+// loads, n^-1 (times the Montgomery factor) into the last group's stores
+template <class A, int V, int L>
+cudaError_t launch_fast_pw_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int* launches, bool* ok) {
+    using C = FastCfg<A, V, L, true>;
+    if constexpr (C::TEAMS < 1) {
+        *ok = false;
+        return cudaSuccess;
+    } else {
+        auto kern = k_fast<A, V, L, C::TEAMS, true, C::RB, false, true>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+        if (e != cudaSuccess) return e;
+        uint64_t ctas = (a.batch + C::TEAMS - 1) / C::TEAMS;
+        uint64_t grid = ctas < (uint64_t)num_sms ? ctas : (uint64_t)num_sms;
+        *ok = true;
+        if (grid == 0) return cudaSuccess;
+        cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(C::TEAMS * C::TT), C::smem, s, a);
+        if (launches) ++*launches;
+        return le != cudaSuccess ? le : cudaGetLastError();
+    }
+}
+
+template <class A, int V>
+cudaError_t launch_fast_pw(int L, const FastArgs<A>& a, cudaStream_t s, int num_sms, int* launches, bool* ok) {
+    *ok = false;
+    switch (L) {
+        case 9: return launch_fast_pw_L<A, V, 9>(a, s, num_sms, launches, ok);
+        case 10: return launch_fast_pw_L<A, V, 10>(a, s, num_sms, launches, ok);
+        case 11: return launch_fast_pw_L<A, V, 11>(a, s, num_sms, launches, ok);
+        case 12: return launch_fast_pw_L<A, V, 12>(a, s, num_sms, launches, ok);
+        case 13: return launch_fast_pw_L<A, V, 13>(a, s, num_sms, launches, ok);
+        default: return cudaSuccess;
     }
 }
 

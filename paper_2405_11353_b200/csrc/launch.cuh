@@ -90,6 +90,24 @@ cudaError_t run_fast_policy(const MultipassReq& r, bool* ok) {
     return fastk::launch_fast<A, V>(r.L, a, r.stream, r.num_sms, r.launches, ok);
 }
 
+// intt(in .* in2) in one fast-kernel launch (LazyF32, 2^9..2^13): the caller
+// passes r.ninv / r.ninv_shoup = n^-1 * 2^32 mod p (the Montgomery factor of
+// the fused pointwise product)
+template <int V>
+cudaError_t run_fast_pw(const MultipassReq& r, const void* in2, bool* ok) {
+    fastk::FastArgs<LazyF32> a{};
+    a.in = static_cast<const uint32_t*>(r.in);
+    a.in2 = static_cast<const uint32_t*>(in2);
+    a.out = static_cast<uint32_t*>(r.out);
+    a.batch = r.batch;
+    a.stw = static_cast<const uint2*>(r.stw);
+    a.p = r.p;
+    a.scale = 1;
+    a.ninv = make_uint2((uint32_t)r.ninv, (uint32_t)r.ninv_shoup);
+    a.counters = r.counters;
+    return fastk::launch_fast_pw<LazyF32, V>(r.L, a, r.stream, r.num_sms, r.launches, ok);
+}
+
 // Specialised single-pass kernels (fast.cuh) where they apply.
 template <class F, int V>
 cudaError_t try_fast(const MultipassReq& r, bool* ok) {

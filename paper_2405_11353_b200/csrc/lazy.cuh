@@ -18,7 +18,21 @@ struct LazyF32 {
     using Field = F32S;
     static constexpr bool lazy = true;
     uint32_t p, p2, p4;
-    NTT_D void init(uint64_t pp) { p = (uint32_t)pp; p2 = 2u * (uint32_t)pp; p4 = 4u * (uint32_t)pp; }
+    uint32_t pinv;            // -p^-1 mod 2^32 (Montgomery, pointwise products)
+    NTT_D void init(uint64_t pp) {
+        p = (uint32_t)pp; p2 = 2u * (uint32_t)pp; p4 = 4u * (uint32_t)pp;
+        uint32_t x = p;                        // p * p == 1 (mod 8) for odd p; Newton doubles the bits
+        for (int i = 0; i < 4; ++i) x *= 2u - p * x;
+        pinv = 0u - x;
+    }
+    // Montgomery product a * b * 2^-32 mod p of two canonical residues, canonical
+    // (a*b + m*p < 2^62 + 2^62: no overflow); the 2^32 is folded into n^-1
+    NTT_D T pwmul(T a, T b) const {
+        const uint64_t t = (uint64_t)a * b;
+        const uint32_t m = (uint32_t)t * pinv;
+        const T r = (T)((t + (uint64_t)m * p) >> 32);
+        return umin32(r, r - p);
+    }
     // x + t written as min(x + t, 4p) (an identity: x + t < 4p): one VIADDMNMX on
     // the ALU pipe, so ptxas cannot move the add onto the FMA pipe (IMAD.IADD),
     // which IMAD.HI + 2 IMAD already saturate (tools/ubench_pipes.cu: IMAD 2,

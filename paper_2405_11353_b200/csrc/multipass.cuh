@@ -298,6 +298,8 @@ struct MultipassReq {
 int mp_num_passes(int L, int word, int variant, uint64_t p);
 uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch, uint64_t p);
 cudaError_t mp_launch_f32s(const MultipassReq& r);
+// intt(in .* in2) fused into one fast-kernel launch (u32 p < 2^30, 2^9..2^13); *ok = false otherwise
+cudaError_t pointwise_inverse_f32(const MultipassReq& r, const void* in2, bool* ok);
 // two-pass four-step for large u32 N (fourstep.cuh, kfs_f32.cu); *ok = false when it does not apply
 cudaError_t fourstep_f32(const MultipassReq& r, bool* ok);
 // four-step: LazyF32 fields (p < 2^30) DIT / Pease_nc 14 <= L <= 20, Goldilocks 2^16

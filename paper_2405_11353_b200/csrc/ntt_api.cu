@@ -244,6 +244,7 @@ struct ntt_plan_s {
     // multi-pass workspace, one per CUDA stream: a plan is immutable and may run
     // concurrently on several streams (each stream's passes are stream-ordered)
     std::map<cudaStream_t, std::pair<void*, uint64_t>> ws;
+    std::map<cudaStream_t, std::pair<void*, uint64_t>> pw_ws;   // unfused pointwise-inverse products
     void* hbuf = nullptr;
     uint64_t hbuf_bytes = 0;
     // host-exec pipeline: hs[0] H2D copies, hs[1] transforms, hs[2] D2H copies,
@@ -258,6 +259,8 @@ struct ntt_plan_s {
         cudaGetDevice(&cur);
         cudaSetDevice(device);
         for (auto& kv : ws)
+            if (kv.second.first) cudaFree(kv.second.first);
+        for (auto& kv : pw_ws)
             if (kv.second.first) cudaFree(kv.second.first);
         if (hbuf) cudaFree(hbuf);
         for (auto st : hs)
@@ -653,6 +656,46 @@ int ntt_sixstep_dist_step(ntt_plan_t plan, int step, int rank, int world, const 
     if (e != cudaSuccess) return cuda_fail(e, "distributed six-step");
     if (!ok) return fail(NTT_E_SIZE_NOT_SUPPORTED, "no compiled tile shape for this (n1, n2) split");
     return NTT_OK;
+}
+
+int ntt_exec_pointwise_inverse(ntt_plan_t plan, const void* d_a, const void* d_b, void* d_out, uint64_t batch,
+                               void* stream) {
+    if (!plan) return fail(NTT_E_INVALID, "NULL plan");
+    if (plan->dir != NTT_INVERSE) return fail(NTT_E_INVALID, "pointwise-inverse requires an inverse-direction plan");
+    if (batch == 0) return NTT_OK;
+    if (!d_a || !d_b || !d_out) return fail(NTT_E_INVALID, "NULL buffer");
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != plan->device) cudaSetDevice(plan->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int st = NTT_OK;
+    bool done = false;
+    if (plan->kind == 0 && plan->variant != NTT_NAIVE && plan->variant != NTT_SIXSTEP && plan->variant != NTT_FLAT) {
+        // fused: Montgomery product in the first group, n^-1 * 2^32 in the last
+        const uint64_t ninv_m = (uint64_t)(((u128)plan->table->n_inv << 32) % plan->p);
+        int launches = 0;
+        MultipassReq r{};
+        r.variant = plan->variant; r.L = plan->L; r.in = d_a; r.out = d_out; r.batch = batch;
+        r.tw = plan->table->tw; r.stw = plan->table->stw; r.p = plan->p; r.scale = 1;
+        r.ninv = ninv_m; r.ninv_shoup = shoup_word(ninv_m, plan->p, 32);
+        r.counters = dev_counters(plan->device); r.stream = s; r.num_sms = plan->num_sms; r.launches = &launches;
+        cudaError_t e = pointwise_inverse_f32(r, d_b, &done);
+        g_launches += launches;
+        if (e != cudaSuccess) st = cuda_fail(e, "pointwise-inverse");
+    }
+    if (!st && !done) {           // pointwise kernel into a per-stream buffer, then intt
+        void* tmp = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(plan->mu);
+            auto& slot = plan->pw_ws[s];
+            st = grow(slot.first, slot.second, batch * plan->n * plan->word);
+            tmp = slot.first;
+        }
+        if (!st) st = ntt_pointwise_mul(plan, d_a, d_b, tmp, batch * plan->n, stream);
+        if (!st) st = exec_device(plan, tmp, d_out, batch, NTT_FLAG_SCALE, s);
+    }
+    if (cur != plan->device) cudaSetDevice(cur);
+    return st;
 }
 
 int ntt_pointwise_mul(ntt_plan_t plan, const void* d_a, const void* d_b, void* d_c, uint64_t count, void* stream) {

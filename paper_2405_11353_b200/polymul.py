@@ -74,8 +74,18 @@ def cyclic_mul_ntt(a, b, params: FieldParams, variant: str = "dit"):
     if torch is not None and isinstance(a, torch.Tensor) and a.is_cuda:
         stacked = torch.stack([a.contiguous(), b.contiguous().to(a.dtype)])
         spec = _alg.ntt(stacked, fwd, variant)                 # one launch for both operands
-        prod = pointwise_mul(spec[0], spec[1], params.p)
-        return _alg.intt(prod, inv, variant)
+        if n == 1:
+            return pointwise_mul(spec[0], spec[1], params.p)
+        # intt(spec_a .* spec_b) as one call (ntt_exec_pointwise_inverse: the
+        # product fused into the inverse's first group on resident u32 plans)
+        wd = 4 if spec.dtype == torch.uint32 else 8
+        dp = _alg._device_plan(params, n, variant, INVERSE, None, None, wd, spec.device.index)
+        sa, sb = spec[0].contiguous(), spec[1].contiguous()
+        out = torch.empty_like(sa)
+        rows = sa.numel() // n
+        dp.pointwise_inverse(sa.data_ptr(), sb.data_ptr(), out.data_ptr(), rows,
+                             torch.cuda.current_stream(spec.device).cuda_stream)
+        return out
     if torch is None or not torch.cuda.is_available():
         # host inputs: the device does the work (no CPU fallback)
         raise_if_no_device()

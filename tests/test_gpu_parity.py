@@ -390,6 +390,25 @@ def test_cyclic_mul_ntt_vs_schoolbook(variant):
         assert C[r].tolist() == P.schoolbook_cyclic(A[r].tolist(), B[r].tolist(), 998244353)
 
 
+@pytest.mark.parametrize("variant", ["dit", "dif", "pease", "pease_nc", "stockham", "flat"])
+def test_pointwise_inverse_fused(variant):
+    """ntt_exec_pointwise_inverse: intt(a .* b) in one call -- fused (Montgomery
+    product in the inverse's first group) for resident u32 sizes 2^9..2^13, the
+    pointwise kernel + intt otherwise (2^6, 2^14, 2^16, Flat) -- against the oracle."""
+    p, g = 998244353, 3
+    params = P.FieldParams(p, g)
+    for L, B in ((6, 5), (9, 7), (10, 9), (11, 3), (12, 9), (13, 5), (14, 3), (16, 2)):
+        fa = O.ntt(rand(p, B, L, np.uint32, 7000 + L), p, g, 32, variant)
+        fb = O.ntt(rand(p, B, L, np.uint32, 8000 + L), p, g, 32, variant)
+        prod = ((fa.astype(np.uint64) * fb.astype(np.uint64)) % p).astype(np.uint32)
+        want = O.ntt(prod, p, g, 32, variant, inverse=True, scale=True)
+        dp = P.algorithms._device_plan(params, 1 << L, variant, P.INVERSE, None, None, 4, 0)
+        da, db = to_dev(fa), to_dev(fb)
+        out = torch.empty_like(da)
+        dp.pointwise_inverse(da.data_ptr(), db.data_ptr(), out.data_ptr(), B, torch.cuda.current_stream().cuda_stream)
+        assert np.array_equal(to_host(out), want), (variant, L)
+
+
 def test_estimator_batched_device_path():
     from sklearn.pipeline import Pipeline
     from paper_2405_11353_b200.estimator import NttTransform
