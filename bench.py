@@ -137,7 +137,7 @@ def run_reference(args, rank: int, world: int) -> None:
     sample = ""
     cores = 1
     for _ in range(args.steps):
-        r, cores, sample = cpu_oracle_rate(w, args.variant, 1.0)
+        r, cores, sample = cpu_oracle_rate(w, args.variant, 0.5)
         rates.append(r)
     val = float(np.median(rates))
     line = {
