@@ -81,6 +81,7 @@ struct TileArgs {
     const T* cor_hi;
     int cor_lb;
     int cor_on;                // TL_COLS: multiply by w_N^(i * k2) in the scatter (six-step correction)
+    int cor_lgn;               // TL_COLS correction: log2 N when the tile's columns are a slab (0: L + l1)
     unsigned long long* counters;
 };
 
@@ -652,7 +653,9 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
             if (LAY == TL_COLS && a.cor_on) {   // w_N^(i * k2), k2 = the column output index (natural order)
                 const uint32_t Qj = Qs[t];
                 const uint64_t k2 = (Qj & ((1u << a.S0) - 1)) | ((uint64_t)x << a.S0) | ((uint64_t)(Qj >> a.S0) << (a.S0 + K));
-                const uint64_t e = ((uint64_t)Is[t] * k2) & ((1ull << (L + a.l1)) - 1);
+                // global column i = qoff + local column (distributed slabs); exponent mod N
+                const int lgn = a.cor_lgn ? a.cor_lgn : L + a.l1;
+                const uint64_t e = ((uint64_t)(Is[t] + a.qoff) * k2) & ((1ull << lgn) - 1);
                 const T w = ar.mulfull(__ldg(a.cor_hi + (e >> a.cor_lb)), __ldg(a.cor_lo + (e & ((1ull << a.cor_lb) - 1))));
                 r = ar.mulfull(r, w);
             }

@@ -649,6 +649,13 @@ int ntt_sixstep_dist_step(ntt_plan_t plan, int step, int rank, int world, const 
     r.cor_lo = plan->cor_lo; r.cor_hi = plan->cor_hi; r.cor_lb = plan->cor_lb;
     r.counters = dev_counters(plan->device);
     r.stream = static_cast<cudaStream_t>(stream); r.num_sms = plan->num_sms; r.launches = &launches;
+    {   // per-stream workspace of the long-run passes (2 x n/G residues)
+        std::lock_guard<std::mutex> lk(plan->mu);
+        auto& slot = plan->ws[r.stream];
+        int st = grow(slot.first, slot.second, sixstep_dist_ws_bytes(plan->n, world, plan->word));
+        if (st) { if (cur != plan->device) cudaSetDevice(cur); return st; }
+        r.ws = slot.first;
+    }
     bool ok = false;
     cudaError_t e = tile_sixstep_dist_gold(r, step, rank, world, d_in, d_out, &ok);
     g_launches += launches;

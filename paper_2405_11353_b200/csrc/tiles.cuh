@@ -405,6 +405,91 @@ cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
     return cudaSuccess;
 }
 
+// Distributed four-step with the long-run column passes (rank g of G):
+//   step A: the slab x_local[j][i_local] (n2 x c, c = n1/G): DIT over j of every
+//           local column (TL_COLS passes, inner i_local), correction
+//           w_N^((g c + i_local) k2) fused into the last pass, then the pack for
+//           the all-to-all as a per-destination transpose: [k2][i_local] ->
+//           [h][i_local][k2 mod n2/G] (k_transpose with batch = G);
+//   step B: [i][k2_local] (n1 x n2/G, the all-to-all's concatenation) -> DIT
+//           over i for every local column k2 (TL_COLS, inner k2_local) ->
+//           out_local[k1][k2_local].
+// ws: 2 x n/G residues.
+template <class A>
+cudaError_t run_sixstep_cols_dist(const MultipassReq& r, int step, int rank, int world, const void* in, void* out,
+                                  void* wsv, bool* ok) {
+    using T = typename A::T;
+    *ok = false;
+    int K1 = 0, K2 = 0, lg = 0;
+    while ((1ull << K1) < r.n1) ++K1;
+    while ((1ull << K2) < r.n2) ++K2;
+    while ((1 << lg) < world) ++lg;
+    int KA[2], KB[2];
+    const int PA = cols_split(K2, KA), PB = cols_split(K1, KB);
+    const int lc = K1 - lg, lk = K2 - lg;             // local columns (step A), local k2 (step B)
+    if (!PA || !PB || lc < 6 || lk < 6 || !wsv) return cudaSuccess;   // TL_COLS tiles span up to 64 columns
+    *ok = true;
+    const uint64_t nloc = 1ull << (K1 + K2 - lg);
+    T* ws0 = static_cast<T*>(wsv);
+    T* ws1 = ws0 + nloc;
+    const bool al = aligned16(in) && aligned16(out) && aligned16(wsv);
+    cudaError_t e = cudaSuccess;
+    if (step == 0) {
+        const T* cur = static_cast<const T*>(in);
+        int done = 0;
+        for (int p = 0; p < PA; ++p) {
+            TileArgs<A> a = tile_base<A>(r);
+            a.batch = 1;
+            a.L = K2; a.l1 = lc; a.S0 = done;
+            a.qmode = TQM_LINEAR; a.in_order = a.out_order = TO_T_FAST;
+            a.vec_in = a.vec_out = al;
+            a.rev_in = (p == 0);
+            a.gstw = static_cast<const typename A::Tw*>(r.stw2);
+            a.smb = K2 < kSmb ? K2 : kSmb;
+            a.cor_on = (p == PA - 1);
+            a.cor_lo = static_cast<const T*>(r.cor_lo);
+            a.cor_hi = static_cast<const T*>(r.cor_hi);
+            a.cor_lb = r.cor_lb;
+            a.cor_lgn = K1 + K2;
+            a.qoff = (uint32_t)rank << lc;
+            a.in = cur;
+            a.out = (p == PA - 1) ? ws1 : ws0;
+            if ((e = cols_pass_any<A>(KA[p], a, r)) != cudaSuccess) return e;
+            cur = a.out;
+            done += KA[p];
+        }
+        // pack: per destination h, [k2_local][i_local] -> [i_local][k2_local]
+        const uint64_t blocks = (uint64_t)world << (lk + lc - 10);
+        const uint64_t cap = (uint64_t)r.num_sms * 8;
+        e = fastk::launch_pdl(k_transpose<T>, dim3((unsigned)(blocks < cap ? blocks : cap)), dim3(256), 0, r.stream,
+                              static_cast<const T*>(ws1), static_cast<T*>(out), (uint64_t)world, lk, lc);
+        if (r.launches) ++*r.launches;
+        if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return e;
+        return cudaSuccess;
+    }
+    const T* cur = static_cast<const T*>(in);
+    int done = 0;
+    for (int p = 0; p < PB; ++p) {
+        const bool last = (p == PB - 1);
+        TileArgs<A> a = tile_base<A>(r);
+        a.batch = 1;
+        a.L = K1; a.l1 = lk; a.S0 = done;
+        a.qmode = TQM_LINEAR; a.in_order = a.out_order = TO_T_FAST;
+        a.vec_in = a.vec_out = al;
+        a.rev_in = (p == 0);
+        a.gstw = static_cast<const typename A::Tw*>(r.stw1);
+        a.smb = K1 < kSmb ? K1 : kSmb;
+        a.count_row = last;
+        a.scale = last ? r.scale : 0;
+        a.in = cur;
+        a.out = last ? static_cast<T*>(out) : ws0;
+        if ((e = cols_pass_any<A>(KB[p], a, r)) != cudaSuccess) return e;
+        cur = a.out;
+        done += KB[p];
+    }
+    return cudaSuccess;
+}
+
 }  // namespace ftile
 
 // entry points compiled in kt_f32.cu / kt_gold.cu
@@ -414,5 +499,7 @@ cudaError_t tile_sixstep_gold(const MultipassReq& r, bool* ok);
 // distributed four-step, rank-local steps (step = 0: A, 1: B)
 cudaError_t tile_sixstep_dist_gold(const MultipassReq& r, int step, int rank, int world, const void* in, void* out,
                                    bool* ok);
+// workspace (bytes) the distributed steps need on one rank
+uint64_t sixstep_dist_ws_bytes(uint64_t n, int world, int word);
 
 }  // namespace nttb200
