@@ -148,7 +148,8 @@ struct FGoldC {
         return c2 ? mk(q0, q1) : mk(s0, s1);
     }
     // 128-bit product by a mad.wide chain (each partial sum fits 64 bits:
-    // (2^32-1)^2 + 2(2^32-1) = 2^64-1), then the same reduction as mul_c
+    // (2^32-1)^2 + 2(2^32-1) = 2^64-1), r2 * EPS as one IMAD.WIDE (FMA pipe: the
+    // Goldilocks kernels are ALU-bound), then the reduction 2^64 = EPS, 2^96 = -1
     NTT_D static T mul_m(T a, T b) {
         const uint32_t a0 = lo(a), a1 = hi(a), b0 = lo(b), b1 = hi(b);
         const uint64_t p00 = (uint64_t)a0 * b0;
@@ -156,27 +157,26 @@ struct FGoldC {
         const uint64_t u = (uint64_t)a1 * b0 + (uint32_t)t;
         const uint64_t v = (uint64_t)a1 * b1 + (t >> 32) + (u >> 32);
         const uint32_t r0 = lo(p00), r1 = lo(u), r2 = lo(v), r3 = hi(v);
-        // x = r1:r0 - r3 + r2 * (2^32 - 1)  (2^64 = EPS, 2^96 = -1)
-        uint32_t t0, t1, m, u0, u1, c, s0, s1, q0, q1, c2;
-        asm("sub.cc.u32 %0, %13, %16;\n\t"         // t = lo64 - r3
-            "subc.cc.u32 %1, %14, 0;\n\t"
+        const uint64_t ue = (uint64_t)r2 * 0xFFFFFFFFu;          // r2 * EPS
+        // x = r1:r0 - r3 + r2 * EPS
+        uint32_t t0, t1, m, c, s0, s1, q0, q1, c2;
+        asm("sub.cc.u32 %0, %9, %11;\n\t"          // t = lo64 - r3
+            "subc.cc.u32 %1, %10, 0;\n\t"
             "subc.u32 %2, 0, 0;\n\t"                // m = borrow ? EPS : 0
             "sub.cc.u32 %0, %0, %2;\n\t"            // t -= EPS on borrow (no underflow)
             "subc.u32 %1, %1, 0;\n\t"
-            "sub.cc.u32 %3, 0, %15;\n\t"            // u = r2 * EPS = (r2 << 32) - r2
-            "subc.u32 %4, %15, 0;\n\t"
-            "add.cc.u32 %0, %0, %3;\n\t"            // t += u, carry c
-            "addc.cc.u32 %1, %1, %4;\n\t"
-            "addc.u32 %5, 0, 0;\n\t"
-            "neg.s32 %5, %5;\n\t"                   // carry: + EPS (cannot overflow again)
-            "add.cc.u32 %6, %0, %5;\n\t"
-            "addc.u32 %7, %1, 0;\n\t"
-            "add.cc.u32 %8, %6, 0xffffffff;\n\t"     // canonical: s >= p <=> s + EPS overflows
-            "addc.cc.u32 %9, %7, 0;\n\t"
-            "addc.u32 %10, 0, 0;"
-            : "=&r"(t0), "=&r"(t1), "=&r"(m), "=&r"(u0), "=&r"(u1), "=&r"(c), "=&r"(s0), "=&r"(s1), "=&r"(q0),
-              "=&r"(q1), "=&r"(c2)
-            : "r"(0u), "r"(0u), "r"(r0), "r"(r1), "r"(r2), "r"(r3));
+            "add.cc.u32 %0, %0, %12;\n\t"           // t += r2 * EPS, carry c
+            "addc.cc.u32 %1, %1, %13;\n\t"
+            "addc.u32 %3, 0, 0;\n\t"
+            "neg.s32 %3, %3;\n\t"                   // carry: + EPS (cannot overflow again)
+            "add.cc.u32 %4, %0, %3;\n\t"
+            "addc.u32 %5, %1, 0;\n\t"
+            "add.cc.u32 %6, %4, 0xffffffff;\n\t"     // canonical: s >= p <=> s + EPS overflows
+            "addc.cc.u32 %7, %5, 0;\n\t"
+            "addc.u32 %8, 0, 0;"
+            : "=&r"(t0), "=&r"(t1), "=&r"(m), "=&r"(c), "=&r"(s0), "=&r"(s1), "=&r"(q0), "=&r"(q1), "=&r"(c2)
+            : "r"(r0), "r"(r1), "r"(r3), "r"(lo(ue)), "r"(hi(ue)));
+        (void)m;
         return c2 ? mk(q0, q1) : mk(s0, s1);
     }
     NTT_D T add(T a, T b) const { return add_c(a, b); }

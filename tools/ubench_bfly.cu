@@ -143,12 +143,92 @@ struct FGoldOld : FGoldC {
     NTT_D T mul(T x, Tw w) const { return mul_c(x, w); }
 };
 
+// mul_m with u = r2 * EPS on the FMA pipe (IMAD.WIDE) instead of two ALU subtractions
+struct FGoldW : FGoldC {
+    NTT_D static T mul_w(T a, T b) {
+        const uint32_t a0 = lo(a), a1 = hi(a), b0 = lo(b), b1 = hi(b);
+        const uint64_t p00 = (uint64_t)a0 * b0;
+        const uint64_t t = (uint64_t)a0 * b1 + (p00 >> 32);
+        const uint64_t u = (uint64_t)a1 * b0 + (uint32_t)t;
+        const uint64_t v = (uint64_t)a1 * b1 + (t >> 32) + (u >> 32);
+        const uint32_t r0 = lo(p00), r1 = lo(u), r2 = lo(v), r3 = hi(v);
+        const uint64_t ue = (uint64_t)r2 * 0xFFFFFFFFu;          // r2 * EPS (IMAD.WIDE)
+        uint32_t t0, t1, m, c, s0, s1, q0, q1, c2;
+        asm("sub.cc.u32 %0, %9, %11;\n\t"
+            "subc.cc.u32 %1, %10, 0;\n\t"
+            "subc.u32 %2, 0, 0;\n\t"
+            "sub.cc.u32 %0, %0, %2;\n\t"
+            "subc.u32 %1, %1, 0;\n\t"
+            "add.cc.u32 %0, %0, %12;\n\t"
+            "addc.cc.u32 %1, %1, %13;\n\t"
+            "addc.u32 %3, 0, 0;\n\t"
+            "neg.s32 %3, %3;\n\t"
+            "add.cc.u32 %4, %0, %3;\n\t"
+            "addc.u32 %5, %1, 0;\n\t"
+            "add.cc.u32 %6, %4, 0xffffffff;\n\t"
+            "addc.cc.u32 %7, %5, 0;\n\t"
+            "addc.u32 %8, 0, 0;"
+            : "=&r"(t0), "=&r"(t1), "=&r"(m), "=&r"(c), "=&r"(s0), "=&r"(s1), "=&r"(q0), "=&r"(q1), "=&r"(c2)
+            : "r"(r0), "r"(r1), "r"(r3), "r"(lo(ue)), "r"(hi(ue)));
+        (void)m;
+        return c2 ? mk(q0, q1) : mk(s0, s1);
+    }
+    NTT_D T mul(T x, Tw w) const { return mul_w(x, w); }
+};
+
+// all-C formulation: 64-bit arithmetic, carries from compares (compiler-chosen SASS)
+struct FGoldCC : FGoldC {
+    static constexpr uint64_t E = 0xFFFFFFFFull;
+    NTT_D static T addcc(T a, T b) {
+        const uint64_t s = a + b;
+        const bool c1 = s < a;
+        const uint64_t t = s + E;
+        const bool c2 = t < s;
+        return (c1 | c2) ? t : s;
+    }
+    NTT_D static T subcc(T a, T b) {
+        const uint64_t d = a - b;
+        return a < b ? d - E : d;
+    }
+    NTT_D static T mulcc(T a, T b) {
+        const uint32_t a0 = lo(a), a1 = hi(a), b0 = lo(b), b1 = hi(b);
+        const uint64_t p00 = (uint64_t)a0 * b0;
+        const uint64_t t = (uint64_t)a0 * b1 + (p00 >> 32);
+        const uint64_t u = (uint64_t)a1 * b0 + (uint32_t)t;
+        const uint64_t v = (uint64_t)a1 * b1 + (t >> 32) + (u >> 32);
+        const uint64_t lo64 = ((uint64_t)(uint32_t)u << 32) | (uint32_t)p00;
+        const uint64_t r2 = (uint32_t)v, r3 = v >> 32;
+        uint64_t t0 = lo64 - r3;
+        if (lo64 < r3) t0 -= E;
+        const uint64_t t1 = (r2 << 32) - r2;
+        uint64_t sm = t0 + t1;
+        if (sm < t1) sm += E;
+        return sm >= P ? sm - P : sm;
+    }
+    NTT_D T add(T a, T b) const { return addcc(a, b); }
+    NTT_D T sub(T a, T b) const { return subcc(a, b); }
+    NTT_D T mul(T x, Tw w) const { return mulcc(x, w); }
+};
+// PTX carry chains for add/sub, all-C multiply
+struct FGoldMix : FGoldC {
+    NTT_D T mul(T x, Tw w) const { return FGoldCC::mulcc(x, w); }
+};
+// all-C add/sub, PTX multiply
+struct FGoldMix2 : FGoldC {
+    NTT_D T add(T a, T b) const { return FGoldCC::addcc(a, b); }
+    NTT_D T sub(T a, T b) const { return FGoldCC::subcc(a, b); }
+};
+
 __global__ void k_goldcheck(const uint64_t* a, const uint64_t* b, int n, int* bad) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     uint64_t x = a[i], y = b[i];
     if (FGoldC::mul_c(x, y) != FGold::reduce128(x * y, __umul64hi(x, y))) atomicAdd(bad, 1);
     if (FGoldC::mul_m(x, y) != FGold::reduce128(x * y, __umul64hi(x, y))) atomicAdd(bad, 1);
+    if (FGoldCC::mulcc(x, y) != FGold::reduce128(x * y, __umul64hi(x, y))) atomicAdd(bad, 1);
+    if (FGoldW::mul_w(x, y) != FGold::reduce128(x * y, __umul64hi(x, y))) atomicAdd(bad, 1);
+    { uint64_t s_ = x + y; if (s_ < x) s_ += FGold::EPS; if (FGoldCC::addcc(x, y) != FGold::canon(s_)) atomicAdd(bad + 1, 1); }
+    if (FGoldCC::subcc(x, y) != (x < y ? x - y - FGold::EPS : x - y)) atomicAdd(bad + 2, 1);
     { uint64_t s_ = x + y; if (s_ < x) s_ += FGold::EPS; if (FGoldC::add_c(x, y) != FGold::canon(s_)) atomicAdd(bad + 1, 1); }
     if (FGoldC::sub_c(x, y) != (x < y ? x - y - FGold::EPS : x - y)) atomicAdd(bad + 2, 1);
 }
@@ -192,6 +272,8 @@ int main() {
     run<Canon<FGoldC>>("gold-carry", G, 7ull, 49ull, 512);
     run<Canon<FGoldOld>>("gold-mulc", G, 7ull, 49ull, 256);
     run<Canon<FGoldOld>>("gold-mulc", G, 7ull, 49ull, 512);
+    run<Canon<FGoldW>>("gold-wideE", G, 7ull, 49ull, 256);
+    run<Canon<FGoldW>>("gold-wideE", G, 7ull, 49ull, 512);
     // exactness check of FGoldC vs FGold on random operands
     check_gold();
     return 0;
