@@ -190,6 +190,29 @@ def test_fourstep_goldilocks_2_16(variant):
                           O.ntt(x, p, g, 64, variant, inverse=True, scale=True))
 
 
+@pytest.mark.parametrize("L", [14, 17, 20])
+def test_fourstep_in_place_and_misaligned(L):
+    """Four-step edge cases: in-place execution (d_in == d_out), and an input
+    only 4-byte aligned (the TMA passes decline it; the cp.async passes run)."""
+    p, g = 998244353, 3
+    plan = P.make_plan(P.FieldParams(p, g), "pease_nc", 1 << L)
+    dp = P.algorithms.device_plan_for(plan, 4, 0)
+    B = 2
+    x = rand(p, B, L, np.uint32, 6000 + L)
+    want = O.ntt(x, p, g, 32, "pease_nc")
+    s = torch.cuda.current_stream().cuda_stream
+    d = to_dev(x)
+    dp.exec_device(d.data_ptr(), d.data_ptr(), B, False, s)
+    assert np.array_equal(to_host(d), want), ("in-place", L)
+    big = torch.zeros(B * (1 << L) + 1, dtype=torch.int32, device="cuda")
+    big[1:] = torch.from_numpy(x.view(np.int32).reshape(-1)).cuda()
+    out = torch.zeros_like(big)
+    dp.exec_device(big.data_ptr() + 4, out.data_ptr() + 4, B, False, s)
+    torch.cuda.synchronize()
+    got = out[1:].cpu().numpy().view(np.uint32).reshape(B, -1)
+    assert np.array_equal(got, want), ("misaligned", L)
+
+
 def test_concurrent_streams_share_a_plan():
     """A multi-pass plan (workspace-backed four-step) executed concurrently on
     two streams: each stream has its own workspace, both results exact."""
