@@ -32,17 +32,8 @@
 #include "fasttile.cuh"
 
 // experiment knobs (defaults = measured best)
-#ifndef NTT_FS_CIN_LATE
-#define NTT_FS_CIN_LATE 0       // issue the next tile's copy-in after the first group instead of before it
-#endif
 #ifndef NTT_FS_DIAG
 #define NTT_FS_DIAG 0           // diagnostics only: 1 = skip the butterflies (data movement alone), 3 = also skip the stores, 4 = skip butterflies + copy-in
-#endif
-#ifndef NTT_FS_L2PF
-#define NTT_FS_L2PF 0           // prefetch the input this many polynomials ahead into L2 (0 = off)
-#endif
-#ifndef NTT_FS_L2PF_ALL
-#define NTT_FS_L2PF_ALL 0       // also in pass B (contiguous tiles)
 #endif
 #ifndef NTT_FS_TWIST_TAB
 #define NTT_FS_TWIST_TAB 1      // pass A twist from the precomputed [k1][n2] table (1) or factored (0):
@@ -188,18 +179,6 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
         }
     };
 
-    // L2 prefetch of the input NTT_FS_L2PF polynomials ahead: tile g of
-    // polynomial b pulls the contiguous 1/(tiles per polynomial) slice g of
-    // polynomial b + NTT_FS_L2PF, so the strided gathers of pass A find their
-    // 32-byte runs in L2 (DRAM sees whole contiguous slices)
-    auto l2_prefetch = [&](uint64_t tl) {
-        if (NTT_FS_L2PF == 0 || tid != 0) return;
-        const uint64_t b = (tl >> tpp_log) + NTT_FS_L2PF;
-        if (b >= a.batch) return;
-        const uint64_t slice = N >> tpp_log;                     // elements per slice
-        const T* src = a.in + b * N + (tl & ((1ull << tpp_log) - 1)) * slice;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((uint32_t)(slice * sizeof(T))) : "memory");
-    };
     __syncthreads();                         // twiddle table in place (before the PDL wait)
     fastk::pdl_trigger();
     fastk::pdl_wait();
@@ -215,9 +194,8 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
             const uint64_t nxt = tile + gridDim.x;
             if (nxt < ntiles) copy_in(nxt, Y);
             cp_async_commit();
-            if (NTT_FS_L2PF_ALL || MODE == 0) l2_prefetch(tile);
         };
-        if (!NTT_FS_CIN_LATE) prefetch_next();
+        prefetch_next();          // the next tile's copy-in overlaps this tile's groups
         // factored pass-A twist: the tile's [c][t] table and this thread's w^(n2 u)
         Tw twA;
         if (MODE == 0 && !NTT_FS_TWIST_TAB) {
@@ -232,7 +210,6 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
 #pragma unroll
         for (int g = 0; g < G - 1; ++g) {
             if (NTT_FS_DIAG >= 1) break;
-            if (NTT_FS_CIN_LATE && g == 1) prefetch_next();   // after the first group's loads
             T v[16];
             const uint32_t t = tid >> (K - 4), u = tid & (TT - 1);
             T* sb = X + t * NP;
@@ -280,7 +257,6 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
             }
             __syncthreads();
         }
-        if (NTT_FS_CIN_LATE && G == 2) prefetch_next();
         // ---- last group: tile-major thread map, stores straight to HBM
         {
             T v[16];
