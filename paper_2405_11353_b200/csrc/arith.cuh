@@ -74,6 +74,8 @@ struct F32W {
 //        (a,b < p: s >= p  <=>  s + EPS overflows)
 //   sub: d = a-b; result = borrow ? d - EPS : d
 //   mul: 128-bit product from 4 mul.wide.u32, reduction 2^64 = EPS, 2^96 = -1.
+// the carry-chain asm blocks below produce temporaries the compiler sees as "set but never used"
+#pragma nv_diag_suppress 550
 struct FGoldC {
     using T = uint64_t;
     using Tw = uint64_t;
@@ -104,6 +106,7 @@ struct FGoldC {
             "subc.u32 %1, %1, 0;"
             : "=r"(d0), "=r"(d1), "=r"(m)
             : "r"(lo(a)), "r"(hi(a)), "r"(lo(b)), "r"(hi(b)));
+        (void)m;
         return mk(d0, d1);
     }
     NTT_D static T mul_c(T a, T b) {
@@ -185,6 +188,7 @@ struct FGoldC {
     NTT_D T mul_full(T a, T b) const { return NTT_GOLD_MULM ? mul_m(a, b) : mul_c(a, b); }
     NTT_D static T tw_value(Tw w) { return w; }
 };
+#pragma nv_diag_default 550
 
 
 // Goldilocks p = 2^64 - 2^32 + 1.  Reduction of a 128-bit product uses

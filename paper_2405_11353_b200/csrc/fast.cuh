@@ -222,7 +222,8 @@ NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[RN], uint32_t pbase, cons
 template <class A, int L, int sg, int kg, int RB, int RN>
 NTT_D void pease_regs(const A& ar, typename A::T (&v)[RN], uint32_t ubase, const typename A::Tw* stw) {
     using T = typename A::T;
-    constexpr int NB = (kg <= RB && sg + kg <= L) ? RN >> kg : 0;
+    if constexpr (kg <= RB && sg + kg <= L) {        // (only valid windows emit code)
+    constexpr int NB = RN >> kg;
     constexpr int H = 1 << (kg - 1);
 #pragma unroll
     for (int n = 0; n < NB; ++n) {
@@ -249,6 +250,7 @@ NTT_D void pease_regs(const A& ar, typename A::T (&v)[RN], uint32_t ubase, const
             for (int c = 0; c < (1 << kg); ++c) v[n * (1 << kg) + c] = nv[c];
         }
     }
+    }
 }
 
 // ------------------------------------------------------------ Stockham ----
@@ -260,7 +262,8 @@ NTT_D void pease_regs(const A& ar, typename A::T (&v)[RN], uint32_t ubase, const
 template <class A, int L, int sg, int kg, int RB, int RN>
 NTT_D void stockham_regs(const A& ar, typename A::T (&v)[RN], uint32_t hi, const typename A::Tw* stw) {
     using T = typename A::T;
-    constexpr int NB = (kg <= RB && sg + kg <= L) ? RN >> kg : 0;
+    if constexpr (kg <= RB && sg + kg <= L) {        // (only valid windows emit code)
+    constexpr int NB = RN >> kg;
     constexpr int H = 1 << (kg - 1);
 #pragma unroll
     for (int x = 0; x < NB; ++x) {
@@ -284,6 +287,7 @@ NTT_D void stockham_regs(const A& ar, typename A::T (&v)[RN], uint32_t hi, const
             for (int c = 0; c < (1 << kg); ++c) v[(c << (RB - kg)) | x] = nv[c];
         }
     }
+    }
 }
 
 // -------------------------------------------------------------- kernel ----
@@ -297,7 +301,6 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     constexpr int N = GG::N, TT = GG::TT, G = GG::G, K0 = GG::K0, RV = GG::R;
     static_assert(RB == 4 || G <= 2, "wide register blocks: first/last groups only");
     constexpr int CW = lane_bits<T>();
-    constexpr bool PP = (V == V_PEASE || V == V_PEASE_NC || V == V_STOCKHAM);   // permuting groups
     // Pease keeps two work buffers + the copy-back (algorithms.py:242); Pease_nc
     // and Stockham swap "buffers" through the registers: every thread holds its
     // whole sub-network, so after a team barrier the group writes the same
@@ -612,8 +615,12 @@ cudaError_t launch_fast_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int
         auto kern = a.scale ? k_fast<A, V, L, C::TEAMS, true, C::RB, C::DS> : k_fast<A, V, L, C::TEAMS, false, C::RB, C::DS>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
         if (e != cudaSuccess) return e;
+        int occ = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::TEAMS * C::TT, C::smem) != cudaSuccess || occ < 1)
+            occ = 1;
         uint64_t ctas = (a.batch + C::TEAMS - 1) / C::TEAMS;
-        uint64_t grid = ctas < (uint64_t)num_sms ? ctas : (uint64_t)num_sms;
+        const uint64_t cap = (uint64_t)num_sms * occ;
+        uint64_t grid = ctas < cap ? ctas : cap;
         *ok = true;
         if (grid == 0) return cudaSuccess;
         cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(C::TEAMS * C::TT), C::smem, s, a);
