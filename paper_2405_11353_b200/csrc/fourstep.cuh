@@ -101,7 +101,7 @@ constexpr size_t fs_smem_bytes() {
 //   Pease (reads u << 4 | c): in-warp bits -> u bits 1..AB (positions 5..)
 template <int V, int K, int AB>
 NTT_D uint32_t last_u(uint32_t up) {
-    if (V == V_DIT || V == V_DIF || AB == 0) return up;
+    if (V == V_DIT || AB == 0) return up;      // DIF / Pease read u << 4 | c: in-warp bits -> u bits 1..AB
     constexpr uint32_t m = (1u << AB) - 1;
     return ((up & m) << 1) | ((up >> AB) & 1u) | ((up >> (AB + 1)) << (AB + 1));
 }
@@ -144,7 +144,9 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
     if (MODE == 0) {
         const uint32_t q = tid & (TQ - 1), rest = tid >> LQ;
         const uint32_t rlo = rest & ((1u << AB) - 1), rhi = rest >> AB;
-        const uint32_t r0 = (rlo << (K - AB)) | (rhi << 4);
+        // bit-reversed placement: the in-warp rest bits on r's top bits (positions 0..AB-1);
+        // natural placement (DIF): on r's low bits; the register index j fills the other end
+        const uint32_t r0 = BRIN ? ((rlo << (K - AB)) | (rhi << 4)) : (rlo | (rhi << AB));
         cin_soff = q * NP + padpos<T>(BRIN ? brev(r0, K) : r0);
         cin_goff = ((uint64_t)r0 << Kc) + q;
     } else {
@@ -166,8 +168,9 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
             uint32_t so;
             uint64_t go;
             if (MODE == 0) {
-                so = padpos<T>(BRIN ? brev((uint32_t)j, K) : (uint32_t)j);   // r bits 0..3 (bit-reversed: positions K-4..K-1)
-                go = (uint64_t)j << Kc;
+                // j = r bits 0..3 (bit-reversed: positions K-4..K-1) / r bits K-4..K-1 (natural)
+                so = padpos<T>(BRIN ? brev((uint32_t)j, K) : ((uint32_t)j << (K - 4)));
+                go = (uint64_t)(BRIN ? (uint32_t)j : ((uint32_t)j << (K - 4))) << Kc;
             } else {
                 // e = tid + j*NT: x = e mod 2^K, q = e >> K (NT = TQ*2^(K-4))
                 constexpr uint32_t NTc = NT;
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
                 const T* wb = sb + padpos<T>(u << 4);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) v[c] = wb[padpos<T>((uint32_t)c)];
-                if (NTT_FS_DIAG == 0) ftile::t_bitwin<A, K, 0, 0, 4, true, false>(ar, v, u << 4, 0u, 0, tws);
+                if (NTT_FS_DIAG == 0) ftile::t_bitwin<A, K, 0, 0, K0, true, false>(ar, v, u << 4, 0u, 0, tws);   // stages K0..1
             } else if (V == V_DIT) {
                 const T* wb = sb + padpos<T>(u);
 #pragma unroll

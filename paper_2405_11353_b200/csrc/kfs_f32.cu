@@ -75,6 +75,8 @@ static cudaError_t fs_pass_tma_k(const MultipassReq& r, const CUtensorMap& map) 
 template <int V, int MODE>
 static bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err) {
     *err = cudaSuccess;
+    if constexpr (V == V_DIF) return false;      // the TMA passes carry DIT / Pease_nc geometries
+    else {
     const void* src = MODE == 0 ? r.in : r.ws;
     const int K = MODE == 0 ? Kr : Kc;
     if (!fs_tma_enabled() || (reinterpret_cast<uintptr_t>(src) & 15)) return false;
@@ -108,6 +110,7 @@ static bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err)
     }
 #undef NTT_FSTK
     return false;
+    }
 }
 
 template <int V>
@@ -146,7 +149,9 @@ cudaError_t fourstep_f32(const MultipassReq& r, bool* ok) {
         return cudaSuccess;
     const int Kr = fourstep_kr(r.L), Kc = r.L - Kr;
     *ok = true;
-    if (r.variant == V_DIT) return fs_run<V_DIT>(r, Kr, Kc);
+    // Flat's per-stage states are DIT's (algorithms.py:161-195): DIT sub-transforms
+    if (r.variant == V_DIT || r.variant == V_FLAT) return fs_run<V_DIT>(r, Kr, Kc);
+    if (r.variant == V_DIF) return fs_run<V_DIF>(r, Kr, Kc);
     return fs_run<V_PEASE_NC>(r, Kr, Kc);
 }
 
