@@ -136,6 +136,13 @@ cudaError_t run_variant(const MultipassReq& r) {
         cudaError_t fe = std::is_same<F, F32S>::value ? fourstep_f32(r, &ok) : fourstep_gold(r, &ok);
         if (fe != cudaSuccess || ok) return fe;
     }
+    if constexpr (std::is_same<F, F32S>::value) {
+        if (tile_2p14_applies(L, V, r.p, 4) && r.ws) {
+            bool ok = false;
+            cudaError_t te = tile_passes_f32(V, r.p < (1ull << 30), r, &ok);
+            if (te != cudaSuccess || ok) return te;
+        }
+    }
     if (L <= single_pass_max_log2(sizeof(T))) {
         bool ok = false;
         cudaError_t fe = try_fast<F, V>(r, &ok);

@@ -312,6 +312,12 @@ inline bool fourstep_applies(int L, int variant, uint64_t p, int word) {
            (variant == V_DIT || variant == V_DIF || variant == V_PEASE_NC);
 }
 inline int fourstep_kr(int L) { return (L + 1) / 2; }
+// u32 (p < 2^31) 2^14 outside the four-step (Pease, Stockham): the compile-time tile
+// passes (2 x 2^7) instead of the generic shared-memory engine
+inline bool tile_2p14_applies(int L, int variant, uint64_t p, int word) {
+    return word == 4 && p < (1ull << 31) && L == 14 && !fourstep_applies(L, variant, p, word) &&
+           variant != V_NAIVE && variant != V_SIXSTEP;
+}
 cudaError_t fourstep_twist_build(const void* tw, void* out, int L, int word, cudaStream_t s);
 cudaError_t fourstep_gold(const MultipassReq& r, bool* ok);
 cudaError_t mp_launch_f32w(const MultipassReq& r);

@@ -10,6 +10,7 @@ cudaError_t pointwise_f64(uint64_t, const void*, const void*, void*, uint64_t, c
 int mp_num_passes(int L, int word, int variant, uint64_t p) {
     if (variant == V_SIXSTEP) return 2;
     if (fourstep_applies(L, variant, p, word)) return 2;
+    if (tile_2p14_applies(L, variant, p, word)) return variant == V_FLAT ? 3 : 2;
     if (variant == V_NAIVE || L <= single_pass_max_log2(word)) return 1;
     int K[8];
     int P = plan_passes(L, word, variant, K);
@@ -20,6 +21,7 @@ uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch, uint64
     const uint64_t row = (1ull << L) * (uint64_t)word;
     if (variant == V_SIXSTEP) return 2 * batch * row;      // column / row passes ping-pong (tiles.cuh)
     if (fourstep_applies(L, variant, p, word)) return 2 * batch * row;   // (NTT_FOURSTEP=0 falls back to tile passes)
+    if (tile_2p14_applies(L, variant, p, word)) return 2 * batch * row;
     if (variant == V_NAIVE || L <= single_pass_max_log2(word)) return 0;
     return 2 * batch * row;
 }
