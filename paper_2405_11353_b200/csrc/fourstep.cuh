@@ -101,7 +101,7 @@ constexpr size_t fs_smem_bytes() {
 //   Pease (reads u << 4 | c): in-warp bits -> u bits 1..AB (positions 5..)
 template <int V, int K, int AB>
 NTT_D uint32_t last_u(uint32_t up) {
-    if (V == V_DIT || AB == 0) return up;      // DIF / Pease read u << 4 | c: in-warp bits -> u bits 1..AB
+    if (V == V_DIT || AB == 0) return up;      // DIF / Pease / Stockham read u << 4 | c: in-warp bits -> u bits 1..AB
     constexpr uint32_t m = (1u << AB) - 1;
     return ((up & m) << 1) | ((up >> AB) & 1u) | ((up >> (AB + 1)) << (AB + 1));
 }
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
     constexpr int EPT = 16;                             // residues per thread per tile
     // DIT / Pease gather their input bit-reversed (algorithms.py:119,238,255); DIF
     // reads it in natural order and bit-reverses its output (algorithms.py:158)
-    constexpr bool BRIN = (V != V_DIF);
+    constexpr bool BRIN = (V != V_DIF && V != V_STOCKHAM);   // Stockham never bit-reverses
     constexpr bool TWE = NTT_FS_TW_EARLY && sizeof(T) == 4;
     static_assert(NT * EPT == (TQ << K), "one 16-residue sub-network per thread");
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -239,6 +239,28 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
 #undef NTT_FSBW
 #pragma unroll
                 for (int c = 0; c < 16; ++c) wb[padpos<T>((uint32_t)c << B)] = v[c];
+            } else if (V == V_STOCKHAM) {   // self-sorting: window [lob, lob+kg), one buffer
+                const int sg = g == 0 ? 0 : K0 + 4 * (g - 1);
+                const int kg = g == 0 ? K0 : 4;
+                const int lob = K - sg - kg;
+                uint32_t hi, lo;
+                if (g == 0) { hi = 0; lo = u; }
+                else { lo = u & ((1u << lob) - 1); hi = u >> lob; }
+                const T* rb = sb + padpos<T>((hi << (K - sg)) | lo);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) v[c] = rb[padpos<T>((uint32_t)c << (lob - (4 - kg)))];
+#define NTT_FSST(SG, KGV) \
+    if (sg == SG && kg == KGV) ftile::t_stockham<A, K, SG, KGV, false>(ar, v, hi, 0u, 0, tws);
+                if (g == 0) { NTT_FSST(0, 1) NTT_FSST(0, 2) NTT_FSST(0, 3) NTT_FSST(0, 4) }
+                else { NTT_FSST(1, 4) NTT_FSST(2, 4) NTT_FSST(3, 4) NTT_FSST(4, 4) NTT_FSST(5, 4) }
+#undef NTT_FSST
+                __syncthreads();             // every read of the (single) work buffer done
+                T* wbo = sb + padpos<T>((hi << lob) | lo);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const uint32_t Rb = (uint32_t)c >> (4 - kg), xx = (uint32_t)c & ((1u << (4 - kg)) - 1);
+                    wbo[padpos<T>((Rb << (K - kg)) | (xx << (lob - (4 - kg))))] = v[c];
+                }
             } else {   // Pease / Pease_nc: constant geometry, one buffer (roles swap through the registers)
                 const int sg = g == 0 ? 0 : K0 + 4 * (g - 1);
                 const int kg = g == 0 ? K0 : 4;
@@ -296,7 +318,11 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
                 const T* rb = sb + padpos<T>(u << 4);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) v[c] = rb[padpos<T>((uint32_t)c)];
-                if (NTT_FS_DIAG == 0) ftile::t_pease<A, K, sgL, 4, false>(ar, v, u, 0u, 0, tws);
+                // Stockham's last window (lob = 0) reads the same 16 contiguous positions
+                if (NTT_FS_DIAG == 0) {
+                    if (V == V_STOCKHAM) ftile::t_stockham<A, K, sgL, 4, false>(ar, v, u, 0u, 0, tws);
+                    else ftile::t_pease<A, K, sgL, 4, false>(ar, v, u, 0u, 0, tws);
+                }
             }
             const uint64_t gb = tile_gbase(tile);
             if (NTT_FS_DIAG == 3) {

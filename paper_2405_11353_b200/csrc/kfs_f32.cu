@@ -75,7 +75,7 @@ static cudaError_t fs_pass_tma_k(const MultipassReq& r, const CUtensorMap& map) 
 template <int V, int MODE>
 static bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err) {
     *err = cudaSuccess;
-    if constexpr (V == V_DIF) return false;      // the TMA passes carry DIT / Pease_nc geometries
+    if constexpr (V == V_DIF || V == V_STOCKHAM) return false;      // the TMA passes carry DIT / Pease_nc geometries
     else {
     const void* src = MODE == 0 ? r.in : r.ws;
     const int K = MODE == 0 ? Kr : Kc;
@@ -130,7 +130,7 @@ static cudaError_t fs_run(const MultipassReq& r, int Kr, int Kc) {
     a.in = static_cast<const uint32_t*>(r.in);
     a.out = static_cast<uint32_t*>(r.ws);
     a.scale = 0;
-    a.count_bitrev = 1;          // DIT / Pease_nc sub-transforms bit-reverse their inputs
+    a.count_bitrev = V == V_STOCKHAM ? 0 : 1;   // DIT / DIF / Pease_nc sub-transforms bit-reverse; Stockham never
     cudaError_t e = cudaSuccess;
     if (!fs_pass_tma<V, 0>(r, Kr, Kc, &e)) e = fstep::fs_pass_any<A, V>(Kr + Kc, 0, a, r.stream, r.num_sms, r.launches);
     if (e != cudaSuccess) return e;
@@ -152,6 +152,7 @@ cudaError_t fourstep_f32(const MultipassReq& r, bool* ok) {
     // Flat's per-stage states are DIT's (algorithms.py:161-195): DIT sub-transforms
     if (r.variant == V_DIT || r.variant == V_FLAT) return fs_run<V_DIT>(r, Kr, Kc);
     if (r.variant == V_DIF) return fs_run<V_DIF>(r, Kr, Kc);
+    if (r.variant == V_STOCKHAM) return fs_run<V_STOCKHAM>(r, Kr, Kc);
     return fs_run<V_PEASE_NC>(r, Kr, Kc);
 }
 

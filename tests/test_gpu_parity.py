@@ -163,7 +163,7 @@ def test_list_api_and_bench_checksum(golden):
             assert isinstance(out, list) and out[0] == rec["checksum"] == (467606314 if n == "1024" else out[0])
 
 
-@pytest.mark.parametrize("variant", ["dit", "pease_nc", "dif", "flat"])
+@pytest.mark.parametrize("variant", ["dit", "pease_nc", "dif", "flat", "stockham"])
 @pytest.mark.parametrize("L", [14, 15, 16, 17, 18, 19, 20])
 def test_fourstep_sizes_vs_oracle(variant, L):
     """Two-pass four-step kernels (fourstep.cuh; every R x C split 7..10):
