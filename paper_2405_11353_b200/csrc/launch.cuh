@@ -109,10 +109,13 @@ cudaError_t run_fast_pw(const MultipassReq& r, const void* in2, bool* ok) {
 }
 
 // Specialised single-pass kernels (fast.cuh) where they apply.
-template <class F, int V>
+template <class F, int V0>
 cudaError_t try_fast(const MultipassReq& r, bool* ok) {
+    // Flat's per-stage states are DIT's (algorithms.py:161-195; its separate
+    // bit_reverse_permute is the gather DIT fuses): the DIT kernel serves it
+    constexpr int V = V0 == V_FLAT ? V_DIT : V0;
     *ok = false;
-    if (V == V_FLAT || V == V_NAIVE || V == V_SIXSTEP) return cudaSuccess;
+    if (V == V_NAIVE || V == V_SIXSTEP) return cudaSuccess;
     if (r.L < 9 || r.L > 13 || !r.stw) return cudaSuccess;
     if ((reinterpret_cast<uintptr_t>(r.in) & 15) || (reinterpret_cast<uintptr_t>(r.out) & 15)) return cudaSuccess;
     if constexpr (std::is_same<F, F32S>::value) {
