@@ -1,5 +1,5 @@
-// Four-step two-pass kernels (fourstep.cuh) for Goldilocks 2^16 = 256 x 256
-// (config 3): DIT / DIF / Pease_nc sub-transforms of length 2^8, canonical field.
+// Four-step two-pass kernels (fourstep.cuh) for Goldilocks 2^14..2^18 (config 3:
+// 2^16 = 256 x 256): DIT / Flat / DIF / Pease_nc / Stockham sub-transforms, canonical field.
 #include <cstdlib>
 #include "fourstep.cuh"
 #include "multipass.cuh"
@@ -10,13 +10,14 @@ static bool fourstep_gold_enabled() {
     return on;
 }
 
-template <int V>
-static cudaError_t fsg_run(const MultipassReq& r) {
+template <int V, int L>
+static cudaError_t fsg_run_l(const MultipassReq& r) {
     using A = Canon<FGold>;
+    constexpr int KR = (L + 1) / 2, KC = L - KR;
     fstep::FsArgs<A> a{};
     a.batch = r.batch;
-    a.Kr = 8;
-    a.Kc = 8;
+    a.Kr = KR;
+    a.Kc = KC;
     a.stw = static_cast<const uint64_t*>(r.stw);
     a.twist = static_cast<const uint64_t*>(r.fst);
     a.tw_main = static_cast<const uint64_t*>(r.tw);
@@ -26,14 +27,26 @@ static cudaError_t fsg_run(const MultipassReq& r) {
     a.in = static_cast<const uint64_t*>(r.in);
     a.out = static_cast<uint64_t*>(r.ws);
     a.scale = 0;
-    a.count_bitrev = 1;          // every variant here bit-reverses (DIT/Pease on input, DIF on output)
-    cudaError_t e = fstep::fs_launch<A, V, 8, 0, 8>(a, r.stream, r.num_sms, r.launches);
+    a.count_bitrev = V == V_STOCKHAM ? 0 : 1;   // Stockham never bit-reverses
+    cudaError_t e = fstep::fs_launch<A, V, KR, 0, KC>(a, r.stream, r.num_sms, r.launches);
     if (e != cudaSuccess) return e;
     a.in = static_cast<const uint64_t*>(r.ws);
     a.out = static_cast<uint64_t*>(r.out);
     a.scale = r.scale;
     a.count_bitrev = 0;
-    return fstep::fs_launch<A, V, 8, 1, 8>(a, r.stream, r.num_sms, r.launches);
+    return fstep::fs_launch<A, V, KC, 1, KR>(a, r.stream, r.num_sms, r.launches);
+}
+
+template <int V>
+static cudaError_t fsg_run(const MultipassReq& r) {
+    switch (r.L) {
+        case 14: return fsg_run_l<V, 14>(r);
+        case 15: return fsg_run_l<V, 15>(r);
+        case 16: return fsg_run_l<V, 16>(r);
+        case 17: return fsg_run_l<V, 17>(r);
+        case 18: return fsg_run_l<V, 18>(r);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t fourstep_gold(const MultipassReq& r, bool* ok) {
@@ -41,8 +54,10 @@ cudaError_t fourstep_gold(const MultipassReq& r, bool* ok) {
     if (!fourstep_gold_enabled() || !fourstep_applies(r.L, r.variant, r.p, 8) || !r.fst || !r.stw || !r.ws)
         return cudaSuccess;
     *ok = true;
-    if (r.variant == V_DIT) return fsg_run<V_DIT>(r);
+    // Flat's per-stage states are DIT's: DIT sub-transforms
+    if (r.variant == V_DIT || r.variant == V_FLAT) return fsg_run<V_DIT>(r);
     if (r.variant == V_DIF) return fsg_run<V_DIF>(r);
+    if (r.variant == V_STOCKHAM) return fsg_run<V_STOCKHAM>(r);
     return fsg_run<V_PEASE_NC>(r);
 }
 

@@ -308,9 +308,10 @@ inline bool fourstep_applies(int L, int variant, uint64_t p, int word) {
         return p < (1ull << 30) && L >= 14 && L <= 20 &&
                (variant == V_DIT || variant == V_PEASE_NC || variant == V_DIF || variant == V_FLAT ||
                 variant == V_STOCKHAM);
-    // Goldilocks 2^16 = 256 x 256 (config 3): DIT, DIF, Pease_nc sub-transforms
-    return word == 8 && p == 0xFFFFFFFF00000001ull && L == 16 &&
-           (variant == V_DIT || variant == V_DIF || variant == V_PEASE_NC);
+    // Goldilocks 2^14..2^18 (config 3: 2^16 = 256 x 256)
+    return word == 8 && p == 0xFFFFFFFF00000001ull && L >= 14 && L <= 18 &&
+           (variant == V_DIT || variant == V_DIF || variant == V_PEASE_NC || variant == V_FLAT ||
+            variant == V_STOCKHAM);
 }
 inline int fourstep_kr(int L) { return (L + 1) / 2; }
 // u32 (p < 2^31) 2^14 outside the four-step (Pease, Stockham): the compile-time tile

@@ -178,12 +178,13 @@ def test_fourstep_sizes_vs_oracle(variant, L):
                           O.ntt(x, p, g, 32, variant, inverse=True, scale=True)), (variant, L)
 
 
-@pytest.mark.parametrize("variant", ["dit", "dif", "pease_nc"])
-def test_fourstep_goldilocks_2_16(variant):
-    """Goldilocks 256 x 256 four-step (config 3's size): forward, unscaled
+@pytest.mark.parametrize("variant", ["dit", "dif", "pease_nc", "stockham", "flat"])
+@pytest.mark.parametrize("L", [14, 15, 16, 17, 18])
+def test_fourstep_goldilocks(variant, L):
+    """Goldilocks four-step 2^14..2^18 (config 3: 256 x 256): forward, unscaled
     inverse and intt against the oracle."""
     p, g = (1 << 64) - (1 << 32) + 1, 7
-    x = rand(p, 3, 16, np.uint64, 4116)
+    x = rand(p, 3 if L <= 16 else 1, L, np.uint64, 4100 + L)
     assert np.array_equal(gpu_ntt(x, p, g, 64, variant), O.ntt(x, p, g, 64, variant))
     assert np.array_equal(gpu_ntt(x, p, g, 64, variant, inverse=True), O.ntt(x, p, g, 64, variant, inverse=True))
     assert np.array_equal(gpu_ntt(x, p, g, 64, variant, inverse=True, scale=True),
