@@ -123,6 +123,8 @@ cudaError_t try_fast(const MultipassReq& r, bool* ok) {
         return run_fast_policy<Canon<F32S>, V>(r, ok);
     } else if constexpr (std::is_same<F, FGold>::value) {
         return run_fast_policy<Canon<FGold>, V>(r, ok);
+    } else if constexpr (std::is_same<F, F32W>::value) {
+        return run_fast_policy<Canon<F32W>, V>(r, ok);     // 2^31 <= p < 2^32 (DEFAULT_PRIME)
     } else {
         return cudaSuccess;
     }
@@ -134,9 +136,9 @@ cudaError_t run_variant(const MultipassReq& r) {
     const int L = r.L;
     const uint64_t N = 1ull << L;
     constexpr int elog = tile_elems_log2<T>();
-    if constexpr (std::is_same<F, F32S>::value || std::is_same<F, FGold>::value) {   // four-step (fourstep.cuh)
-        bool ok = false;
-        cudaError_t fe = std::is_same<F, F32S>::value ? fourstep_f32(r, &ok) : fourstep_gold(r, &ok);
+    if constexpr (std::is_same<F, F32S>::value || std::is_same<F, F32W>::value || std::is_same<F, FGold>::value) {
+        bool ok = false;                                                             // four-step (fourstep.cuh)
+        cudaError_t fe = std::is_same<F, FGold>::value ? fourstep_gold(r, &ok) : fourstep_f32(r, &ok);
         if (fe != cudaSuccess || ok) return fe;
     }
     if constexpr (std::is_same<F, F32S>::value) {

@@ -302,10 +302,10 @@ cudaError_t mp_launch_f32s(const MultipassReq& r);
 cudaError_t pointwise_inverse_f32(const MultipassReq& r, const void* in2, bool* ok);
 // two-pass four-step for large u32 N (fourstep.cuh, kfs_f32.cu); *ok = false when it does not apply
 cudaError_t fourstep_f32(const MultipassReq& r, bool* ok);
-// four-step: LazyF32 fields (p < 2^30) DIT / Flat / DIF / Pease_nc / Stockham 14 <= L <= 20, Goldilocks 2^16
+// four-step: u32 fields DIT / Flat / DIF / Pease_nc / Stockham 14 <= L <= 20, Goldilocks 2^14..2^18
 inline bool fourstep_applies(int L, int variant, uint64_t p, int word) {
     if (word == 4)
-        return p < (1ull << 30) && L >= 14 && L <= 20 &&
+        return p < (1ull << 32) && L >= 14 && L <= 20 &&
                (variant == V_DIT || variant == V_PEASE_NC || variant == V_DIF || variant == V_FLAT ||
                 variant == V_STOCKHAM);
     // Goldilocks 2^14..2^18 (config 3: 2^16 = 256 x 256)

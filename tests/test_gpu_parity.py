@@ -178,6 +178,18 @@ def test_fourstep_sizes_vs_oracle(variant, L):
                           O.ntt(x, p, g, 32, variant, inverse=True, scale=True)), (variant, L)
 
 
+@pytest.mark.parametrize("variant", ["dit", "dif", "pease_nc", "stockham"])
+@pytest.mark.parametrize("p,g", [(3221225473, 5), (2013265921, 31)])
+@pytest.mark.parametrize("L", [14, 17, 20])
+def test_fourstep_canonical_u32_fields(variant, p, g, L):
+    """Four-step with canonical u32 arithmetic: the reference's DEFAULT_PRIME
+    3221225473 (2^31 <= p: Shoup with a 33-bit intermediate) and BabyBear."""
+    x = rand(p, 2 if L < 20 else 1, L, np.uint32, 4300 + L)
+    assert np.array_equal(gpu_ntt(x, p, g, 32, variant), O.ntt(x, p, g, 32, variant)), (p, variant, L)
+    assert np.array_equal(gpu_ntt(x, p, g, 32, variant, inverse=True, scale=True),
+                          O.ntt(x, p, g, 32, variant, inverse=True, scale=True)), (p, variant, L)
+
+
 @pytest.mark.parametrize("variant", ["dit", "dif", "pease_nc", "stockham", "flat"])
 @pytest.mark.parametrize("L", [14, 15, 16, 17, 18])
 def test_fourstep_goldilocks(variant, L):
