@@ -572,8 +572,10 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     // (A zero-copy variant -- the kernel reading and writing the pinned host
     // buffers through UVA -- is bit-exact but measured slower: 1.81 vs 1.69 ms
     // for config 2, tools/pcie_pipe.py.)
-    // Multi-pass plans share one workspace and run as a single chunk.
-    const bool resident = ntt_plan_workspace_bytes(plan, 1) == 0;
+    // Multi-pass plans chunk the same way: every chunk's transform runs on the
+    // one compute stream, so they take turns on that stream's workspace.
+    // (The six-step's single giant row is one chunk.)
+    const bool resident = plan->variant != NTT_SIXSTEP && plan->variant != NTT_NAIVE;
     uint64_t chunks = 1;
     // 8 chunks measured best for 64 MiB each way (tools/e2e_sweep.py): every
     // pinned copy costs ~20 us on the copy engines, so more chunks lose more
