@@ -125,6 +125,8 @@ cudaError_t try_fast(const MultipassReq& r, bool* ok) {
         return run_fast_policy<Canon<FGold>, V>(r, ok);
     } else if constexpr (std::is_same<F, F32W>::value) {
         return run_fast_policy<Canon<F32W>, V>(r, ok);     // 2^31 <= p < 2^32 (DEFAULT_PRIME)
+    } else if constexpr (std::is_same<F, F64>::value) {
+        return run_fast_policy<Canon<F64>, V>(r, ok);      // generic 64-bit primes (Shoup, 65-bit z)
     } else {
         return cudaSuccess;
     }
