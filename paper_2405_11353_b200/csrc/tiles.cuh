@@ -16,9 +16,14 @@ template <> inline uint64_t make_tw2<FGold>(uint64_t w, uint64_t) { return w; }
 
 template <class T>
 __global__ void k_copy_rows(const T* src, T* dst, uint64_t n, uint64_t rows, unsigned long long* counters) {
-    const uint64_t n4 = n * sizeof(T) / 16;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += (uint64_t)gridDim.x * blockDim.x)
-        reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0 && (n * sizeof(T)) % 16 == 0) {
+        const uint64_t n4 = n * sizeof(T) / 16;
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += stride)
+            reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+    } else {                                   // caller buffers only element-aligned
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
+    }
     if (counters && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(counters + C_COPIES, (unsigned long long)rows);
 }
 

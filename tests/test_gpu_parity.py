@@ -9,6 +9,7 @@ package's public API, which executes through the C ABI (libntt_b200.so).
 from __future__ import annotations
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -488,3 +489,14 @@ def test_host_buffer_path_config2(variant):
     dp = P.algorithms.device_plan_for(P.make_plan(params, variant, w.n), 4, 0)
     dp.exec_host(pinned.data_ptr(), out.data_ptr(), w.batch, False)
     assert O.sha256_le(out.numpy().view(np.uint32)) == GOLDEN[2][1]
+
+
+def test_randomised_parity_sweep():
+    """tools/fuzz_parity.py: 250 seeded random (field, variant, N, batch,
+    direction, in-place, 4-byte-aligned) cases, every one bit-exact."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_parity.py"), "250", "3"],
+                         capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
