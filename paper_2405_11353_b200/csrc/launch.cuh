@@ -268,9 +268,105 @@ cudaError_t run_variant(const MultipassReq& r) {
     return cudaSuccess;
 }
 
+// ---- six-step with any split (algorithms.py:355-389) whose sub-transforms
+// exceed one shared-memory pass: the same six steps out of batched pieces --
+// transposes, the batched size-n2 / size-n1 DITs through the ordinary
+// dispatcher (multi-pass / four-step as their sizes need), and the correction
+// w_N^(i*k2) from the plan's two-level table.  Workspace 4 x batch x N.
+template <class F>
+__global__ void k_transpose_gen(const typename F::T* in, typename F::T* out, uint64_t batch, int rb, int cb,
+                                F f, int scale, typename F::T ninv) {
+    using T = typename F::T;
+    __shared__ T tile[32][33];
+    const uint64_t R = 1ull << rb, C = 1ull << cb;
+    const uint64_t tr = (R + 31) / 32, tc = (C + 31) / 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (uint64_t blk = blockIdx.x; blk < batch * tr * tc; blk += gridDim.x) {
+        const uint64_t b = blk / (tr * tc), rem = blk % (tr * tc);
+        const uint64_t br = (rem / tc) * 32, bc = (rem % tc) * 32;
+        const T* src = in + b * R * C;
+        T* dst = out + b * R * C;
+        for (int k = ty; k < 32; k += 8)
+            if (br + k < R && bc + tx < C) tile[k][tx] = src[(br + k) * C + bc + tx];
+        __syncthreads();
+        for (int k = ty; k < 32; k += 8)
+            if (bc + k < C && br + tx < R) {
+                T v = tile[tx][k];
+                if (scale) v = f.mul_full(v, ninv);
+                dst[(bc + k) * R + br + tx] = v;
+            }
+        __syncthreads();
+    }
+}
+
+template <class F>
+__global__ void k_six_correct(typename F::T* a, uint64_t batch, int l1, int l2, const typename F::T* cor_lo,
+                              const typename F::T* cor_hi, int cor_lb, F f) {
+    const uint64_t n = 1ull << (l1 + l2);
+    for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < batch * n;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t e0 = idx & (n - 1);
+        const uint64_t i = e0 >> l2, k2 = e0 & ((1ull << l2) - 1);
+        const uint64_t e = (i * k2) & (n - 1);
+        const typename F::T w = f.mul_full(cor_hi[e >> cor_lb], cor_lo[e & ((1ull << cor_lb) - 1)]);
+        a[idx] = f.mul_full(a[idx], w);
+    }
+}
+
+template <class F>
+cudaError_t launch_field(const MultipassReq& r);
+
+template <class F>
+cudaError_t run_sixstep_general(const MultipassReq& r) {
+    using T = typename F::T;
+    int l1 = 0, l2 = 0;
+    while ((1ull << l1) < r.n1) ++l1;
+    while ((1ull << l2) < r.n2) ++l2;
+    const uint64_t N = 1ull << (l1 + l2);
+    T* w0 = static_cast<T*>(r.ws);
+    T* w1 = w0 + r.batch * N;
+    T* wsub = w1 + r.batch * N;                 // 2 x batch x N for the sub-transforms' own passes
+    F f;
+    f.p = (T)r.p;
+    const unsigned tgrid = (unsigned)((r.batch * ((N + 1023) / 1024) < (uint64_t)r.num_sms * 8)
+                                          ? r.batch * ((N + 1023) / 1024) : (uint64_t)r.num_sms * 8);
+    auto sub = [&](const void* tw, const void* stw, int L, uint64_t rows, T* buf) -> cudaError_t {
+        MultipassReq q = r;
+        q.variant = V_DIT; q.L = L; q.in = buf; q.out = buf; q.batch = rows;
+        q.tw = tw; q.stw = stw; q.scale = 0; q.fst = nullptr; q.ws = wsub;
+        q.counters = nullptr;                    // the pieces are not transforms of the plan's size
+        return L == 0 ? cudaSuccess : launch_field<F>(q);
+    };
+    cudaError_t e;
+    // T1: x[j*n1 + i] -> w0[i][j]
+    k_transpose_gen<F><<<tgrid, 256, 0, r.stream>>>(static_cast<const T*>(r.in), w0, r.batch, l2, l1, f, 0, T(0));
+    if (r.launches) ++*r.launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // D1: size-n2 DIT of every column i (algorithms.py:372-376)
+    if ((e = sub(r.tw2, r.stw2, l2, r.batch << l1, w0)) != cudaSuccess) return e;
+    // C: w0[i][k2] *= w_N^(i*k2) (algorithms.py:377-379)
+    k_six_correct<F><<<(unsigned)r.num_sms * 8, 256, 0, r.stream>>>(w0, r.batch, l1, l2, static_cast<const T*>(r.cor_lo),
+                                                                    static_cast<const T*>(r.cor_hi), r.cor_lb, f);
+    if (r.launches) ++*r.launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // T2: w0[i][k2] -> w1[k2][i]
+    k_transpose_gen<F><<<tgrid, 256, 0, r.stream>>>(w0, w1, r.batch, l1, l2, f, 0, T(0));
+    if (r.launches) ++*r.launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // D2: size-n1 DIT of every row k2 (algorithms.py:381-387)
+    if ((e = sub(r.tw1, r.stw1, l1, r.batch << l2, w1)) != cudaSuccess) return e;
+    // T3: w1[k2][k1] -> out[k1*n2 + k2] (n^-1 folded in for intt)
+    k_transpose_gen<F><<<tgrid, 256, 0, r.stream>>>(w1, static_cast<T*>(r.out), r.batch, l2, l1, f, r.scale,
+                                                   (T)r.ninv);
+    if (r.launches) ++*r.launches;
+    return cudaGetLastError();
+}
+
 template <class F>
 cudaError_t run_sixstep(const MultipassReq& r) {
     using T = typename F::T;
+    if (r.n1 > (1ull << single_pass_max_log2(sizeof(T))) || r.n2 > (1ull << single_pass_max_log2(sizeof(T))))
+        return run_sixstep_general<F>(r);
     if constexpr (std::is_same<F, FGold>::value) {
         bool ok = false;
         cudaError_t te = tile_sixstep_gold(r, &ok);

@@ -416,8 +416,7 @@ int ntt_plan_create(uint64_t p, uint64_t g, int w_bits, uint64_t n, int variant,
         if (st) return st;
     }
     if (variant == NTT_SIXSTEP) {
-        if (ilog2(n1) > smem_max_log2_word(word_bytes) || ilog2(n2) > smem_max_log2_word(word_bytes))
-            return fail(NTT_E_SIZE_NOT_SUPPORTED, "six-step sub-transforms must fit in shared memory");
+        // sub-transforms beyond one shared-memory pass run the general six-step (launch.cuh)
         if (n1 > 1 && (st = get_dev_table(p, g, n1, direction, word_bytes, device, pl->table1))) return st;
         if (n2 > 1 && (st = get_dev_table(p, g, n2, direction, word_bytes, device, pl->table2))) return st;
         uint64_t omega = powmod(g, (p - 1) / n, p);
@@ -489,7 +488,11 @@ int ntt_plan_info(ntt_plan_t plan, ntt_plan_info_t* info) {
 
 uint64_t ntt_plan_workspace_bytes(ntt_plan_t plan, uint64_t batch) {
     if (!plan) return 0;
-    if (plan->variant == NTT_SIXSTEP) return 2 * batch * plan->n * plan->word;   // step ping-pong (tiles.cuh)
+    if (plan->variant == NTT_SIXSTEP) {
+        const bool general = plan->n1 > (1ull << smem_max_log2_word(plan->word)) ||
+                             plan->n2 > (1ull << smem_max_log2_word(plan->word));
+        return (general ? 4 : 2) * batch * plan->n * plan->word;   // step ping-pong (tiles.cuh) / general path
+    }
     return mp_workspace_bytes(plan->L, plan->word, plan->variant, batch, plan->p);
 }
 

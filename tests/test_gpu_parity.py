@@ -491,6 +491,18 @@ def test_host_buffer_path_config2(variant):
     assert O.sha256_le(out.numpy().view(np.uint32)) == GOLDEN[2][1]
 
 
+@pytest.mark.parametrize("p,g,w,dt", [(998244353, 3, 32, np.uint32), ((1 << 64) - (1 << 32) + 1, 7, 64, np.uint64)])
+@pytest.mark.parametrize("L,n1", [(18, 2), (18, 1 << 15), (17, 1 << 16), (20, 1 << 3)])
+def test_sixstep_any_split(p, g, w, dt, L, n1):
+    """make_plan(..., n1) with sub-transforms beyond one shared-memory pass
+    (algorithms.py:322-352 accepts any power-of-two split): the general
+    six-step, forward and intt, against the oracle."""
+    x = rand(p, 1, L, dt, 4500 + L)
+    assert np.array_equal(gpu_ntt(x, p, g, w, "sixstep", n1=n1), O.ntt(x, p, g, w, "sixstep", n1=n1))
+    assert np.array_equal(gpu_ntt(x, p, g, w, "sixstep", inverse=True, scale=True, n1=n1),
+                          O.ntt(x, p, g, w, "sixstep", inverse=True, scale=True, n1=n1))
+
+
 def test_randomised_parity_sweep():
     """tools/fuzz_parity.py: 250 seeded random (field, variant, N, batch,
     direction, in-place, 4-byte-aligned) cases, every one bit-exact."""

@@ -36,10 +36,24 @@ for k in range(cases):
     misalign = word == 4 and rng.random() < 0.2
     x = np.random.default_rng(k).integers(0, p, size=(B, 1 << L), dtype=np.uint64).astype(np.uint32 if word == 4 else np.uint64)
     inverse, scale = mode != "fwd", mode == "intt"
-    want = O.ntt(x, p, g, w, variant, inverse=inverse, scale=scale)
+    n1 = None
+    if variant == "sixstep" and rng.random() < 0.5:
+        n1 = 1 << rng.randint(1, L - 1)            # explicit split (make_plan n1)
+    want = O.ntt(x, p, g, w, variant, inverse=inverse, scale=scale, n1=n1) if n1 else \
+        O.ntt(x, p, g, w, variant, inverse=inverse, scale=scale)
     params = P.FieldParams(p, g, w)
-    plan = P.make_plan(params, variant, 1 << L, P.INVERSE if inverse else P.FORWARD)
+    plan = P.make_plan(params, variant, 1 << L, P.INVERSE if inverse else P.FORWARD, n1=n1)
     dp = P.algorithms.device_plan_for(plan, word, 0)
+    if rng.random() < 0.15:                        # host-buffer path (ntt_exec_host)
+        src = np.ascontiguousarray(x)
+        out_h = np.empty_like(src)
+        if os.environ.get("FUZZ_VERBOSE"):
+            print(f"case {k}: HOST p={p} word={word} {variant} L={L} B={B} {mode} n1={n1}", flush=True)
+        dp.exec_host(src.ctypes.data, out_h.ctypes.data, B, scale)
+        if not np.array_equal(out_h, want):
+            fails += 1
+            print(f"FAIL case {k}: HOST p={p} w={w} word={word} {variant} L={L} B={B} {mode} n1={n1}", flush=True)
+        continue
     tdt, vdt = (torch.int32, np.int32) if word == 4 else (torch.int64, np.int64)
     flat = torch.from_numpy(x.view(vdt).reshape(-1)).cuda()
     off = 1 if misalign else 0
