@@ -504,6 +504,10 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
     if (!d_in || !d_out) return fail(NTT_E_INVALID, "NULL buffer");
     unsigned long long* ctr = dev_counters(plan->device);
     uint64_t need = ntt_plan_workspace_bytes(plan, batch);
+    // the O(N^2) naive DFT reads every input while writing: in place it first
+    // copies the input aside (the reference is pure, algorithms.py:52-79)
+    const bool naive_inplace = plan->variant == NTT_NAIVE && d_in == d_out;
+    if (naive_inplace) need = batch * plan->n * plan->word;
     void* ws = nullptr;
     if (need) {
         std::lock_guard<std::mutex> lk(plan->mu);
@@ -511,6 +515,11 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
         int st = grow(slot.first, slot.second, need);
         if (st) return st;
         ws = slot.first;
+    }
+    if (naive_inplace) {
+        cudaError_t ce = cudaMemcpyAsync(ws, d_in, need, cudaMemcpyDeviceToDevice, stream);
+        if (ce != cudaSuccess) return cuda_fail(ce, "naive in-place copy");
+        d_in = ws;
     }
     int launches = 0;
     MultipassReq r{};

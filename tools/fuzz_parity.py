@@ -19,7 +19,7 @@ def generic64():
 g64 = generic64()
 FIELDS = [(998244353, 3, 32, 4, 20), (3221225473, 5, 32, 4, 20), (2013265921, 31, 32, 4, 20),
           (GOLD, 7, 64, 8, 18), (g64[0], g64[1], 64, 8, 12), (998244353, 3, 64, 8, 12)]
-VARIANTS = ("dit", "dif", "flat", "pease", "pease_nc", "stockham", "sixstep")
+VARIANTS = ("dit", "dif", "flat", "pease", "pease_nc", "stockham", "sixstep", "naive")
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 fails = 0
@@ -30,6 +30,26 @@ for k in range(cases):
     L = rng.randint(1, lmax)
     if variant == "sixstep" and L < 2:
         L = 2
+    if variant == "naive":
+        L = min(L, 10)
+    if rng.random() < 0.1 and L <= 14:             # polymul: intt(ntt(a) . ntt(b)) vs the oracle's
+        va = rng.choice(("dit", "dif", "pease_nc", "stockham", "flat", "pease"))
+        params = P.FieldParams(p, g, w)
+        a = np.random.default_rng(10 * k).integers(0, p, size=(2, 1 << L), dtype=np.uint64).astype(np.uint32 if word == 4 else np.uint64)
+        b = np.random.default_rng(10 * k + 1).integers(0, p, size=(2, 1 << L), dtype=np.uint64).astype(a.dtype)
+        fa, fb = O.ntt(a, p, g, w, va), O.ntt(b, p, g, w, va)
+        prod = np.array([[int(u) * int(v) % p for u, v in zip(ra, rb)] for ra, rb in zip(fa, fb)], dtype=a.dtype) \
+            if word == 8 else ((fa.astype(np.uint64) * fb.astype(np.uint64)) % p).astype(np.uint32)
+        want = O.ntt(prod, p, g, w, va, inverse=True, scale=True)
+        vdt = np.int32 if word == 4 else np.int64
+        tdt = torch.uint32 if word == 4 else torch.uint64
+        ta = torch.from_numpy(a.view(vdt)).view(tdt).cuda()
+        tb = torch.from_numpy(b.view(vdt)).view(tdt).cuda()
+        got = P.cyclic_mul_ntt(ta, tb, params, va).cpu().view(torch.int32 if word == 4 else torch.int64).numpy().view(a.dtype)
+        if not np.array_equal(got, want):
+            fails += 1
+            print(f"FAIL case {k}: POLYMUL p={p} word={word} {va} L={L}", flush=True)
+        continue
     B = rng.randint(1, 4) if L <= 16 else 1
     mode = rng.choice(("fwd", "inv", "intt"))
     inplace = rng.random() < 0.3
