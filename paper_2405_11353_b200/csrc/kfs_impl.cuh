@@ -72,6 +72,43 @@ inline cudaError_t fs_pass_tma_k(const MultipassReq& r, const CUtensorMap& map) 
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// NTT_FS_RB5=1: the 2^10 passes with 32-residue register blocks (experiment switch)
+inline bool fs_rb5_enabled() {
+    static const bool on = [] { const char* e = getenv("NTT_FS_RB5"); return e && e[0] == '1'; }();
+    return on;
+}
+
+template <class A, int V, int MODE, int KO>
+inline cudaError_t fs_pass_tma5(const MultipassReq& r, const CUtensorMap& map) {
+    constexpr int Kr = MODE == 0 ? 10 : KO, Kc = MODE == 0 ? KO : 10;
+    fstep::FsTmaArgs<A> a{};
+    a.in = static_cast<const uint32_t*>(MODE == 0 ? r.in : r.ws);
+    a.out = static_cast<uint32_t*>(MODE == 0 ? r.ws : r.out);
+    a.batch = r.batch;
+    a.Kr = Kr;
+    a.Kc = Kc;
+    a.stw = static_cast<const uint2*>(r.stw);
+    a.tw_main = static_cast<const uint2*>(r.tw);
+    a.p = r.p;
+    a.scale = MODE == 1 ? r.scale : 0;
+    a.ninv = make_uint2((uint32_t)r.ninv, (uint32_t)r.ninv_shoup);
+    a.count_bitrev = MODE == 0 ? 1 : 0;
+    a.counters = r.counters;
+    constexpr size_t smem = fstep::fsa5_smem_bytes<MODE>();
+    auto kern = fstep::k_fs_tma5<A, V, MODE, KO>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    const uint64_t ntiles = r.batch << ((MODE == 0 ? Kc : Kr) - 3);
+    uint64_t grid = (uint64_t)r.num_sms * occ;
+    if (grid > ntiles) grid = ntiles;
+    e = fastk::launch_pdl(kern, dim3((unsigned)grid), dim3(256), smem, r.stream, map, a);
+    if (r.launches) ++*r.launches;
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 // true when the pass ran through the TMA kernel (*err its status)
 template <class A, int V, int MODE>
 inline bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err) {
@@ -104,6 +141,12 @@ inline bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err)
     // (K, other dimension) pairs of 2^14 .. 2^20 (Kr = ceil(L/2), Kc = floor(L/2))
 #define NTT_FSTK(KK, KOO) \
     if (K == KK && (MODE == 0 ? Kc : Kr) == KOO) { *err = fs_pass_tma_k<A, V, MODE, KK, KOO>(r, map); return true; }
+    if constexpr (std::is_same<A, LazyF32>::value) {
+        if (K == 10 && fs_rb5_enabled()) {
+            if ((MODE == 0 ? Kc : Kr) == 10) { *err = fs_pass_tma5<A, V, MODE, 10>(r, map); return true; }
+            if (MODE == 0 && Kc == 9) { *err = fs_pass_tma5<A, V, 0, 9>(r, map); return true; }
+        }
+    }
     if constexpr (MODE == 0) {
         NTT_FSTK(7, 7) NTT_FSTK(8, 7) NTT_FSTK(8, 8) NTT_FSTK(9, 8) NTT_FSTK(9, 9) NTT_FSTK(10, 9) NTT_FSTK(10, 10)
     } else {
