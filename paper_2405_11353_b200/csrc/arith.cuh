@@ -22,6 +22,9 @@
 #define NTT_HD __host__ __device__ __forceinline__
 #define NTT_D __device__ __forceinline__
 // Goldilocks multiply: mad.wide product chain (1) or four mul.wide + carry adds (0)
+#ifndef NTT_GOLD_W
+#define NTT_GOLD_W 0      // 1: Goldilocks wrap corrections as IMAD.WIDE (FGoldC::madw) -- slower, FMA-pipe bound
+#endif
 #ifndef NTT_GOLD_MULM
 #define NTT_GOLD_MULM 1
 #endif
@@ -182,10 +185,86 @@ struct FGoldC {
         (void)m;
         return c2 ? mk(q0, q1) : mk(s0, s1);
     }
-    NTT_D T add(T a, T b) const { return add_c(a, b); }
+    // ---- wrap corrections as c * EPS + s (one IMAD.WIDE.U32 on the FMA pipe)
+    // instead of compare / SEL pairs on the ALU pipe, which the Goldilocks
+    // kernels saturate.  c is a carry bit; the 64-bit sum wraps mod 2^64, so
+    // s + EPS - 2^64 = s - p comes out of the same instruction.
+    NTT_D static T madw(uint32_t c, T s) {
+        T r;
+        asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(c), "r"(0xffffffffu), "l"(s));
+        return r;
+    }
+    // carry of s + EPS (s >= p  <=>  s + EPS >= 2^64)
+    NTT_D static uint32_t ge_p(T s) {
+        uint32_t c;
+        asm("add.cc.u32 %0, %1, 0xffffffff;\n\t"
+            "addc.cc.u32 %0, %2, 0;\n\t"
+            "addc.u32 %0, 0, 0;"
+            : "=&r"(c) : "r"(lo(s)), "r"(hi(s)));
+        return c;
+    }
+    NTT_D static T canon_w(T s) { return madw(ge_p(s), s); }
+    // a + b reduced once: for any a < 2^64 and b < p the result is < 2^64 and
+    // congruent to a + b (a + b - 2^64 <= p - 2, so + EPS cannot wrap again)
+    NTT_D static T add_lazy(T a, T b) {
+        uint32_t s0, s1, c;
+        asm("add.cc.u32 %0, %3, %5;\n\t"
+            "addc.cc.u32 %1, %4, %6;\n\t"
+            "addc.u32 %2, 0, 0;"
+            : "=r"(s0), "=r"(s1), "=r"(c)
+            : "r"(lo(a)), "r"(hi(a)), "r"(lo(b)), "r"(hi(b)));
+        return madw(c, mk(s0, s1));
+    }
+    NTT_D static T add_w(T a, T b) { return canon_w(add_lazy(a, b)); }   // a, b < p
+    // the same lazy sum with the correction on the ALU pipe
+    NTT_D static T add_lazy_a(T a, T b) {
+        uint32_t s0, s1, c;
+        asm("add.cc.u32 %0, %3, %5;\n\t"
+            "addc.cc.u32 %1, %4, %6;\n\t"
+            "addc.u32 %2, 0, 0;\n\t"
+            "neg.s32 %2, %2;\n\t"                 // carry: + EPS
+            "add.cc.u32 %0, %0, %2;\n\t"
+            "addc.u32 %1, %1, 0;"
+            : "=&r"(s0), "=&r"(s1), "=&r"(c)
+            : "r"(lo(a)), "r"(hi(a)), "r"(lo(b)), "r"(hi(b)));
+        return mk(s0, s1);
+    }
+    // canonical by compare / select (s + EPS overflows  <=>  s >= p)
+    NTT_D static T canon_s(T s) {
+        uint32_t q0, q1, c;
+        asm("add.cc.u32 %0, %3, 0xffffffff;\n\t"
+            "addc.cc.u32 %1, %4, 0;\n\t"
+            "addc.u32 %2, 0, 0;"
+            : "=&r"(q0), "=&r"(q1), "=&r"(c) : "r"(lo(s)), "r"(hi(s)));
+        return c ? mk(q0, q1) : s;
+    }
+    // mul_m with both corrections as IMAD.WIDE; canonical for any a < 2^64, b < 2^64
+    NTT_D static T mul_w(T a, T b) {
+        const uint32_t a0 = lo(a), a1 = hi(a), b0 = lo(b), b1 = hi(b);
+        const uint64_t p00 = (uint64_t)a0 * b0;
+        const uint64_t t = (uint64_t)a0 * b1 + (p00 >> 32);
+        const uint64_t u = (uint64_t)a1 * b0 + (uint32_t)t;
+        const uint64_t v = (uint64_t)a1 * b1 + (t >> 32) + (u >> 32);
+        const uint32_t r0 = lo(p00), r1 = lo(u), r2 = lo(v), r3 = hi(v);
+        const uint64_t ue = (uint64_t)r2 * 0xFFFFFFFFu;          // r2 * EPS
+        uint32_t t0, t1, m, c;
+        asm("sub.cc.u32 %0, %4, %6;\n\t"          // t = lo64 - r3
+            "subc.cc.u32 %1, %5, 0;\n\t"
+            "subc.u32 %2, 0, 0;\n\t"                // m = borrow ? EPS : 0
+            "sub.cc.u32 %0, %0, %2;\n\t"            // t -= EPS on borrow (no underflow)
+            "subc.u32 %1, %1, 0;\n\t"
+            "add.cc.u32 %0, %0, %7;\n\t"           // t += r2 * EPS, carry c
+            "addc.cc.u32 %1, %1, %8;\n\t"
+            "addc.u32 %3, 0, 0;"
+            : "=&r"(t0), "=&r"(t1), "=&r"(m), "=&r"(c)
+            : "r"(r0), "r"(r1), "r"(r3), "r"(lo(ue)), "r"(hi(ue)));
+        (void)m;
+        return canon_w(madw(c, mk(t0, t1)));       // carry: + EPS (cannot wrap again)
+    }
+    NTT_D T add(T a, T b) const { return NTT_GOLD_W ? add_w(a, b) : add_c(a, b); }
     NTT_D T sub(T a, T b) const { return sub_c(a, b); }
-    NTT_D T mul(T x, Tw w) const { return NTT_GOLD_MULM ? mul_m(x, w) : mul_c(x, w); }
-    NTT_D T mul_full(T a, T b) const { return NTT_GOLD_MULM ? mul_m(a, b) : mul_c(a, b); }
+    NTT_D T mul(T x, Tw w) const { return NTT_GOLD_W ? mul_w(x, w) : NTT_GOLD_MULM ? mul_m(x, w) : mul_c(x, w); }
+    NTT_D T mul_full(T a, T b) const { return NTT_GOLD_W ? mul_w(a, b) : NTT_GOLD_MULM ? mul_m(a, b) : mul_c(a, b); }
     NTT_D static T tw_value(Tw w) { return w; }
 };
 #pragma nv_diag_default 550
@@ -204,7 +283,7 @@ struct FGold {
     NTT_D static T canon(T x) { return x >= P ? x - P : x; }
     // the kernels use the carry-chain forms (FGoldC, bit-identical results,
     // ~15% more butterflies/s); reduce128/canon stay for reference
-    NTT_D T add(T a, T b) const { return FGoldC::add_c(a, b); }
+    NTT_D T add(T a, T b) const { return NTT_GOLD_W ? FGoldC::add_w(a, b) : FGoldC::add_c(a, b); }
     NTT_D T sub(T a, T b) const { return FGoldC::sub_c(a, b); }
     NTT_D static T reduce128(uint64_t lo, uint64_t hi) {
         uint64_t hh = hi >> 32, hl = hi & EPS;
@@ -215,8 +294,8 @@ struct FGold {
         if (t2 < t1) t2 += EPS;        // carry: 2^64 == EPS
         return canon(t2);
     }
-    NTT_D T mul_full(T a, T b) const { return NTT_GOLD_MULM ? FGoldC::mul_m(a, b) : FGoldC::mul_c(a, b); }
-    NTT_D T mul(T x, Tw w) const { return NTT_GOLD_MULM ? FGoldC::mul_m(x, w) : FGoldC::mul_c(x, w); }
+    NTT_D T mul_full(T a, T b) const { return FGoldC().mul_full(a, b); }
+    NTT_D T mul(T x, Tw w) const { return FGoldC().mul(x, w); }
     NTT_D static T tw_value(Tw w) { return w; }
 };
 

@@ -12,7 +12,7 @@ static bool fourstep_gold_enabled() {
 
 template <int V, int L>
 static cudaError_t fsg_run_l(const MultipassReq& r) {
-    using A = Canon<FGold>;
+    using A = GoldPolicy<V == V_DIF>;
     constexpr int KR = (L + 1) / 2, KC = L - KR;
     fstep::FsArgs<A> a{};
     a.batch = r.batch;

@@ -4,10 +4,10 @@
 #include <cstdlib>
 namespace nttb200 {
 cudaError_t tile_passes_gold(int variant, const MultipassReq& r, bool* ok) {
-    using A = Canon<FGold>;
+    using A = GoldPolicy<false>;
     switch (variant) {
         case V_DIT: return ftile::run_tile_passes<A, V_DIT>(r, ok);
-        case V_DIF: return ftile::run_tile_passes<A, V_DIF>(r, ok);
+        case V_DIF: return ftile::run_tile_passes<GoldPolicy<true>, V_DIF>(r, ok);
         case V_FLAT: return ftile::run_tile_passes<A, V_FLAT>(r, ok);
         case V_PEASE: return ftile::run_tile_passes<A, V_PEASE>(r, ok);
         case V_PEASE_NC: return ftile::run_tile_passes<A, V_PEASE_NC>(r, ok);
@@ -20,7 +20,7 @@ static bool six_match(const MultipassReq& r) {
     return r.n1 == (1ull << K1) && r.n2 == (1ull << K2);
 }
 cudaError_t tile_sixstep_gold(const MultipassReq& r, bool* ok) {
-    using A = Canon<FGold>;
+    using A = GoldPolicy<false>;
     *ok = false;
     if (!r.stw1 || !r.stw2 || !r.cor_lo) return cudaSuccess;
     // long-run column/row passes + explicit transpose; the column-at-a-time
@@ -40,7 +40,7 @@ uint64_t sixstep_dist_ws_bytes(uint64_t n, int world, int word) { return 2 * (n 
 
 cudaError_t tile_sixstep_dist_gold(const MultipassReq& r, int step, int rank, int world, const void* in, void* out,
                                    bool* ok) {
-    using A = Canon<FGold>;
+    using A = GoldPolicy<false>;
     *ok = false;
     if (!r.stw1 || !r.stw2 || !r.cor_lo) return cudaSuccess;
     // long-run column passes + per-destination transpose (NTT_SIXSTEP_LEGACY=1: column-at-a-time kernels)

@@ -122,7 +122,7 @@ cudaError_t try_fast(const MultipassReq& r, bool* ok) {
         if (r.p < (1ull << 30)) return run_fast_policy<LazyF32, V>(r, ok);
         return run_fast_policy<Canon<F32S>, V>(r, ok);
     } else if constexpr (std::is_same<F, FGold>::value) {
-        return run_fast_policy<Canon<FGold>, V>(r, ok);
+        return run_fast_policy<GoldPolicy<V == V_DIF>, V>(r, ok);
     } else if constexpr (std::is_same<F, F32W>::value) {
         return run_fast_policy<Canon<F32W>, V>(r, ok);     // 2^31 <= p < 2^32 (DEFAULT_PRIME)
     } else if constexpr (std::is_same<F, F64>::value) {

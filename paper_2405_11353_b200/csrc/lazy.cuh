@@ -9,6 +9,7 @@
 // (every stage canonical, exactly like the reference).
 #pragma once
 #include "arith.cuh"
+#include <type_traits>
 
 namespace nttb200 {
 
@@ -103,6 +104,59 @@ struct LazyF32 {
     }
 };
 
+// LazyGold: Goldilocks DIT-type butterflies with lazy sums.  Values live in
+// [0, 2^64) between stages (congruent mod p, not canonical); products are
+// canonical, so x + t (t < p) wraps 2^64 at most once and x - t (t < p)
+// borrows at most once; fin() canonicalises at the stores.  Per butterfly
+// 19 ALU-pipe instructions instead of 29 (the canonical kernels are ALU-bound).
+// DIF-type butterflies (both inputs lazy) canonicalise their inputs first:
+// DIF plans keep Canon<FGold>.
+template <int AW>
+struct LazyGoldT {
+    NTT_D static uint64_t addl(uint64_t a, uint64_t b) { return AW ? FGoldC::add_lazy(a, b) : FGoldC::add_lazy_a(a, b); }
+    NTT_D static uint64_t canon(uint64_t s) { return AW == 2 ? FGoldC::canon_w(s) : FGoldC::canon_s(s); }
+    NTT_D static uint64_t mul(uint64_t a, uint64_t b) { return AW == 2 ? FGoldC::mul_w(a, b) : FGoldC::mul_m(a, b); }
+    NTT_D static uint64_t add(uint64_t a, uint64_t b) { return AW == 2 ? FGoldC::add_w(a, b) : FGoldC::add_c(a, b); }
+    using T = uint64_t;
+    using Tw = uint64_t;
+    using Field = FGold;
+    static constexpr bool lazy = true;
+    NTT_D void init(uint64_t) {}
+    NTT_D void dit(T& x, T& y, Tw w) const {
+        const T t = mul(y, w);
+        const T a = x;
+        x = addl(a, t);
+        y = FGoldC::sub_c(a, t);
+    }
+    NTT_D void dit1(T& x, T& y) const {
+        const T t = canon(y);
+        const T a = x;
+        x = addl(a, t);
+        y = FGoldC::sub_c(a, t);
+    }
+    NTT_D void dit1_c(T& x, T& y) const { dit1(x, y); }
+    NTT_D void dit_2p(T& x, T& y, Tw w) const { dit(x, y, w); }
+    NTT_D void dit1_2p(T& x, T& y) const { dit1(x, y); }
+    NTT_D void dif(T& x, T& y, Tw w) const {
+        const T a = canon(x), b = canon(y);
+        x = add(a, b);
+        y = mul(FGoldC::sub_c(a, b), w);
+    }
+    NTT_D void dif1(T& x, T& y) const {
+        const T a = canon(x), b = canon(y);
+        x = add(a, b);
+        y = FGoldC::sub_c(a, b);
+    }
+    NTT_D T fin(T x) const { return canon(x); }
+    NTT_D T mulc(T x, Tw w) const { return mul(x, w); }
+    NTT_D T mull(T x, Tw w) const { return mul(x, w); }
+    NTT_D T mulfull(T a, T b) const { return mul(a, b); }
+};
+#ifndef NTT_GOLD_LAZY_AW
+#define NTT_GOLD_LAZY_AW 0
+#endif
+using LazyGold = LazyGoldT<NTT_GOLD_LAZY_AW>;
+
 template <class F>
 struct Canon {
     using T = typename F::T;
@@ -141,5 +195,13 @@ struct Canon {
     NTT_D T mull(T x, Tw w) const { return f.mul(x, w); }
     NTT_D T mulfull(T a, T b) const { return f.mul_full(a, b); }
 };
+
+#ifndef NTT_GOLD_LAZY
+#define NTT_GOLD_LAZY 1      // 0: every Goldilocks plan on Canon<FGold>
+#endif
+// Goldilocks policy of a plan: lazy sums for the DIT-type dataflows (DIT,
+// Flat, Pease, Pease_nc, Stockham, six-step), canonical for DIF
+template <bool DIF_TYPE>
+using GoldPolicy = typename std::conditional<DIF_TYPE || !NTT_GOLD_LAZY, Canon<FGold>, LazyGold>::type;
 
 }  // namespace nttb200

@@ -219,6 +219,11 @@ struct FGoldMix2 : FGoldC {
     NTT_D T sub(T a, T b) const { return FGoldCC::subcc(a, b); }
 };
 
+// the previous default (mad.wide product, SEL-based corrections)
+struct FGoldM : FGoldC {
+    NTT_D T add(T a, T b) const { return add_c(a, b); }
+    NTT_D T mul(T x, Tw w) const { return mul_m(x, w); }
+};
 __global__ void k_goldcheck(const uint64_t* a, const uint64_t* b, int n, int* bad) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -231,6 +236,22 @@ __global__ void k_goldcheck(const uint64_t* a, const uint64_t* b, int n, int* ba
     if (FGoldCC::subcc(x, y) != (x < y ? x - y - FGold::EPS : x - y)) atomicAdd(bad + 2, 1);
     { uint64_t s_ = x + y; if (s_ < x) s_ += FGold::EPS; if (FGoldC::add_c(x, y) != FGold::canon(s_)) atomicAdd(bad + 1, 1); }
     if (FGoldC::sub_c(x, y) != (x < y ? x - y - FGold::EPS : x - y)) atomicAdd(bad + 2, 1);
+    // wide-correction forms; lazy operand xl anywhere in [0, 2^64)
+    const uint64_t xl = x + (uint64_t)(i & 3) * (0xFFFFFFFFull * 0x55555555ull) ;
+    if (FGoldC::mul_w(xl, y) != FGold::reduce128(xl * y, __umul64hi(xl, y))) atomicAdd(bad, 1);
+    if (FGoldC::mul_w(x, y) != FGold::reduce128(x * y, __umul64hi(x, y))) atomicAdd(bad, 1);
+    if (FGoldC::mul_m(xl, y) != FGold::reduce128(xl * y, __umul64hi(xl, y))) atomicAdd(bad, 1);
+    if (FGoldC::canon_s(xl) != (xl >= FGold::P ? xl - FGold::P : xl)) atomicAdd(bad + 1, 1);
+    { const uint64_t l = FGoldC::add_lazy_a(xl, y);
+      uint64_t s_ = FGold::canon(FGold::canon(xl)) + y; if (s_ < y) s_ += FGold::EPS;
+      if (FGoldC::canon_s(l) != FGold::canon(s_)) atomicAdd(bad + 1, 1); }
+    { uint64_t s_ = x + y; if (s_ < x) s_ += FGold::EPS; if (FGoldC::add_w(x, y) != FGold::canon(s_)) atomicAdd(bad + 1, 1); }
+    { const uint64_t l = FGoldC::add_lazy(xl, y);
+      uint64_t s_ = FGold::canon(FGold::canon(xl)) + y; if (s_ < y) s_ += FGold::EPS;
+      if (FGoldC::canon_w(l) != FGold::canon(s_)) atomicAdd(bad + 1, 1); }
+    if (FGoldC::canon_w(xl) != (xl >= FGold::P ? xl - FGold::P : xl)) atomicAdd(bad + 1, 1);
+    { const uint64_t xc = FGold::canon(xl);
+      if (FGoldC::canon_w(FGoldC::sub_c(xl, y)) != (xc < y ? xc - y - FGold::EPS : xc - y)) atomicAdd(bad + 2, 1); }
 }
 void check_gold() {
     const int n = 1 << 22;
@@ -274,6 +295,12 @@ int main() {
     run<Canon<FGoldOld>>("gold-mulc", G, 7ull, 49ull, 512);
     run<Canon<FGoldW>>("gold-wideE", G, 7ull, 49ull, 256);
     run<Canon<FGoldW>>("gold-wideE", G, 7ull, 49ull, 512);
+    run<Canon<FGoldM>>("gold-mulm", G, 7ull, 49ull, 256);
+    run<Canon<FGoldM>>("gold-mulm", G, 7ull, 49ull, 512);
+    run<LazyGoldT<0>>("gold-lazy0", G, 7ull, 49ull, 256);
+    run<LazyGoldT<0>>("gold-lazy0", G, 7ull, 49ull, 512);
+    run<LazyGoldT<1>>("gold-lazy1", G, 7ull, 49ull, 512);
+    run<LazyGoldT<2>>("gold-lazy2", G, 7ull, 49ull, 512);
     // exactness check of FGoldC vs FGold on random operands
     check_gold();
     return 0;
