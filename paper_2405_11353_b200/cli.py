@@ -2,6 +2,8 @@
 
     python -m paper_2405_11353_b200.cli verify [--max-log 10] [--prime P] [--vectors 5]
     python -m paper_2405_11353_b200.cli bench  [--algo A ...] [--size N ...] [--batch B] [--reps R] [--csv F]
+    python -m paper_2405_11353_b200.cli banks  --algo A --log-n L [--interleave M | --blocksize B | --banks K --search
+                                                | --units U] [--ports 2] [--unroll 1] [--csv F]
 
 ``bench`` keeps the reference CSV schema (cli.py:24) and seeding (cli.py:39-42)
 and appends GPU columns (batch, device time, NTT/s, Gbutterfly/s, algorithmic
@@ -21,6 +23,7 @@ import sys
 
 import numpy as np
 
+from . import bankmodel
 from .algorithms import VARIANTS, intt, make_plan, naive_dft, ntt
 from .errors import InvalidSize, NttError
 from .modmath import DEFAULT_PRIME, FieldParams, find_primitive_root
@@ -125,6 +128,51 @@ def write_bench_csv(records, path) -> None:
             w.writerow({k: r[k] for k in BENCH_CSV_FIELDS})
 
 
+def banks_run(args) -> int:
+    """``banks``: the bank-conflict model (nttkit/cli.py:181-241, same output)."""
+    if args.units is not None:
+        if args.algo != "pease_nc":
+            print("error: --units applies to the pease_nc swap-safety check")
+            return 1
+        rep = bankmodel.pease_nc_partition_check(args.log_n, args.units, args.ports)
+    else:
+        trace = bankmodel.gen_trace(args.algo, args.log_n)
+        if args.search:
+            if args.banks is None:
+                print("error: --search requires --banks")
+                return 1
+            part = bankmodel.feasible_partition(trace, args.banks, ports=args.ports, unroll=args.unroll)
+            if part is None:
+                print(f"infeasible: no II=1 partition with {args.banks} bank(s) per array")
+                return 0
+            for arr, m in sorted(part.items()):
+                desc = (" ".join(f"{a}->{b}" for a, b in enumerate(m.table)) if m.kind == "explicit"
+                        else f"{m.kind}={m.param}")
+                print(f"array {arr}: {desc}")
+            print("feasible: II=1")
+            return 0
+        mapping = bankmodel.blocksize(args.blocksize) if args.blocksize is not None else \
+            bankmodel.interleave(args.interleave)
+        rep = bankmodel.schedule(trace, bankmodel.BankConfig(mapping, ports=args.ports, unroll=args.unroll))
+    print(bankmodel.report_text(rep))
+    if args.csv:
+        row = dict(algo=args.algo, log_n=args.log_n, ports=args.ports, unroll=args.unroll,
+                   **bankmodel.report_csv_row(rep))
+        fields = ["algo", "log_n", "ports", "unroll", "achieved_ii", "target_ii", "feasible", "conflicts",
+                  "swap_safe"]
+        try:
+            empty = not open(args.csv, "rb").read(1)
+        except FileNotFoundError:
+            empty = True
+        with open(args.csv, "a", newline="") as fh:
+            w = csv.DictWriter(fh, fieldnames=fields)
+            if empty:
+                w.writeheader()
+            w.writerow(row)
+        print(f"wrote report to {args.csv}")
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser(prog="paper_2405_11353_b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -141,6 +189,17 @@ def build_parser() -> argparse.ArgumentParser:
     b.add_argument("--seed", type=int, default=42)
     b.add_argument("--prime", type=int, default=DEFAULT_PRIME)
     b.add_argument("--csv")
+    k = sub.add_parser("banks")
+    k.add_argument("--algo", required=True, choices=bankmodel.TRACE_VARIANTS)
+    k.add_argument("--log-n", type=int, required=True)
+    k.add_argument("--interleave", type=int, default=1)
+    k.add_argument("--blocksize", type=int)
+    k.add_argument("--banks", type=int)
+    k.add_argument("--ports", type=int, default=2)
+    k.add_argument("--unroll", type=int, default=1)
+    k.add_argument("--units", type=int)
+    k.add_argument("--search", action="store_true")
+    k.add_argument("--csv")
     return ap
 
 
@@ -149,7 +208,12 @@ def main(argv=None) -> int:
         args = build_parser().parse_args(argv)
     except SystemExit as e:
         return 2 if e.code else 0
+    if args.cmd == "banks" and not 1 <= args.log_n <= 16:
+        print("error: --log-n must be in [1, 16]", file=sys.stderr)
+        return 2
     try:
+        if args.cmd == "banks":
+            return banks_run(args)
         if args.cmd == "verify":
             fails = verify_run(args.max_log, args.seed, args.prime, args.vectors)
             for f in fails:
