@@ -276,8 +276,12 @@ def main() -> None:
         return {"total_ms": total_ms, "per_step_ms": per_launch_ms, "launches": launches, "parity": parity,
                 "clocks": clocks, "nset": nset, "footprint_bytes": 2 * nset * nbytes, "dp": dp}
 
-    def e2e(w, variant, steps):
-        """Through the C-ABI host-buffer call: pinned H2D + transform + D2H per step."""
+    def e2e(w, variant, steps, asynchronous=True):
+        """Through the C-ABI host-buffer call: pinned H2D + transform + D2H per step.
+        asynchronous: NTT_FLAG_HOST_ASYNC -- each call enqueues its step and
+        returns, so step i's copy-out overlaps step i+1's copy-in; one stream
+        synchronise after the K steps, inside the timed region.  Otherwise the
+        synchronous call (the reference's list-in / list-out contract)."""
         params = P.FieldParams(w.p, w.g, w.w)
         plan = P.make_plan(params, variant, w.n, P.FORWARD, n1=w.n1)
         dp = P.algorithms.device_plan_for(plan, w.word, local_rank)
@@ -287,11 +291,13 @@ def main() -> None:
         hout = torch.empty_like(hin).pin_memory()
         sp = stream.cuda_stream
         for _ in range(2):
-            dp.exec_host(hin.data_ptr(), hout.data_ptr(), w.batch, False, sp)
+            dp.exec_host(hin.data_ptr(), hout.data_ptr(), w.batch, False, sp, asynchronous)
+        stream.synchronize()
         barrier()
         t0 = time.perf_counter()
         for _ in range(steps):
-            dp.exec_host(hin.data_ptr(), hout.data_ptr(), w.batch, False, sp)
+            dp.exec_host(hin.data_ptr(), hout.data_ptr(), w.batch, False, sp, asynchronous)
+        stream.synchronize()
         el = max_over_ranks(time.perf_counter() - t0)
         del tdt
         return world * w.batch * steps / el, x_host.nbytes
@@ -305,6 +311,7 @@ def main() -> None:
     alg_bytes = w.algorithmic_bytes()
     achieved = alg_bytes / (m["per_step_ms"] / 1e3) / 1e9
     e2e_val, io_bytes = e2e(w, args.variant, max(3, min(args.steps, 20)))
+    e2e_sync, _ = e2e(w, args.variant, max(3, min(args.steps, 20)), asynchronous=False)
     dit = measure(w, "dit", args.steps, args.warmup)
 
     extra = {}
@@ -463,7 +470,8 @@ def main() -> None:
                          "algorithmic_bytes_per_launch": alg_bytes},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "NTT/s", "h2d_bytes_per_step": io_bytes,
-                    "d2h_bytes_per_step": io_bytes},
+                    "d2h_bytes_per_step": io_bytes, "api": "ntt_exec_host, NTT_FLAG_HOST_ASYNC (steps pipelined)",
+                    "synchronous_value": e2e_sync},
             "gpu_launches": m["launches"],
             "clocks": m["clocks"],
             "dit": {"ntt_per_s": world * w.batch / (dit["total_ms"] / 1e3 / args.steps),

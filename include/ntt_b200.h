@@ -53,6 +53,10 @@ typedef enum { NTT_FORWARD = 0, NTT_INVERSE = 1 } ntt_direction_t;
 
 /* ntt_exec flags. */
 #define NTT_FLAG_SCALE 1u   /* multiply by n_inv (intt, algorithms.py:415-423); needs an INVERSE plan */
+#define NTT_FLAG_HOST_ASYNC 2u  /* ntt_exec_host only: enqueue and return; completion is ordered on `stream`
+                                   (synchronise it before touching h_out or reusing h_in; h_in must be
+                                   ready on the host at the call).  Successive calls pipeline: the
+                                   copy-out of one overlaps the copy-in of the next. */
 
 typedef struct ntt_plan_s* ntt_plan_t;
 
@@ -100,7 +104,7 @@ int ntt_exec(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t batch, uns
 
 /* Same with HOST buffers: H2D copy, transform, D2H copy, synchronise (the
  * path a list[int] / numpy caller takes; `stream` is unused -- the call is
- * synchronous).  Large batches of shared-memory-resident plans are cut into
+ * synchronous -- unless flags has NTT_FLAG_HOST_ASYNC).  Large batches of shared-memory-resident plans are cut into
  * chunks pipelined over three internal streams so the copies in both
  * directions overlap the transforms (use pinned host memory for overlap). */
 int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch, unsigned flags,

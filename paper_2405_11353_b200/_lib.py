@@ -35,6 +35,7 @@ _STATUS_EXC = {
 VARIANT_IDS = {"naive": 0, "dit": 1, "dif": 2, "flat": 3, "pease": 4, "pease_nc": 5, "stockham": 6,
                "sixstep": 7}
 NTT_FLAG_SCALE = 1
+NTT_FLAG_HOST_ASYNC = 2
 
 # every symbol include/ntt_b200.h declares
 EXPORTS = (
@@ -145,8 +146,12 @@ class DevicePlan:
     def exec_device(self, in_ptr: int, out_ptr: int, batch: int, scale: bool, stream: int) -> None:
         check(load().ntt_exec(self._h, in_ptr, out_ptr, batch, NTT_FLAG_SCALE if scale else 0, stream))
 
-    def exec_host(self, in_ptr: int, out_ptr: int, batch: int, scale: bool, stream: int = 0) -> None:
-        check(load().ntt_exec_host(self._h, in_ptr, out_ptr, batch, NTT_FLAG_SCALE if scale else 0, stream))
+    def exec_host(self, in_ptr: int, out_ptr: int, batch: int, scale: bool, stream: int = 0,
+                  asynchronous: bool = False) -> None:
+        """Host buffers in and out.  asynchronous: enqueue and return, completion
+        ordered on `stream` (NTT_FLAG_HOST_ASYNC; successive calls pipeline)."""
+        flags = (NTT_FLAG_SCALE if scale else 0) | (NTT_FLAG_HOST_ASYNC if asynchronous else 0)
+        check(load().ntt_exec_host(self._h, in_ptr, out_ptr, batch, flags, stream))
 
     def pointwise_inverse(self, a_ptr: int, b_ptr: int, out_ptr: int, batch: int, stream: int) -> None:
         """out = intt(a .* b) (fused on shared-memory-resident u32 plans)"""

@@ -252,6 +252,13 @@ struct ntt_plan_s {
     static constexpr int kMaxChunks = 64;
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t hev[2 * kMaxChunks] = {};
+    // NTT_FLAG_HOST_ASYNC: two device buffer sets used by alternate calls;
+    // hout[set][chunk] = that chunk's copy-out done (the next call on the set
+    // waits for it before overwriting), hend orders the caller's stream
+    // after the copy-out
+    cudaEvent_t hout[2 * kMaxChunks] = {};
+    cudaEvent_t hend = nullptr;
+    uint64_t host_seq = 0;
     std::mutex mu;        // guards ws / hbuf / stream + event creation
     std::mutex host_mu;   // serialises ntt_exec_host calls (one host pipeline per plan)
     ~ntt_plan_s() {
@@ -262,11 +269,16 @@ struct ntt_plan_s {
             if (kv.second.first) cudaFree(kv.second.first);
         for (auto& kv : pw_ws)
             if (kv.second.first) cudaFree(kv.second.first);
+        for (auto st : hs)                 // asynchronous host calls may still be in flight
+            if (st) cudaStreamSynchronize(st);
         if (hbuf) cudaFree(hbuf);
         for (auto st : hs)
             if (st) cudaStreamDestroy(st);
         for (auto ev : hev)
             if (ev) cudaEventDestroy(ev);
+        for (auto ev : hout)
+            if (ev) cudaEventDestroy(ev);
+        if (hend) cudaEventDestroy(hend);
         if (cor_lo) cudaFree(cor_lo);
         if (cor_hi) cudaFree(cor_hi);
         if (twh) cudaFree(twh);
@@ -564,16 +576,28 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     const uint64_t row_bytes = plan->n * plan->word;
     const uint64_t bytes = batch * row_bytes;
     int st = NTT_OK;
+    const bool async = (flags & NTT_FLAG_HOST_ASYNC) != 0;
+    flags &= ~NTT_FLAG_HOST_ASYNC;
     std::lock_guard<std::mutex> host_lk(plan->host_mu);
+    const int set = async ? (int)(plan->host_seq++ & 1) : 0;
     {
         std::lock_guard<std::mutex> lk(plan->mu);
-        st = grow(plan->hbuf, plan->hbuf_bytes, bytes);
+        const uint64_t need = (async ? 2 : 1) * bytes;
+        if (need > plan->hbuf_bytes)       // reallocation: earlier asynchronous calls must be done with it
+            for (auto hs : plan->hs)
+                if (hs) cudaStreamSynchronize(hs);
+        st = grow(plan->hbuf, plan->hbuf_bytes, need);
         for (auto& hs : plan->hs)
             if (!st && !hs && cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking) != cudaSuccess)
                 st = fail(NTT_E_CUDA, "stream creation failed");
         for (auto& ev : plan->hev)
             if (!st && !ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
                 st = fail(NTT_E_CUDA, "event creation failed");
+        for (auto& ev : plan->hout)
+            if (!st && !ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+                st = fail(NTT_E_CUDA, "event creation failed");
+        if (!st && !plan->hend && cudaEventCreateWithFlags(&plan->hend, cudaEventDisableTiming) != cudaSuccess)
+            st = fail(NTT_E_CUDA, "event creation failed");
     }
     cudaError_t e = cudaSuccess;
     // Shared-memory-resident plans need no workspace, so the batch is cut into
@@ -593,13 +617,22 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     // pinned copy costs ~20 us on the copy engines, so more chunks lose more
     // than the shorter pipeline fill/drain gains
     if (resident && bytes >= (16ull << 20)) chunks = bytes >= (64ull << 20) ? 8 : 4;
+    // asynchronous calls overlap one call's copy-out with the next call's
+    // copy-in, so the within-call pipeline only needs to cover the transform:
+    // 2 chunks (config 2: 1.43 ms/step at 1-2 chunks, 1.55 at 8; the PCIe
+    // floor with both directions busy is 1.35 ms, tools/e2e_async.py)
+    if (async && resident && bytes >= (16ull << 20)) chunks = 2;
     static const int env_chunks = [] { const char* v = getenv("NTT_HOST_CHUNKS"); return v ? atoi(v) : 0; }();
     if (resident && env_chunks > 0) chunks = (uint64_t)env_chunks;     // tuning knob (tools/e2e_sweep.py)
     if (chunks > (uint64_t)ntt_plan_s::kMaxChunks) chunks = ntt_plan_s::kMaxChunks;
     if (chunks > batch) chunks = batch;
-    (void)stream;
-    char* d = static_cast<char*>(plan->hbuf);
+    char* d = static_cast<char*>(plan->hbuf) + (size_t)set * bytes;
     cudaStream_t sH = plan->hs[0], sC = plan->hs[1], sD = plan->hs[2];
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaEvent_t* hout = plan->hout + set * ntt_plan_s::kMaxChunks;
+    // (no wait on `stream` at the start: it carries the previous asynchronous
+    // call's completion, and waiting for it would serialise the calls -- h_in
+    // must be ready on the host when the call is made)
     auto span = [&](uint64_t c, uint64_t& r0, uint64_t& off, uint64_t& nb) {
         r0 = batch * c / chunks;
         const uint64_t r1 = batch * (c + 1) / chunks;
@@ -612,7 +645,11 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     uint64_t r0, off, nb;
     for (uint64_t c = 0; !st && c < chunks; ++c) {
         span(c, r0, off, nb);
-        e = cudaMemcpyAsync(d + off, static_cast<const char*>(h_in) + off, nb, cudaMemcpyHostToDevice, sH);
+        // the previous call on this buffer set has copied this chunk out (a
+        // never-recorded event is already complete)
+        e = cudaStreamWaitEvent(sH, hout[c], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(d + off, static_cast<const char*>(h_in) + off, nb, cudaMemcpyHostToDevice, sH);
         if (e == cudaSuccess) e = cudaEventRecord(plan->hev[2 * c], sH);
         if (e != cudaSuccess) st = cuda_fail(e, "H2D copy");
     }
@@ -628,7 +665,15 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
         e = cudaStreamWaitEvent(sD, plan->hev[2 * c + 1], 0);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(static_cast<char*>(h_out) + off, d + off, nb, cudaMemcpyDeviceToHost, sD);
+        if (e == cudaSuccess) e = cudaEventRecord(hout[c], sD);
         if (e != cudaSuccess) st = cuda_fail(e, "D2H copy");
+    }
+    if (async && !st) {                    // the caller's stream continues after the copy-out
+        e = cudaEventRecord(plan->hend, sD);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(user, plan->hend, 0);
+        if (e != cudaSuccess) st = cuda_fail(e, "stream order");
+        if (cur != plan->device) cudaSetDevice(cur);
+        return st;
     }
     for (auto hs : plan->hs) {
         cudaError_t e2 = cudaStreamSynchronize(hs);

@@ -491,6 +491,43 @@ def test_host_buffer_path_config2(variant):
     assert O.sha256_le(out.numpy().view(np.uint32)) == GOLDEN[2][1]
 
 
+def test_host_buffer_async_pipelined():
+    """NTT_FLAG_HOST_ASYNC: back-to-back calls on distinct host buffers (the
+    copy-out of one overlapping the copy-in of the next, alternating device
+    buffer sets), one synchronise, every output exact -- including a third call
+    that reuses the first call's buffer set and a synchronous call after."""
+    w = CONFIGS[2]
+    params = P.FieldParams(w.p, w.g, w.w)
+    dp = P.algorithms.device_plan_for(P.make_plan(params, "pease_nc", w.n), 4, 0)
+    xs = [seeded_input(w)] + [rand(w.p, w.batch, 12, np.uint32, 7100 + i) for i in range(3)]
+    hin = [torch.from_numpy(x.view(np.int32)).pin_memory() for x in xs]
+    hout = [torch.empty_like(h).pin_memory() for h in hin]
+    st = torch.cuda.Stream()
+    for i in range(4):
+        dp.exec_host(hin[i].data_ptr(), hout[i].data_ptr(), w.batch, False, st.cuda_stream, True)
+    st.synchronize()
+    assert O.sha256_le(hout[0].numpy().view(np.uint32)) == GOLDEN[2][1]
+    for i in (1, 2, 3):
+        want = P.ntt(torch.from_numpy(xs[i].view(np.int32)).view(torch.uint32).cuda(), P.build_table(params, w.n),
+                     "pease_nc").cpu().view(torch.int32).numpy().view(np.uint32)
+        assert np.array_equal(hout[i].numpy().view(np.uint32), want), i
+    # a synchronous call right after asynchronous ones, and small / multi-pass plans
+    out = torch.empty_like(hin[1]).pin_memory()
+    dp.exec_host(hin[1].data_ptr(), out.data_ptr(), w.batch, False)
+    assert np.array_equal(out.numpy(), hout[1].numpy())
+    for L, B in ((10, 3), (16, 5)):
+        x = rand(w.p, B, L, np.uint32, 7200 + L)
+        dq = P.algorithms.device_plan_for(P.make_plan(params, "dit", 1 << L), 4, 0)
+        hi = torch.from_numpy(x.view(np.int32)).pin_memory()
+        ho = [torch.empty_like(hi).pin_memory() for _ in range(3)]
+        for o in ho:
+            dq.exec_host(hi.data_ptr(), o.data_ptr(), B, False, st.cuda_stream, True)
+        st.synchronize()
+        want = O.ntt(x, w.p, w.g, 32, "dit")
+        for o in ho:
+            assert np.array_equal(o.numpy().view(np.uint32), want)
+
+
 @pytest.mark.parametrize("p,g,w,dt", [(998244353, 3, 32, np.uint32), ((1 << 64) - (1 << 32) + 1, 7, 64, np.uint64)])
 @pytest.mark.parametrize("L,n1", [(18, 2), (18, 1 << 15), (17, 1 << 16), (20, 1 << 3)])
 def test_sixstep_any_split(p, g, w, dt, L, n1):
