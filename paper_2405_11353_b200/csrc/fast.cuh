@@ -336,7 +336,9 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     fence_mbar_init();
     __syncthreads();
     // programmatic dependent launch: the prologue above (plan-owned tables only)
-    // overlaps the previous launch's tail; its outputs are visible after the wait
+    // overlaps the previous launch's tail; its outputs are visible after the wait.
+    // (Issuing the first TMA loads before the table copy moves the copy behind
+    // the wait: config 2 37.1 vs 34.6 us per step, measured A/B.)
     pdl_trigger();
     pdl_wait();
 
