@@ -235,6 +235,16 @@ def main() -> None:
             torch.cuda.synchronize(dev)
             out = ys[0].cpu().view(torch.int32 if w.word == 4 else torch.int64).numpy()
             parity = hashlib.sha256(out.astype("<u4" if w.word == 4 else "<u8").tobytes()).hexdigest() == GOLDEN[w.cfg][1]
+        roundtrip = None
+        if check_hash and inverse:
+            # no reference hash for the inverse: intt(ntt(x)) == x on the seeded input
+            fplan = P.make_plan(params, variant, w.n, P.FORWARD, n1=w.n1)
+            fdp = P.algorithms.device_plan_for(fplan, w.word, local_rank)
+            fdp.exec_device(xs[0].data_ptr(), ys[0].data_ptr(), w.batch, False, sp)
+            dp.exec_device(ys[0].data_ptr(), ys[1].data_ptr(), w.batch, True, sp)
+            torch.cuda.synchronize(dev)
+            sdt = torch.int32 if w.word == 4 else torch.int64
+            roundtrip = bool(torch.equal(ys[1].view(sdt), xs[0].view(sdt)))
         with torch.cuda.stream(stream):
             for i in range(warmup):
                 dp.exec_device(xs[i % nset].data_ptr(), ys[i % nset].data_ptr(), w.batch, inverse, sp)
@@ -274,7 +284,7 @@ def main() -> None:
         del xs, ys, graph
         torch.cuda.empty_cache()
         return {"total_ms": total_ms, "per_step_ms": per_launch_ms, "launches": launches, "parity": parity,
-                "clocks": clocks, "nset": nset, "footprint_bytes": 2 * nset * nbytes, "dp": dp}
+                "roundtrip": roundtrip, "clocks": clocks, "nset": nset, "footprint_bytes": 2 * nset * nbytes, "dp": dp}
 
     def e2e(w, variant, steps, asynchronous=True):
         """Through the C-ABI host-buffer call: pinned H2D + transform + D2H per step.
@@ -329,6 +339,7 @@ def main() -> None:
                     "hbm_alg_gbs": ab / (r["per_step_ms"] / 1e3) / 1e9,
                     "roofline_frac": ab / (r["per_step_ms"] / 1e3) / 1e9 / peak,
                     "launches_per_step": r["launches"] / ext_steps, "sha256_parity": r["parity"],
+                    "roundtrip_parity": r["roundtrip"],
                     "workload": f"{wc.batch} x 2^{wc.log2n}, p={wc.p}"}
             except Exception as exc:  # report, do not hide
                 extra[f"config{cfg}_{var}"] = {"error": repr(exc)[:300]}

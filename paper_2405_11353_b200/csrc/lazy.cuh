@@ -109,8 +109,11 @@ struct LazyF32 {
 // canonical, so x + t (t < p) wraps 2^64 at most once and x - t (t < p)
 // borrows at most once; fin() canonicalises at the stores.  Per butterfly
 // 19 ALU-pipe instructions instead of 29 (the canonical kernels are ALU-bound).
-// DIF-type butterflies (both inputs lazy) canonicalise their inputs first:
-// DIF plans keep Canon<FGold>.
+// DIF-type butterflies canonicalise the y input only (one canon per butterfly
+// instead of canonical sums).  Bit-exact, but measured slower on config 3
+// (four-step DIF 322 vs 314 us/step, ncu: 118 M instructions in pass A at the
+// same 62 % issue-active), so DIF plans keep Canon<FGold> unless built with
+// NTT_GOLD_LAZY_DIF=1.
 template <int AW>
 struct LazyGoldT {
     NTT_D static uint64_t addl(uint64_t a, uint64_t b) { return AW ? FGoldC::add_lazy(a, b) : FGoldC::add_lazy_a(a, b); }
@@ -137,14 +140,17 @@ struct LazyGoldT {
     NTT_D void dit1_c(T& x, T& y) const { dit1(x, y); }
     NTT_D void dit_2p(T& x, T& y, Tw w) const { dit(x, y, w); }
     NTT_D void dit1_2p(T& x, T& y) const { dit1(x, y); }
+    // DIF: only y is canonicalised -- x + b (x < 2^64, b < p) wraps at most once
+    // and x - b borrows at most once, exactly the DIT forms; the sum stays lazy,
+    // the product is canonical
     NTT_D void dif(T& x, T& y, Tw w) const {
-        const T a = canon(x), b = canon(y);
-        x = add(a, b);
+        const T a = x, b = canon(y);
+        x = addl(a, b);
         y = mul(FGoldC::sub_c(a, b), w);
     }
     NTT_D void dif1(T& x, T& y) const {
-        const T a = canon(x), b = canon(y);
-        x = add(a, b);
+        const T a = x, b = canon(y);
+        x = addl(a, b);
         y = FGoldC::sub_c(a, b);
     }
     NTT_D T fin(T x) const { return canon(x); }
@@ -201,7 +207,11 @@ struct Canon {
 #endif
 // Goldilocks policy of a plan: lazy sums for the DIT-type dataflows (DIT,
 // Flat, Pease, Pease_nc, Stockham, six-step), canonical for DIF
+#ifndef NTT_GOLD_LAZY_DIF
+#define NTT_GOLD_LAZY_DIF 0
+#endif
 template <bool DIF_TYPE>
-using GoldPolicy = typename std::conditional<DIF_TYPE || !NTT_GOLD_LAZY, Canon<FGold>, LazyGold>::type;
+using GoldPolicy =
+    typename std::conditional<(DIF_TYPE && !NTT_GOLD_LAZY_DIF) || !NTT_GOLD_LAZY, Canon<FGold>, LazyGold>::type;
 
 }  // namespace nttb200
