@@ -127,6 +127,19 @@ uint64_t ntt_plan_workspace_bytes(ntt_plan_t plan, uint64_t batch);
 int ntt_sixstep_dist_step(ntt_plan_t plan, int step, int rank, int world, const void* d_in, void* d_out,
                           void* stream);
 
+/* Step A of ntt_sixstep_dist_step with the exchange fused into its pack: the
+ * per-destination blocks are stored straight into every rank's receive
+ * buffer over NVLink (P2P stores; d_peer_recv[h] = rank h's receive buffer,
+ * mapped into this process, e.g. torch symmetric memory buffer_ptrs), block h
+ * at offset rank * n1*n2/G^2 residues -- the layout the all-to-all would have
+ * produced, so step B (ntt_sixstep_dist_step, step 1) runs unchanged.  The
+ * caller orders the ranks: a barrier before (no rank still reads its receive
+ * buffer) and after (every block has landed) on the stream.  world <= 8.
+ * Replaces the reference's serial ntt_sixstep (algorithms.py:355-389); no
+ * reference counterpart for the exchange itself. */
+int ntt_sixstep_dist_step_a_peer(ntt_plan_t plan, int rank, int world, const void* d_in, void* const* d_peer_recv,
+                                 void* stream);
+
 /* The second half of polymul.cyclic_mul_ntt (polymul.py:61-63, intt of the
  * pointwise product) as ONE call: d_out = intt(d_a .* d_b) for `batch` rows,
  * d_a / d_b the forward transforms of the operands.  `plan` must be an

@@ -41,7 +41,7 @@ NTT_FLAG_HOST_ASYNC = 2
 EXPORTS = (
     "ntt_field_check", "ntt_find_primitive_root", "ntt_root_of_unity", "ntt_table_build",
     "ntt_plan_create", "ntt_plan_destroy", "ntt_plan_info", "ntt_exec", "ntt_exec_host",
-    "ntt_plan_workspace_bytes", "ntt_pointwise_mul", "ntt_exec_pointwise_inverse", "ntt_sixstep_dist_step", "ntt_counters_enable", "ntt_counters_read",
+    "ntt_plan_workspace_bytes", "ntt_pointwise_mul", "ntt_exec_pointwise_inverse", "ntt_sixstep_dist_step", "ntt_sixstep_dist_step_a_peer", "ntt_counters_enable", "ntt_counters_read",
     "ntt_counters_reset", "ntt_last_error", "ntt_abi_version", "ntt_device_count",
 )
 
@@ -98,6 +98,7 @@ def load():
         L.ntt_pointwise_mul.argtypes = [_vp, _vp, _vp, _vp, _u64, _vp]
         L.ntt_exec_pointwise_inverse.argtypes = [_vp, _vp, _vp, _vp, _u64, _vp]
         L.ntt_sixstep_dist_step.argtypes = [_vp, _int, _int, _int, _vp, _vp, _vp]
+        L.ntt_sixstep_dist_step_a_peer.argtypes = [_vp, _int, _int, _vp, ctypes.POINTER(_vp), _vp]
         L.ntt_counters_enable.argtypes = [_int]
         L.ntt_counters_read.argtypes = [ctypes.POINTER(Counters)]
         L.ntt_counters_reset.argtypes = []
@@ -162,6 +163,12 @@ class DevicePlan:
 
     def sixstep_dist_step(self, step: int, rank: int, world: int, in_ptr: int, out_ptr: int, stream: int) -> None:
         check(load().ntt_sixstep_dist_step(self._h, step, rank, world, in_ptr, out_ptr, stream))
+
+    def sixstep_dist_step_a_peer(self, rank: int, world: int, in_ptr: int, peer_recv_ptrs, stream: int) -> None:
+        """Step A with the exchange fused into its pack: block h is stored into
+        peer_recv_ptrs[h] (rank h's receive buffer, mapped here) at slot `rank`."""
+        arr = (_vp * len(peer_recv_ptrs))(*[int(p) for p in peer_recv_ptrs])
+        check(load().ntt_sixstep_dist_step_a_peer(self._h, rank, world, in_ptr, arr, stream))
 
     def workspace_bytes(self, batch: int) -> int:
         return int(load().ntt_plan_workspace_bytes(self._h, batch))

@@ -39,15 +39,15 @@ cudaError_t tile_sixstep_gold(const MultipassReq& r, bool* ok) {
 uint64_t sixstep_dist_ws_bytes(uint64_t n, int world, int word) { return 2 * (n / (uint64_t)world) * (uint64_t)word; }
 
 cudaError_t tile_sixstep_dist_gold(const MultipassReq& r, int step, int rank, int world, const void* in, void* out,
-                                   bool* ok) {
+                                   bool* ok, void* const* peers) {
     using A = GoldPolicy<false>;
     *ok = false;
     if (!r.stw1 || !r.stw2 || !r.cor_lo) return cudaSuccess;
     // long-run column passes + per-destination transpose (NTT_SIXSTEP_LEGACY=1: column-at-a-time kernels)
     static const int legacy = [] { const char* v = getenv("NTT_SIXSTEP_LEGACY"); return v ? atoi(v) : 0; }();
-    if (!legacy) {
-        cudaError_t e = ftile::run_sixstep_cols_dist<A>(r, step, rank, world, in, out, r.ws, ok);
-        if (e != cudaSuccess || *ok) return e;
+    if (!legacy || peers) {
+        cudaError_t e = ftile::run_sixstep_cols_dist<A>(r, step, rank, world, in, out, r.ws, ok, peers);
+        if (e != cudaSuccess || *ok || peers) return e;      // the peer pack exists on the long-run path only
     }
     *ok = true;
     if (six_match<13, 13>(r))

@@ -229,6 +229,38 @@ __global__ void __launch_bounds__(256) k_transpose(const T* in, T* out, uint64_t
     }
 }
 
+// Peer-memory variant of the distributed four-step's pack (step A's last
+// store): block h of the per-destination transpose is written straight into
+// rank h's receive buffer at this rank's slot, over NVLink (P2P stores through
+// pointers the caller mapped, e.g. torch symmetric memory), so the exchange
+// rides the pack instead of a separate all-to-all.  dst[h] = peers.p[h] +
+// slot * 2^(rb+cb); same 32 x 32 tiling as k_transpose.
+constexpr int kMaxPeers = 8;
+template <class T>
+struct PeerPtrs {
+    T* p[kMaxPeers];
+};
+template <class T>
+__global__ void __launch_bounds__(256) k_transpose_peer(const T* in, PeerPtrs<T> peers, uint64_t world, int slot,
+                                                        int rb, int cb) {
+    __shared__ T tile[32][33];
+    const uint64_t R = 1ull << rb, C = 1ull << cb;
+    const int pb = rb + cb - 10;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (uint64_t blk = blockIdx.x; blk < (world << pb); blk += gridDim.x) {
+        const uint64_t h = blk >> pb, b = blk & ((1ull << pb) - 1);
+        const uint64_t br = (b >> (cb - 5)) << 5, bc = (b & ((C >> 5) - 1)) << 5;
+        const T* src = in + (h << (rb + cb));
+        T* dst = peers.p[h] + ((uint64_t)slot << (rb + cb));
+        for (int k = ty; k < 32; k += 8) tile[k][tx] = src[(br + k) * C + bc + tx];
+        __syncthreads();
+        for (int k = ty; k < 32; k += 8) dst[(bc + k) * R + br + tx] = tile[tx][k];
+        __syncthreads();
+    }
+}
+
 template <class F>
 __global__ void k_pointwise(const typename F::T* a, const typename F::T* b, typename F::T* c, uint64_t n, F f) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)

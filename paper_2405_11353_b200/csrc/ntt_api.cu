@@ -683,15 +683,20 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     return st;
 }
 
-int ntt_sixstep_dist_step(ntt_plan_t plan, int step, int rank, int world, const void* d_in, void* d_out,
-                          void* stream) {
+static int dist_step(ntt_plan_t plan, int step, int rank, int world, const void* d_in, void* d_out,
+                     void* const* d_peers, void* stream) {
     if (!plan) return fail(NTT_E_INVALID, "NULL plan");
     if (plan->variant != NTT_SIXSTEP) return fail(NTT_E_BAD_FACTORIZATION, "plan is not a six-step plan");
     if (step != 0 && step != 1) return fail(NTT_E_INVALID, "step must be 0 (A) or 1 (B)");
     if (world < 1 || (world & (world - 1)) || (uint64_t)world > plan->n1 || (uint64_t)world > plan->n2 ||
         rank < 0 || rank >= world)
         return fail(NTT_E_INVALID, "world must be a power of two dividing n1 and n2; 0 <= rank < world");
-    if (!d_in || !d_out) return fail(NTT_E_INVALID, "NULL buffer");
+    if (!d_in || (!d_out && !d_peers)) return fail(NTT_E_INVALID, "NULL buffer");
+    if (d_peers) {
+        if (world > kMaxPeers) return fail(NTT_E_INVALID, "peer pack supports at most 8 ranks");
+        for (int h = 0; h < world; ++h)
+            if (!d_peers[h]) return fail(NTT_E_INVALID, "NULL peer receive buffer");
+    }
     if (plan->kind != 2)
         return fail(NTT_E_SIZE_NOT_SUPPORTED, "distributed four-step is implemented for the Goldilocks field");
     int cur = 0;
@@ -716,12 +721,23 @@ int ntt_sixstep_dist_step(ntt_plan_t plan, int step, int rank, int world, const 
         r.ws = slot.first;
     }
     bool ok = false;
-    cudaError_t e = tile_sixstep_dist_gold(r, step, rank, world, d_in, d_out, &ok);
+    cudaError_t e = tile_sixstep_dist_gold(r, step, rank, world, d_in, d_out, &ok, d_peers);
     g_launches += launches;
     if (cur != plan->device) cudaSetDevice(cur);
     if (e != cudaSuccess) return cuda_fail(e, "distributed six-step");
     if (!ok) return fail(NTT_E_SIZE_NOT_SUPPORTED, "no compiled tile shape for this (n1, n2) split");
     return NTT_OK;
+}
+
+int ntt_sixstep_dist_step(ntt_plan_t plan, int step, int rank, int world, const void* d_in, void* d_out,
+                          void* stream) {
+    return dist_step(plan, step, rank, world, d_in, d_out, nullptr, stream);
+}
+
+int ntt_sixstep_dist_step_a_peer(ntt_plan_t plan, int rank, int world, const void* d_in, void* const* d_peer_recv,
+                                 void* stream) {
+    if (!d_peer_recv) return fail(NTT_E_INVALID, "NULL peer table");
+    return dist_step(plan, 0, rank, world, d_in, nullptr, d_peer_recv, stream);
 }
 
 int ntt_exec_pointwise_inverse(ntt_plan_t plan, const void* d_a, const void* d_b, void* d_out, uint64_t batch,

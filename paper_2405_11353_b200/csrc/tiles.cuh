@@ -422,7 +422,7 @@ cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
 // ws: 2 x n/G residues.
 template <class A>
 cudaError_t run_sixstep_cols_dist(const MultipassReq& r, int step, int rank, int world, const void* in, void* out,
-                                  void* wsv, bool* ok) {
+                                  void* wsv, bool* ok, void* const* peers = nullptr) {
     using T = typename A::T;
     *ok = false;
     int K1 = 0, K2 = 0, lg = 0;
@@ -466,6 +466,16 @@ cudaError_t run_sixstep_cols_dist(const MultipassReq& r, int step, int rank, int
         // pack: per destination h, [k2_local][i_local] -> [i_local][k2_local]
         const uint64_t blocks = (uint64_t)world << (lk + lc - 10);
         const uint64_t cap = (uint64_t)r.num_sms * 8;
+        if (peers) {      // pack straight into every rank's receive buffer (slot = this rank)
+            if (world > kMaxPeers) return cudaErrorInvalidValue;
+            PeerPtrs<T> pp{};
+            for (int h = 0; h < world; ++h) pp.p[h] = static_cast<T*>(peers[h]);
+            e = fastk::launch_pdl(k_transpose_peer<T>, dim3((unsigned)(blocks < cap ? blocks : cap)), dim3(256), 0,
+                                  r.stream, static_cast<const T*>(ws1), pp, (uint64_t)world, rank, lk, lc);
+            if (r.launches) ++*r.launches;
+            if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return e;
+            return cudaSuccess;
+        }
         e = fastk::launch_pdl(k_transpose<T>, dim3((unsigned)(blocks < cap ? blocks : cap)), dim3(256), 0, r.stream,
                               static_cast<const T*>(ws1), static_cast<T*>(out), (uint64_t)world, lk, lc);
         if (r.launches) ++*r.launches;
@@ -503,7 +513,7 @@ cudaError_t tile_passes_gold(int variant, const MultipassReq& r, bool* ok);
 cudaError_t tile_sixstep_gold(const MultipassReq& r, bool* ok);
 // distributed four-step, rank-local steps (step = 0: A, 1: B)
 cudaError_t tile_sixstep_dist_gold(const MultipassReq& r, int step, int rank, int world, const void* in, void* out,
-                                   bool* ok);
+                                   bool* ok, void* const* peers = nullptr);
 // workspace (bytes) the distributed steps need on one rank
 uint64_t sixstep_dist_ws_bytes(uint64_t n, int world, int word);
 

@@ -14,6 +14,13 @@
   columns k2 of rank h; step B runs the size-n1 DITs and leaves
   ``out_local[k1][k2_local]`` = out[k1*n2 + k2] for k2 in rank g's column slab.
 
+With ``exchange="peer"`` the all-to-all is fused into step A instead: the
+pack kernel stores block h straight into rank h's receive buffer over NVLink
+(``ntt_sixstep_dist_step_a_peer``; receive buffers from torch symmetric
+memory, whose ``buffer_ptrs`` map every peer's buffer into this process), with
+a symmetric-memory barrier before (no rank still reads its buffer) and after
+(every block has landed).
+
 The rank-local steps are ``ntt_sixstep_dist_step`` of the C ABI; they are
 injectable (``step_fns``) so the orchestration itself -- slab layout, pack
 layout, exchange, unpack -- is tested on CPU ranks with the gloo backend.
@@ -56,7 +63,7 @@ class DistributedSixStep:
     """Four-step of ONE transform across the ranks of a process group."""
 
     def __init__(self, params, n: int, direction: str = FORWARD, n1: int | None = None, n2: int | None = None,
-                 group=None, step_fns=None, device: int | None = None):
+                 group=None, step_fns=None, device: int | None = None, exchange: str = "nccl"):
         if dist is None or not dist.is_initialized():
             raise RuntimeError("torch.distributed must be initialised (one process per GPU)")
         self.plan = make_plan(params, "sixstep", n, direction, n1, n2)
@@ -71,6 +78,12 @@ class DistributedSixStep:
         self.kcols = self.n2 // G             # output columns per rank
         self.block = self.cols * self.kcols   # residues per peer in the all-to-all
         self.word = 4 if params.p < (1 << 32) else 8
+        if exchange not in ("nccl", "peer"):
+            raise ValueError("exchange must be 'nccl' or 'peer'")
+        if exchange == "peer" and (step_fns is not None or G > 8):
+            raise ValueError("the peer-memory exchange runs the device kernels on at most 8 ranks")
+        self.exchange = exchange
+        self._symm = None
         if step_fns is None:
             dev = torch.cuda.current_device() if device is None else device
             self._dp = device_plan_for(self.plan, self.word, dev)
@@ -95,12 +108,33 @@ class DistributedSixStep:
         path).  Returns out_local [n1, n2/G]."""
         if tuple(x_local.shape) != (self.n2, self.cols):
             raise ValueError(f"local slab must be {(self.n2, self.cols)}, got {tuple(x_local.shape)}")
+        out_local = torch.empty((self.n1, self.kcols), dtype=x_local.dtype, device=x_local.device)
+        if self.exchange == "peer":
+            return self._run_peer(x_local, out_local)
         send = torch.empty(self.world * self.block, dtype=x_local.dtype, device=x_local.device)
         recv = torch.empty_like(send)
-        out_local = torch.empty((self.n1, self.kcols), dtype=x_local.dtype, device=x_local.device)
         self.step_a(x_local, send, self.rank, self.world)
         # ONE exchange: block h of `send` goes to rank h (equal splits)
         self._exchange(recv, send)
+        self.step_b(recv, out_local, self.rank, self.world)
+        return out_local
+
+    def _peer_buffers(self, like):
+        """Receive buffer in symmetric memory + every rank's mapping of it."""
+        if self._symm is None:
+            import torch.distributed._symmetric_memory as symm_mem
+            group = self.group if self.group is not None else dist.group.WORLD
+            recv = symm_mem.empty(self.world * self.block, dtype=like.dtype, device=like.device)
+            handle = symm_mem.rendezvous(recv, group.group_name)
+            self._symm = (recv, handle, [int(p) for p in handle.buffer_ptrs])
+        return self._symm
+
+    def _run_peer(self, x_local, out_local):
+        recv, handle, ptrs = self._peer_buffers(x_local)
+        stream = torch.cuda.current_stream().cuda_stream
+        handle.barrier(channel=0)            # every rank is done reading its receive buffer
+        self._dp.sixstep_dist_step_a_peer(self.rank, self.world, x_local.data_ptr(), ptrs, stream)
+        handle.barrier(channel=1)            # every block has landed (stream-ordered signal)
         self.step_b(recv, out_local, self.rank, self.world)
         return out_local
 

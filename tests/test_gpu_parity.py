@@ -364,10 +364,13 @@ def test_pointwise_mul():
     assert to_host(tc)[0].tolist() == want
 
 
-def _emulate_distributed(x, p, g, n, n1, world):
+def _emulate_distributed(x, p, g, n, n1, world, peer=False):
     """Run the rank-local steps of the distributed four-step for every rank on
     ONE device through the C ABI, with the all-to-all done as a local block
-    permutation (never launching mutually-waiting ranks on one GPU)."""
+    permutation (never launching mutually-waiting ranks on one GPU).
+    peer=True: step A's pack stores straight into every rank's receive buffer
+    (ntt_sixstep_dist_step_a_peer, the NVLink path with local pointers);
+    ranks run one after another, so no kernel waits on another."""
     from paper_2405_11353_b200.distributed import assemble_output, column_slab
     n2 = n // n1
     params = P.FieldParams(p, g, 64)
@@ -376,6 +379,18 @@ def _emulate_distributed(x, p, g, n, n1, world):
     c, r = n1 // world, n2 // world
     block = c * r
     s = torch.cuda.current_stream().cuda_stream
+    if peer:
+        recvs = [torch.full((world * block,), 0xFFFF, dtype=torch.uint64, device=dev()) for _ in range(world)]
+        ptrs = [t.data_ptr() for t in recvs]
+        for rank in range(world):
+            slab = to_dev(column_slab(x, rank, world, n1, n2))
+            dp.sixstep_dist_step_a_peer(rank, world, slab.data_ptr(), ptrs, s)
+        outs = []
+        for rank in range(world):
+            out = torch.empty(n1 * r, dtype=torch.uint64, device=dev())
+            dp.sixstep_dist_step(1, rank, world, recvs[rank].data_ptr(), out.data_ptr(), s)
+            outs.append(to_host(out))
+        return assemble_output(outs, n1, n2)
     sends = []
     for rank in range(world):
         slab = to_dev(column_slab(x, rank, world, n1, n2))
@@ -397,6 +412,54 @@ def test_distributed_sixstep_emulated_small(world):
     x = rand(GOLD, 1, 14, np.uint64, 55)[0]
     got = _emulate_distributed(x, GOLD, 7, n, n1, world)
     assert np.array_equal(got, O.ntt(x, GOLD, 7, 64, "sixstep", n1=n1))
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_distributed_sixstep_peer_pack_emulated_small(world):
+    """Exchange fused into step A's pack (P2P stores into each rank's receive
+    buffer): bit-identical to the oracle's six-step."""
+    n, n1 = 1 << 18, 1 << 9      # long-run passes: n1/G, n2/G >= 64 columns at G = 8
+    x = rand(GOLD, 1, 18, np.uint64, 56)[0]
+    got = _emulate_distributed(x, GOLD, 7, n, n1, world, peer=True)
+    assert np.array_equal(got, O.ntt(x, GOLD, 7, 64, "sixstep", n1=n1))
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_distributed_sixstep_peer_pack_config5(world):
+    w = CONFIGS[5]
+    x = seeded_input(w)[0]
+    got = _emulate_distributed(x, w.p, w.g, w.n, w.n1, world, peer=True)
+    assert O.sha256_le(got) == GOLDEN[5][1]
+
+
+def test_distributed_peer_exchange_one_rank_group():
+    """DistributedSixStep(exchange="peer") through torch symmetric memory in a
+    one-rank NCCL group (subprocess with a timeout: a rendezvous that cannot
+    complete must not hang the suite)."""
+    import json, subprocess, sys
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "peer.npz")
+        pr = subprocess.run([sys.executable, os.path.join(here, "tools", "peer_world1.py"), path],
+                            capture_output=True, text=True, timeout=300)
+        lines = [ln for ln in pr.stdout.splitlines() if ln.startswith("{")]
+        assert lines, pr.stderr[-2000:]
+        res = json.loads(lines[-1])
+        assert res["ok"], res
+        d = np.load(path)
+        assert np.array_equal(d["out"], O.ntt(d["x"], GOLD, 7, 64, "sixstep", n1=res["n1"]))
+
+
+def test_distributed_peer_pack_errors():
+    params = P.FieldParams(GOLD, 7, 64)
+    dp = P.algorithms.device_plan_for(P.make_plan(params, "sixstep", 1 << 14, n1=1 << 7), 8, 0)
+    x = torch.zeros(1 << 14, dtype=torch.uint64, device=dev())
+    s = torch.cuda.current_stream().cuda_stream
+    with pytest.raises(ValueError):
+        dp.sixstep_dist_step_a_peer(0, 2, x.data_ptr(), [x.data_ptr(), 0], s)      # NULL peer buffer
+    with pytest.raises(ValueError):
+        dp.sixstep_dist_step_a_peer(0, 16, x.data_ptr(), [x.data_ptr()] * 16, s)   # > 8 ranks
 
 
 @pytest.mark.parametrize("world", [2, 8])
