@@ -173,6 +173,9 @@ def main() -> None:
     ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the N = 2^9..2^20 u32 sweep")
+    ap.add_argument("--peer-exchange", action="store_true",
+                    help="N>1: also time config 5's four-step with the exchange fused into step A's pack "
+                         "(P2P stores into symmetric memory) -- off by default: not yet run on >1 GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -456,6 +459,26 @@ def main() -> None:
                 "workload": "1 x 2^26 Goldilocks, four-step 2^13 x 2^13, one NCCL all_to_all_single"}
         except Exception as exc:
             extra["config5_sixstep_distributed"] = {"error": repr(exc)[:300]}
+        if args.peer_exchange:
+            try:
+                dsp = DistributedSixStep(params, wc.n, n1=wc.n1, n2=wc.n // wc.n1, exchange="peer")
+                with torch.cuda.stream(stream):
+                    for _ in range(3):
+                        dsp.run(slab)
+                    barrier()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    for _ in range(nst):
+                        dsp.run(slab)
+                    e1.record(stream)
+                    stream.synchronize()
+                barrier()
+                t = max_over_ranks(e0.elapsed_time(e1)) / 1e3 / nst
+                extra["config5_sixstep_distributed_peer"] = {
+                    "ntt_per_s": 1.0 / t, "ms_per_step": 1e3 * t, "scaling": "strong", "ranks": world,
+                    "workload": "1 x 2^26 Goldilocks, four-step, exchange fused into step A's pack (P2P stores)"}
+            except Exception as exc:
+                extra["config5_sixstep_distributed_peer"] = {"error": repr(exc)[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
