@@ -67,6 +67,13 @@ def _worker(rank, world, port, n, n1, q):
         n2 = n // n1
         x = np.random.default_rng(77).integers(0, GOLD, size=n, dtype=np.uint64)
         ds = DistributedSixStep(params, n, n1=n1, n2=n2, step_fns=make_cpu_steps(GOLD, 7, n, n1, n2))
+        for bad in ({"exchange": "bogus"}, {"exchange": "peer", "step_fns": make_cpu_steps(GOLD, 7, n, n1, n2)}):
+            try:
+                DistributedSixStep(params, n, n1=n1, n2=n2, **bad)
+            except ValueError:
+                pass
+            else:
+                raise AssertionError(f"accepted {bad}")
         slab = torch.from_numpy(column_slab(x, rank, world, n1, n2).view(np.int64))
         out_local = ds.run(slab)
         q.put((rank, out_local.numpy().view(np.uint64).copy()))
