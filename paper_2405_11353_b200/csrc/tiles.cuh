@@ -36,7 +36,10 @@ namespace ftile {
 #ifndef NTT_TILE_E32_K10
 #define NTT_TILE_E32_K10 14
 #endif
-constexpr int tile_e_rt(int word, int K) { return word == 4 ? (K == 10 ? NTT_TILE_E32_K10 : 13) : 12; }
+#ifndef NTT_TILE_E64
+#define NTT_TILE_E64 12
+#endif
+constexpr int tile_e_rt(int word, int K) { return word == 4 ? (K == 10 ? NTT_TILE_E32_K10 : 13) : NTT_TILE_E64; }
 template <class T, int K>
 constexpr int tile_e() { return tile_e_rt((int)sizeof(T), K); }
 template <class T, int K>
@@ -318,7 +321,14 @@ cudaError_t run_sixstep_tiles_k(const MultipassReq& r) {
 // Each length-2^b step is one pass (b <= 9) or two (b = 12, 13: 6+6, 7+6).
 inline int cols_split(int b, int* K) {
     if (b >= 6 && b <= 9) { K[0] = b; return 1; }
-    if (b == 12 || b == 13) { K[0] = b - 6; K[1] = 6; return 2; }
+#ifndef NTT_COLS_SPLIT_SWAP
+#define NTT_COLS_SPLIT_SWAP 0
+#endif
+    if (b == 12 || b == 13) {
+        K[0] = NTT_COLS_SPLIT_SWAP ? 6 : b - 6;
+        K[1] = NTT_COLS_SPLIT_SWAP ? b - 6 : 6;
+        return 2;
+    }
     return 0;
 }
 
