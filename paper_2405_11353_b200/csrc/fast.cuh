@@ -24,6 +24,9 @@
 #include "engine.cuh"
 #include "lazy.cuh"
 
+#ifndef NTT_FAST_TABLE_TMA
+#define NTT_FAST_TABLE_TMA 0
+#endif
 #ifndef NTT_FAST_TRIGGER_FIRST
 #define NTT_FAST_TRIGGER_FIRST 1
 #endif
@@ -323,6 +326,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     constexpr int NSTG = STG_ ? ((DS || PW) ? 2 : 1) : 0;
     static_assert(!PW || (STG_ && !DS), "pointwise-fused kernels stage both operands");
     __shared__ uint64_t mbar[TEAMS * 2];
+    __shared__ uint64_t tbar;              // NTT_FAST_TABLE_TMA: the stage table's bulk copy
 
     Tw* stw = reinterpret_cast<Tw*>(smem_raw);
     const int team = threadIdx.x / TT;
@@ -334,8 +338,17 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     A ar;
     ar.init(a.p);
 
-    // twiddle table once per CTA; barriers
-    for (int i = threadIdx.x; i < N; i += blockDim.x) stw[i] = a.stw[i];
+    // twiddle table once per CTA (one bulk async copy, or a thread loop); barriers
+    if constexpr (NTT_FAST_TABLE_TMA) {
+        if (threadIdx.x == 0) {
+            mbar_init(&tbar, 1);
+            fence_mbar_init();
+            mbar_expect_tx(&tbar, (uint32_t)(N * sizeof(Tw)));
+            tma_load_1d(stw, a.stw, (uint32_t)(N * sizeof(Tw)), &tbar);
+        }
+    } else {
+        for (int i = threadIdx.x; i < N; i += blockDim.x) stw[i] = a.stw[i];
+    }
     if (t == 0) { mbar_init(&mbar[2 * team], 1); mbar_init(&mbar[2 * team + 1], 1); }
     fence_mbar_init();
     __syncthreads();
@@ -365,6 +378,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
             tma_load_1d(S + N, a.in + (poly + stride) * N, bytes, &mbar[2 * team + 1]);
         }
     }
+    if constexpr (NTT_FAST_TABLE_TMA) mbar_wait(&tbar, 0);   // the table has landed
     uint32_t it = 0;
     int copies = 0;
     const int bar_id = 1 + team;
