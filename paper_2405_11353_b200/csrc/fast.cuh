@@ -24,6 +24,9 @@
 #include "engine.cuh"
 #include "lazy.cuh"
 
+#ifndef NTT_FAST_DS_LATE
+#define NTT_FAST_DS_LATE 0
+#endif
 #ifndef NTT_FAST_TABLE_TMA
 #define NTT_FAST_TABLE_TMA 0
 #endif
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
         mbar_expect_tx(&mbar[2 * team], PW ? 2 * bytes : bytes);
         tma_load_1d(S, a.in + poly * N, bytes, &mbar[2 * team]);
         if (PW) tma_load_1d(S + N, a.in2 + poly * N, bytes, &mbar[2 * team]);
-        if (DS && poly + stride < a.batch) {
+        if (DS && !NTT_FAST_DS_LATE && poly + stride < a.batch) {
             mbar_expect_tx(&mbar[2 * team + 1], bytes);
             tma_load_1d(S + N, a.in + (poly + stride) * N, bytes, &mbar[2 * team + 1]);
         }
@@ -387,6 +390,14 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
         T v[RV];
         const uint32_t sb_ = DS ? (it & 1) : 0;     // staging buffer of this polynomial
         if (STG_) mbar_wait(&mbar[2 * team + sb_], DS ? ((it >> 1) & 1) : (it & 1));
+        if constexpr (DS && NTT_FAST_DS_LATE) {
+            // the second polynomial's copy starts once the first has landed, so
+            // the first round's loads do not share HBM with the second round's
+            if (it == 0 && t == 0 && poly + stride < a.batch) {
+                mbar_expect_tx(&mbar[2 * team + 1], bytes);
+                tma_load_1d(S + N, a.in + (poly + stride) * N, bytes, &mbar[2 * team + 1]);
+            }
+        }
         ++it;
         T* Sb = S + sb_ * N;
         const T* S0 = STG_ ? Sb : a.in + poly * N;   // first-group source
