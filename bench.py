@@ -146,8 +146,9 @@ def run_reference(args, rank: int, world: int) -> None:
         cpu_oracle_rate(w, args.variant, 0.2)
     sample = ""
     cores = 1
+    per_step = max(0.05, min(0.5, 60.0 / max(1, args.steps)))   # whole run ~1 min of CPU work
     for _ in range(args.steps):
-        r, cores, sample = cpu_oracle_rate(w, args.variant, 0.5)
+        r, cores, sample = cpu_oracle_rate(w, args.variant, per_step, 1024 if args.steps > 100 else None)
         rates.append(r)
     val = float(np.median(rates))
     line = {
@@ -166,7 +167,7 @@ def run_reference(args, rank: int, world: int) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--variant", default="pease_nc")
