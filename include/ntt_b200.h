@@ -70,7 +70,10 @@ int ntt_root_of_unity(uint64_t p, uint64_t g, uint64_t n, uint64_t* omega_out);
 /* build_table -- twiddle.py:57-88, computed natively on the host:
  * w_pow[i] = omega^i, w_shoup[i] = floor(w_pow[i] * 2^w / p), i < n;
  * for INVERSE also n_inv = n^(p-2) and its Shoup word.  Bit-identical to
- * the reference tables.  Arrays hold n uint64 entries each. */
+ * the reference tables.  Arrays hold n uint64 entries each.  For w > 64
+ * (accepted, like the reference, whenever p < 2^w) the Shoup words do not
+ * fit 64 bits: w_shoup / n_inv_shoup are written as 0 and the caller derives
+ * them (the device arithmetic never uses the plan's w). */
 int ntt_table_build(uint64_t p, uint64_t g, int w_bits, uint64_t n, int direction,
                     uint64_t* w_pow, uint64_t* w_shoup, uint64_t* n_inv, uint64_t* n_inv_shoup);
 
@@ -109,6 +112,17 @@ int ntt_exec(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t batch, uns
  * directions overlap the transforms (use pinned host memory for overlap). */
 int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch, unsigned flags,
                   void* stream);
+
+/* Batch scheduler over several devices -- the reference's batch path
+ * (NttTransform._apply, estimator.py:61-65: one transform per row, "may run
+ * fully in parallel") sharded with NO collective
+ * (SURVEY.md sec.8e row 1): plans[i] (one plan per device, all of the same
+ * field / size / variant / direction) transforms the contiguous row block
+ * [batch*i/nplans, batch*(i+1)/nplans) of the HOST batch, every device's
+ * copy-in / transform / copy-out pipeline running concurrently.  Synchronous
+ * (returns when every row is back in h_out).  Flags: NTT_FLAG_SCALE. */
+int ntt_exec_host_sharded(const ntt_plan_t* plans, int nplans, const void* h_in, void* h_out, uint64_t batch,
+                          unsigned flags);
 
 /* Bytes of device scratch ntt_exec needs for `batch` rows (0 for
  * shared-memory-resident plans); the library allocates and caches it. */

@@ -40,7 +40,7 @@ NTT_FLAG_HOST_ASYNC = 2
 # every symbol include/ntt_b200.h declares
 EXPORTS = (
     "ntt_field_check", "ntt_find_primitive_root", "ntt_root_of_unity", "ntt_table_build",
-    "ntt_plan_create", "ntt_plan_destroy", "ntt_plan_info", "ntt_exec", "ntt_exec_host",
+    "ntt_plan_create", "ntt_plan_destroy", "ntt_plan_info", "ntt_exec", "ntt_exec_host", "ntt_exec_host_sharded",
     "ntt_plan_workspace_bytes", "ntt_pointwise_mul", "ntt_exec_pointwise_inverse", "ntt_sixstep_dist_step", "ntt_sixstep_dist_step_a_peer", "ntt_counters_enable", "ntt_counters_read",
     "ntt_counters_reset", "ntt_last_error", "ntt_abi_version", "ntt_device_count",
 )
@@ -93,6 +93,7 @@ def load():
         L.ntt_plan_info.argtypes = [_vp, ctypes.POINTER(PlanInfo)]
         L.ntt_exec.argtypes = [_vp, _vp, _vp, _u64, ctypes.c_uint, _vp]
         L.ntt_exec_host.argtypes = [_vp, _vp, _vp, _u64, ctypes.c_uint, _vp]
+        L.ntt_exec_host_sharded.argtypes = [ctypes.POINTER(_vp), _int, _vp, _vp, _u64, ctypes.c_uint]
         L.ntt_plan_workspace_bytes.argtypes = [_vp, _u64]
         L.ntt_plan_workspace_bytes.restype = _u64
         L.ntt_pointwise_mul.argtypes = [_vp, _vp, _vp, _vp, _u64, _vp]
@@ -167,6 +168,8 @@ class DevicePlan:
     def sixstep_dist_step_a_peer(self, rank: int, world: int, in_ptr: int, peer_recv_ptrs, stream: int) -> None:
         """Step A with the exchange fused into its pack: block h is stored into
         peer_recv_ptrs[h] (rank h's receive buffer, mapped here) at slot `rank`."""
+        if len(peer_recv_ptrs) != world:
+            raise ValueError(f"need one receive buffer per rank: {len(peer_recv_ptrs)} != world {world}")
         arr = (_vp * len(peer_recv_ptrs))(*[int(p) for p in peer_recv_ptrs])
         check(load().ntt_sixstep_dist_step_a_peer(self._h, rank, world, in_ptr, arr, stream))
 
@@ -178,6 +181,13 @@ class DevicePlan:
         if h is not None and _lib is not None:
             _lib.ntt_plan_destroy(h)
             self._h = None
+
+
+def exec_host_sharded(plans, in_ptr: int, out_ptr: int, batch: int, scale: bool) -> None:
+    """One host batch split in contiguous row blocks over `plans` (one per
+    device), every device's pipeline concurrent, no collective."""
+    arr = (_vp * len(plans))(*[p.handle.value for p in plans])
+    check(load().ntt_exec_host_sharded(arr, len(plans), in_ptr, out_ptr, batch, NTT_FLAG_SCALE if scale else 0))
 
 
 def counters_enable(on: bool = True) -> None:

@@ -12,7 +12,12 @@ Inputs may be what the reference takes (a list of ints; a list comes back) or
 batched arrays: a numpy array or a torch tensor of shape [..., N] (uint32 for
 p < 2^32, uint64 / int64 storage otherwise).  CUDA tensors stay on the device
 (stream-ordered on torch's current stream); host inputs are copied in, every
-row is transformed in ONE device call, and copied back.  Every variant runs
+row is transformed in ONE device call, and copied back.  ``ntt`` / ``intt`` /
+``run_plan`` also take ``devices=[...]``: a host batch is then split in
+contiguous row blocks across those GPUs (one plan per device, every device's
+copy-in / transform / copy-out concurrent, no collective; C ABI
+``ntt_exec_host_sharded``) -- the reference's per-row batch loop
+(estimator.py:61-65) sharded as SURVEY.md sec.8e prescribes.  Every variant runs
 its own dataflow on the GPU (see csrc/engine.cuh); there is no CPU fallback.
 """
 
@@ -79,9 +84,20 @@ def _current_device() -> int:
     return 0
 
 
+def _check_devices(devices):
+    if devices is None:
+        return None
+    devs = [int(d) for d in devices]
+    if not devs or len(set(devs)) != len(devs):
+        raise ValueError("devices must list distinct CUDA device ordinals")
+    return devs
+
+
 def _execute(x, params: FieldParams, n: int, variant: str, direction: str, scale: bool,
-             n1=None, n2=None):
-    """Run one plan over every row of x; returns the same container kind."""
+             n1=None, n2=None, devices=None):
+    """Run one plan over every row of x; returns the same container kind.
+    devices: host batches are sharded by rows over these GPUs (a CUDA tensor
+    always runs on its own device)."""
     if torch is not None and isinstance(x, torch.Tensor):
         if x.shape[-1] != n:
             raise SizeMismatch(f"vector length {x.shape[-1]} != table size {n}")
@@ -101,7 +117,7 @@ def _execute(x, params: FieldParams, n: int, variant: str, direction: str, scale
             stream = torch.cuda.current_stream(x.device).cuda_stream
             dp.exec_device(src.data_ptr(), out.data_ptr(), rows, scale, stream)
             return out
-        arr = _execute(x.contiguous().numpy(), params, n, variant, direction, scale, n1, n2)
+        arr = _execute(x.contiguous().numpy(), params, n, variant, direction, scale, n1, n2, devices)
         return torch.from_numpy(arr)
     if isinstance(x, np.ndarray):
         if x.ndim == 0 or x.shape[-1] != n:
@@ -120,7 +136,13 @@ def _execute(x, params: FieldParams, n: int, variant: str, direction: str, scale
         src = np.ascontiguousarray(x)
         out = np.empty_like(src)
         rows = src.size // n
-        dp = _device_plan(params, n, variant, direction, n1, n2, word, _current_device())
+        devs = _check_devices(devices)
+        if devs is not None and len(devs) > 1:
+            plans = [_device_plan(params, n, variant, direction, n1, n2, word, d) for d in devs]
+            _lib.exec_host_sharded(plans, src.ctypes.data, out.ctypes.data, rows, scale)
+            return out
+        dev = devs[0] if devs else _current_device()
+        dp = _device_plan(params, n, variant, direction, n1, n2, word, dev)
         dp.exec_host(src.ctypes.data, out.ctypes.data, rows, scale)
         return out
     # list / sequence of ints: the reference's own calling convention
@@ -131,7 +153,7 @@ def _execute(x, params: FieldParams, n: int, variant: str, direction: str, scale
         return [int(v) for v in x]
     dt = np.uint32 if _default_word(params.p) == 4 else np.uint64
     arr = np.fromiter((int(v) for v in x), dtype=np.uint64, count=n).astype(dt)
-    return [int(v) for v in _execute(arr, params, n, variant, direction, scale, n1, n2)]
+    return [int(v) for v in _execute(arr, params, n, variant, direction, scale, n1, n2, devices)]
 
 
 # ----------------------------------------------------------- public API ----
@@ -228,11 +250,22 @@ def ntt_sixstep(x, plan: NttPlan):
     return _execute(x, plan.table.params, plan.N, "sixstep", plan.direction, False, plan.n1, plan.n2)
 
 
-def ntt(x, table: TwiddleTable, variant: str = "dit"):
+def ntt(x, table: TwiddleTable, variant: str = "dit", devices=None):
     """Forward transform by the chosen variant (algorithms.py:402-412).
 
     As in the reference, the table's direction is honoured: an inverse table
-    gives the unscaled inverse transform."""
+    gives the unscaled inverse transform.  devices: shard a host batch by rows
+    over these GPUs (module docstring)."""
+    if devices is not None:
+        if variant not in VARIANTS:
+            raise UnsupportedVariant(f"unknown variant {variant!r}")
+        n1 = n2 = None
+        if variant == "sixstep":
+            plan = make_plan(table.params, "sixstep", table.N, table.direction)
+            n1, n2 = plan.n1, plan.n2
+        elif variant != "naive":
+            _log2(table.N)
+        return _execute(x, table.params, table.N, variant, table.direction, False, n1, n2, devices)
     if variant == "naive":
         return naive_dft(x, table)
     if variant == "sixstep":
@@ -243,9 +276,9 @@ def ntt(x, table: TwiddleTable, variant: str = "dit"):
     return _VARIANT_FUNCS[variant](x, table)
 
 
-def intt(x, table: TwiddleTable, variant: str = "dit"):
+def intt(x, table: TwiddleTable, variant: str = "dit", devices=None):
     """Inverse transform: the variant with inverse twiddles, n_inv fused into
-    the last store (algorithms.py:415-423)."""
+    the last store (algorithms.py:415-423).  devices: as for ``ntt``."""
     if table.direction != INVERSE:
         raise ValueError("intt requires an inverse-direction table")
     if variant not in VARIANTS:
@@ -256,23 +289,26 @@ def intt(x, table: TwiddleTable, variant: str = "dit"):
         n1, n2 = plan.n1, plan.n2
     elif variant != "naive":
         _log2(table.N)
-    return _execute(x, table.params, table.N, variant, INVERSE, True, n1, n2)
+    return _execute(x, table.params, table.N, variant, INVERSE, True, n1, n2, devices)
 
 
-def run_plan(plan: NttPlan, x):
-    """Forward plans return the NTT, inverse plans the INTT (algorithms.py:426-434)."""
+def run_plan(plan: NttPlan, x, devices=None):
+    """Forward plans return the NTT, inverse plans the INTT (algorithms.py:426-434).
+    devices: as for ``ntt``."""
     m = x.shape[-1] if hasattr(x, "shape") else len(x)
     if m != plan.N:
         raise SizeMismatch(f"vector length {m} != plan size {plan.N}")
     if plan.direction == FORWARD:
         if plan.variant == "sixstep":
+            if devices is not None:
+                return _execute(x, plan.table.params, plan.N, "sixstep", FORWARD, False, plan.n1, plan.n2, devices)
             return ntt_sixstep(x, plan)
-        return ntt(x, plan.table, plan.variant)
+        return ntt(x, plan.table, plan.variant, devices=devices)
     if plan.variant == "sixstep":
         # keep the plan's own split (the reference rebuilds the default one;
         # the output is identical either way)
-        return _execute(x, plan.table.params, plan.N, "sixstep", INVERSE, True, plan.n1, plan.n2)
-    return intt(x, plan.table, plan.variant)
+        return _execute(x, plan.table.params, plan.N, "sixstep", INVERSE, True, plan.n1, plan.n2, devices)
+    return intt(x, plan.table, plan.variant, devices=devices)
 
 
 _VARIANT_FUNCS = {

@@ -76,3 +76,19 @@ def seeded_input(w: Workload, rows: int | None = None) -> np.ndarray:
     b = w.batch if rows is None else rows
     x = np.random.default_rng(w.seed).integers(0, w.p, size=(b, w.n), dtype=np.uint64)
     return x.astype(np.uint32) if w.word == 4 else x
+
+
+def seeded_rows(w: Workload, lo: int, hi: int, chunk: int = 1024) -> np.ndarray:
+    """Rows [lo, hi) of the seeded stream of ``seeded_input`` -- for a batch of
+    any size (the stream is shape-independent), so rank r of a weak-scaling run
+    transforms rows [r*B, (r+1)*B) of ONE global seeded batch and rank 0's rows
+    are exactly the config's own input.  Rows before `lo` are drawn and
+    discarded in chunks (bounded memory)."""
+    rng = np.random.default_rng(w.seed)
+    skip = lo
+    while skip:
+        k = min(chunk, skip)
+        rng.integers(0, w.p, size=(k, w.n), dtype=np.uint64)
+        skip -= k
+    x = rng.integers(0, w.p, size=(hi - lo, w.n), dtype=np.uint64)
+    return x.astype(np.uint32) if w.word == 4 else x

@@ -99,8 +99,10 @@ bool is_generator(uint64_t g, uint64_t p, const std::vector<uint64_t>& fac) {
 
 int check_field(uint64_t p, uint64_t g, int w) {
     if (!is_prime(p)) return fail(NTT_E_NOT_PRIME, std::to_string(p) + " is not prime");
-    if (w < 2 || w > 64) return fail(NTT_E_INVALID, "word width w must be in [2, 64]");
-    if (p == 2 || (w < 64 && p >= (1ull << w)))
+    // modmath.py:95-96: any width with p < 2^w (w > 64 only changes the host
+    // table's Shoup words; the device arithmetic has its own word)
+    if (w > 4096) return fail(NTT_E_INVALID, "word width w is unreasonably large");
+    if (p == 2 || w < 1 || (w < 64 && p >= (1ull << w)))
         return fail(NTT_E_INVALID, "p must be odd and fit in " + std::to_string(w) + " bits");
     if (!(2 <= g && g < p)) return fail(NTT_E_INVALID, "generator out of range");
     if (!is_generator(g, p, prime_factors(p - 1)))
@@ -245,8 +247,14 @@ struct ntt_plan_s {
     // concurrently on several streams (each stream's passes are stream-ordered)
     std::map<cudaStream_t, std::pair<void*, uint64_t>> ws;
     std::map<cudaStream_t, std::pair<void*, uint64_t>> pw_ws;   // unfused pointwise-inverse products
+    // two device buffer sets at FIXED offsets set * hset_bytes (a set never
+    // moves while a call that uses it may be in flight); last_chunks / last_bytes
+    // remember the chunking of the previous call on each set
     void* hbuf = nullptr;
     uint64_t hbuf_bytes = 0;
+    uint64_t hset_bytes = 0;
+    uint64_t last_chunks[2] = {0, 0};
+    uint64_t last_bytes[2] = {0, 0};
     // host-exec pipeline: hs[0] H2D copies, hs[1] transforms, hs[2] D2H copies,
     // chained per chunk by events (kMaxChunks x {copied-in, transformed})
     static constexpr int kMaxChunks = 64;
@@ -371,11 +379,12 @@ int ntt_table_build(uint64_t p, uint64_t g, int w_bits, uint64_t n, int directio
     std::vector<uint64_t> wp;
     host_powers(p, omega, n, wp);
     memcpy(w_pow, wp.data(), n * 8);
-    for (uint64_t i = 0; i < n; ++i) w_shoup[i] = shoup_word(wp[i], p, w_bits);
+    // (w > 64: the Shoup words do not fit the u64 output; the host computes them)
+    for (uint64_t i = 0; i < n; ++i) w_shoup[i] = w_bits <= 64 ? shoup_word(wp[i], p, w_bits) : 0;
     if (direction == NTT_INVERSE) {
         uint64_t ni = powmod(n % p, p - 2, p);
         if (n_inv) *n_inv = ni;
-        if (n_inv_shoup) *n_inv_shoup = shoup_word(ni, p, w_bits);
+        if (n_inv_shoup) *n_inv_shoup = w_bits <= 64 ? shoup_word(ni, p, w_bits) : 0;
     }
     return NTT_OK;
 }
@@ -492,7 +501,7 @@ int ntt_plan_info(ntt_plan_t plan, ntt_plan_info_t* info) {
     if (plan->variant == NTT_SIXSTEP) info->passes = 2;
     else info->passes = mp_num_passes(plan->L, plan->word, plan->variant, plan->p);
     info->n_inv = plan->table->n_inv;
-    info->n_inv_shoup = plan->dir == NTT_INVERSE ? shoup_word(plan->table->n_inv, plan->p, plan->w) : 0;
+    info->n_inv_shoup = plan->dir == NTT_INVERSE && plan->w <= 64 ? shoup_word(plan->table->n_inv, plan->p, plan->w) : 0;
     info->device_table_bytes = plan->table->bytes + (plan->table1 ? plan->table1->bytes : 0) +
                                (plan->table2 ? plan->table2->bytes : 0);
     return NTT_OK;
@@ -582,11 +591,13 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     const int set = async ? (int)(plan->host_seq++ & 1) : 0;
     {
         std::lock_guard<std::mutex> lk(plan->mu);
-        const uint64_t need = (async ? 2 : 1) * bytes;
-        if (need > plan->hbuf_bytes)       // reallocation: earlier asynchronous calls must be done with it
+        if (bytes > plan->hset_bytes) {    // reallocation: earlier asynchronous calls must be done with it
             for (auto hs : plan->hs)
                 if (hs) cudaStreamSynchronize(hs);
-        st = grow(plan->hbuf, plan->hbuf_bytes, need);
+            st = grow(plan->hbuf, plan->hbuf_bytes, 2 * bytes);
+            plan->hset_bytes = st ? 0 : bytes;
+            plan->last_chunks[0] = plan->last_chunks[1] = 0;
+        }
         for (auto& hs : plan->hs)
             if (!st && !hs && cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking) != cudaSuccess)
                 st = fail(NTT_E_CUDA, "stream creation failed");
@@ -626,10 +637,19 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     if (resident && env_chunks > 0) chunks = (uint64_t)env_chunks;     // tuning knob (tools/e2e_sweep.py)
     if (chunks > (uint64_t)ntt_plan_s::kMaxChunks) chunks = ntt_plan_s::kMaxChunks;
     if (chunks > batch) chunks = batch;
-    char* d = static_cast<char*>(plan->hbuf) + (size_t)set * bytes;
+    char* d = static_cast<char*>(plan->hbuf) + (size_t)set * plan->hset_bytes;
     cudaStream_t sH = plan->hs[0], sC = plan->hs[1], sD = plan->hs[2];
     cudaStream_t user = static_cast<cudaStream_t>(stream);
     cudaEvent_t* hout = plan->hout + set * ntt_plan_s::kMaxChunks;
+    // chunk c of this call overwrites exactly chunk c of the previous call on
+    // this set only if both calls cut the same bytes into the same chunks;
+    // otherwise the first copy-in waits for EVERY copy-out of that call
+    const bool same_cut = plan->last_chunks[set] == chunks && plan->last_bytes[set] == bytes;
+    if (!st && !same_cut)
+        for (uint64_t c = 0; c < plan->last_chunks[set]; ++c)
+            if ((e = cudaStreamWaitEvent(sH, hout[c], 0)) != cudaSuccess) { st = cuda_fail(e, "stream wait"); break; }
+    plan->last_chunks[set] = chunks;
+    plan->last_bytes[set] = bytes;
     // (no wait on `stream` at the start: it carries the previous asynchronous
     // call's completion, and waiting for it would serialise the calls -- h_in
     // must be ready on the host when the call is made)
@@ -680,6 +700,51 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
         if (!st && e2 != cudaSuccess) st = cuda_fail(e2, "host exec");
     }
     if (cur != plan->device) cudaSetDevice(cur);
+    return st;
+}
+
+int ntt_exec_host_sharded(const ntt_plan_t* plans, int nplans, const void* h_in, void* h_out, uint64_t batch,
+                          unsigned flags) {
+    if (!plans || nplans < 1) return fail(NTT_E_INVALID, "plans must hold at least one plan");
+    for (int i = 0; i < nplans; ++i) {
+        if (!plans[i]) return fail(NTT_E_INVALID, "NULL plan in the shard list");
+        const ntt_plan_s& a = *plans[0];
+        const ntt_plan_s& b = *plans[i];
+        if (a.p != b.p || a.g != b.g || a.n != b.n || a.variant != b.variant || a.dir != b.dir ||
+            a.word != b.word || a.n1 != b.n1 || a.n2 != b.n2)
+            return fail(NTT_E_INVALID, "sharded plans must share field, size, variant, direction and word");
+        for (int j = 0; j < i; ++j)
+            if (plans[j] == plans[i] || plans[j]->device == plans[i]->device)
+                return fail(NTT_E_INVALID, "one plan per device");
+    }
+    if (batch == 0) return NTT_OK;
+    if (!h_in || !h_out) return fail(NTT_E_INVALID, "NULL buffer");
+    const uint64_t row_bytes = plans[0]->n * plans[0]->word;
+    // enqueue every device's pipeline first (each call returns once its copies
+    // and transforms are queued), then wait for all of them
+    int st = NTT_OK;
+    int queued = 0;
+    for (int i = 0; i < nplans && !st; ++i, ++queued) {
+        const uint64_t lo = batch * i / nplans, hi = batch * (i + 1) / nplans;
+        if (hi == lo) continue;
+        st = ntt_exec_host(plans[i], static_cast<const char*>(h_in) + lo * row_bytes,
+                           static_cast<char*>(h_out) + lo * row_bytes, hi - lo,
+                           (flags & NTT_FLAG_SCALE) | NTT_FLAG_HOST_ASYNC, nullptr);
+    }
+    const std::string err = st ? g_last_error : std::string();
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (int i = 0; i < queued; ++i) {
+        cudaSetDevice(plans[i]->device);
+        std::lock_guard<std::mutex> lk(plans[i]->host_mu);
+        for (auto hs : plans[i]->hs) {
+            if (!hs) continue;
+            cudaError_t e = cudaStreamSynchronize(hs);
+            if (!st && e != cudaSuccess) st = cuda_fail(e, "sharded host exec");
+        }
+    }
+    cudaSetDevice(cur);
+    if (!err.empty()) g_last_error = err;
     return st;
 }
 

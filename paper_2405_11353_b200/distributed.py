@@ -1,8 +1,11 @@
 """Multi-GPU execution.
 
 * Batches (independent polynomials) shard by rows with NO collective:
-  :func:`shard_rows` gives each rank its contiguous row block; every rank runs
-  the ordinary batched transform on its own GPU.
+  :func:`shard_rows` gives each rank its contiguous row block and
+  :class:`BatchShard` runs the ordinary batched transform of that block on the
+  rank's own GPU (one process per GPU); within ONE process, ``ntt(x_host,
+  table, variant, devices=[...])`` splits a host batch over several GPUs
+  (C ABI ``ntt_exec_host_sharded``).
 * One giant transform (config 5: 2^26 Goldilocks) is split four-step across
   ranks with exactly ONE exchange: :class:`DistributedSixStep`.  The reference's
   six-step indexing (algorithms.py:355-389) is kept: the input is the n2 x n1
@@ -46,6 +49,66 @@ def shard_rows(batch: int, rank: int, world: int) -> tuple[int, int]:
     lo = batch * rank // world
     hi = batch * (rank + 1) // world
     return lo, hi
+
+
+class BatchShard:
+    """This rank's contiguous row block of a batch sharded over a process group
+    (independent polynomials, NO collective on the data
+    path).  ``transform`` runs the ordinary batched transform of the block on
+    this rank's device (``ntt`` / ``intt`` of algorithms.py, or an injected
+    function for CPU tests); ``gather`` collects every rank's output rows in
+    rank order for verification only (outside any timed region)."""
+
+    def __init__(self, batch: int, group=None):
+        if dist is None or not dist.is_initialized():
+            raise RuntimeError("torch.distributed must be initialised (one process per GPU)")
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.batch = batch
+        self.lo, self.hi = shard_rows(batch, self.rank, self.world)
+        self.blocks = [shard_rows(batch, r, self.world) for r in range(self.world)]
+
+    @property
+    def rows(self) -> int:
+        return self.hi - self.lo
+
+    def local(self, x_global):
+        """This rank's rows of a global batch [batch, N] (host array or tensor)."""
+        if x_global.shape[0] != self.batch:
+            raise ValueError(f"global batch has {x_global.shape[0]} rows, expected {self.batch}")
+        return x_global[self.lo:self.hi]
+
+    def transform(self, x_local, table, variant: str = "dit", inverse: bool = False, fn=None):
+        """Transform this rank's rows: ntt (or intt) on this rank's device."""
+        if fn is not None:
+            return fn(x_local, table, variant)
+        from .algorithms import intt, ntt
+        return (intt if inverse else ntt)(x_local, table, variant)
+
+    def gather(self, y_local, dst: int = 0):
+        """Every rank's output rows, in rank order, on rank `dst` (None elsewhere).
+        Uneven blocks are padded to the largest block for the collective."""
+        y = torch.as_tensor(y_local)
+        n = y.shape[-1]
+        maxr = max(hi - lo for lo, hi in self.blocks)
+        raw = y.reshape(-1, n)
+        view = {torch.uint64: torch.int64, torch.uint32: torch.int32}.get(raw.dtype)
+        raw = raw.view(view) if view is not None else raw
+        pad = torch.zeros((maxr, n), dtype=raw.dtype, device=raw.device)
+        pad[: raw.shape[0]] = raw
+        outs = [torch.empty_like(pad) for _ in range(self.world)] if self.rank == dst else None
+        if dist.get_backend(self.group) == "nccl":
+            full = torch.empty((self.world * maxr, n), dtype=pad.dtype, device=pad.device)
+            dist.all_gather_into_tensor(full, pad, group=self.group)
+            outs = list(full.split(maxr)) if self.rank == dst else None
+        else:
+            dist.gather(pad, outs, dst=dst, group=self.group)
+        if self.rank != dst:
+            return None
+        rows = [o[: hi - lo] for o, (lo, hi) in zip(outs, self.blocks)]
+        full = torch.cat(rows)
+        return full.view(y.dtype) if view is not None else full
 
 
 def column_slab(x: np.ndarray, rank: int, world: int, n1: int, n2: int) -> np.ndarray:
@@ -103,16 +166,30 @@ class DistributedSixStep:
     def local_input_shape(self) -> tuple[int, int]:
         return (self.n2, self.cols)
 
-    def run(self, x_local, timings: dict | None = None):
+    def _exchange_buffers(self, like):
+        """send / recv of the all-to-all, allocated once per (dtype, device)."""
+        key = (like.dtype, like.device)
+        if getattr(self, "_bufs_key", None) != key:
+            send = torch.empty(self.world * self.block, dtype=like.dtype, device=like.device)
+            self._bufs = (send, torch.empty_like(send))
+            self._bufs_key = key
+        return self._bufs
+
+    def run(self, x_local, out=None):
         """x_local: this rank's slab [n2, n1/G] (device tensor for the GPU
-        path).  Returns out_local [n1, n2/G]."""
+        path).  Returns out_local [n1, n2/G] (written into `out` when given;
+        the exchange buffers are allocated once and reused)."""
         if tuple(x_local.shape) != (self.n2, self.cols):
             raise ValueError(f"local slab must be {(self.n2, self.cols)}, got {tuple(x_local.shape)}")
-        out_local = torch.empty((self.n1, self.kcols), dtype=x_local.dtype, device=x_local.device)
+        if out is None:
+            out_local = torch.empty((self.n1, self.kcols), dtype=x_local.dtype, device=x_local.device)
+        else:
+            if tuple(out.shape) != (self.n1, self.kcols) or out.dtype != x_local.dtype or not out.is_contiguous():
+                raise ValueError(f"out must be a contiguous {(self.n1, self.kcols)} tensor of {x_local.dtype}")
+            out_local = out
         if self.exchange == "peer":
             return self._run_peer(x_local, out_local)
-        send = torch.empty(self.world * self.block, dtype=x_local.dtype, device=x_local.device)
-        recv = torch.empty_like(send)
+        send, recv = self._exchange_buffers(x_local)
         self.step_a(x_local, send, self.rank, self.world)
         # ONE exchange: block h of `send` goes to rank h (equal splits)
         self._exchange(recv, send)

@@ -69,16 +69,23 @@ def cyclic_mul_ntt(a, b, params: FieldParams, variant: str = "dit"):
     if nb != n:
         raise SizeMismatch(f"operand lengths differ: {n} vs {nb}")
     fwd = build_table(params, n, FORWARD)
-    inv = build_table(params, n, INVERSE)
+    build_table(params, n, INVERSE)
     word = 4 if params.p < (1 << 32) else 8
     if torch is not None and isinstance(a, torch.Tensor) and a.is_cuda:
+        wd = _alg._TORCH_WORD.get(a.dtype)
+        if wd is None:
+            raise TypeError(f"unsupported residue dtype {a.dtype}")
+        if n == 1:          # X^1 - 1: the product itself (no transform plan of size 1)
+            a64, b64 = a.to(torch.int64), b.to(a.device).to(torch.int64)
+            if params.p < (1 << 31):
+                return ((a64 * b64) % params.p).to(a.dtype)
+            host = [int(u) * int(v) % params.p for u, v in zip(a.cpu().view(-1).tolist(), b.cpu().view(-1).tolist())]
+            return torch.tensor(host, dtype=torch.int64).view(a.shape).to(a.dtype).to(a.device)
         stacked = torch.stack([a.contiguous(), b.contiguous().to(a.dtype)])
         spec = _alg.ntt(stacked, fwd, variant)                 # one launch for both operands
-        if n == 1:
-            return pointwise_mul(spec[0], spec[1], params.p)
         # intt(spec_a .* spec_b) as one call (ntt_exec_pointwise_inverse: the
-        # product fused into the inverse's first group on resident u32 plans)
-        wd = 4 if spec.dtype == torch.uint32 else 8
+        # product fused into the inverse's first group on resident u32 plans);
+        # the plan's storage word is the tensors' (int32 / uint32 -> 4 bytes)
         dp = _alg._device_plan(params, n, variant, INVERSE, None, None, wd, spec.device.index)
         sa, sb = spec[0].contiguous(), spec[1].contiguous()
         out = torch.empty_like(sa)
@@ -86,6 +93,9 @@ def cyclic_mul_ntt(a, b, params: FieldParams, variant: str = "dit"):
         dp.pointwise_inverse(sa.data_ptr(), sb.data_ptr(), out.data_ptr(), rows,
                              torch.cuda.current_stream(spec.device).cuda_stream)
         return out
+    if n == 1:              # X^1 - 1: the product itself (no transform plan of size 1)
+        prod = [int(u) * int(v) % params.p for u, v in zip(a, b)]
+        return prod if is_list else np.asarray(prod, dtype=np.uint64).astype(np.asarray(a).dtype)
     if torch is None or not torch.cuda.is_available():
         # host inputs: the device does the work (no CPU fallback)
         raise_if_no_device()

@@ -43,6 +43,8 @@ class TwiddleTable:
             _lib.check(_lib.load().ntt_table_build(
                 self.params.p, self.params.g, self.params.w, self.N, int(self.direction == INVERSE),
                 wp.ctypes.data, ws.ctypes.data, ctypes.byref(ni), ctypes.byref(nis)))
+            if self.params.w > 64:      # Shoup words wider than the C ABI's u64 (modmath.py:129-132)
+                ws = np.array([(int(v) << self.params.w) // self.params.p for v in wp], dtype=object)
             self._arrays = (wp, ws)
         return self._arrays
 

@@ -115,3 +115,44 @@ def test_row_sharding_and_layout_helpers():
     outs = [np.arange(n1 * 2) + 100 * r for r in range(2)]
     full = assemble_output(outs, n1, n2).reshape(n1, n2)
     assert full[3, 1] == 3 * 2 + 1 and full[3, 2] == 100 + 3 * 2
+
+
+def _shard_worker(rank, world, port, batch, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        from paper_2405_11353_b200.distributed import BatchShard
+        p, n = 998244353, 64
+        x = np.random.default_rng(5).integers(0, p, size=(batch, n), dtype=np.uint64).astype(np.uint32)
+        sh = BatchShard(batch)
+        assert (sh.lo, sh.hi) == (batch * rank // world, batch * (rank + 1) // world)
+        mine = sh.local(x)
+        # the rank-local transform is injected (CPU oracle); on a B200 it is ntt() on the rank's GPU
+        y = sh.transform(mine, None, "pease_nc", fn=lambda v, _t, var: O.ntt(np.ascontiguousarray(v), p, 3, 32, var))
+        full = sh.gather(torch.from_numpy(y.view(np.int32)).view(torch.uint32))
+        q.put((rank, None if full is None else full.view(torch.int32).numpy().view(np.uint32).copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("batch", [8, 7])
+def test_batch_shard_gloo_world2(batch):
+    """Row sharding of one batch over 2 ranks, no collective on the data path;
+    the gathered rows equal the oracle's transform of the whole batch."""
+    from oracle import oracle as O
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, batch, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res[1] is None
+    x = np.random.default_rng(5).integers(0, 998244353, size=(batch, 64), dtype=np.uint64).astype(np.uint32)
+    assert np.array_equal(res[0], O.ntt(x, 998244353, 3, 32, "pease_nc"))

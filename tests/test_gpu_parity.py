@@ -612,3 +612,69 @@ def test_randomised_parity_sweep():
     res = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_parity.py"), "250", "3"],
                          capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+
+
+def test_host_async_varying_batch_sizes():
+    """NTT_FLAG_HOST_ASYNC with SHRINKING and growing batches between calls
+    (a set must not move while a call on it is in flight), then a
+    synchronous call: every output exact."""
+    w = CONFIGS[2]
+    params = P.FieldParams(w.p, w.g, w.w)
+    dp = P.algorithms.device_plan_for(P.make_plan(params, "dit", w.n), 4, 0)
+    st = torch.cuda.Stream()
+    sizes = [4096, 1024, 3000, 17, 4096, 2048]
+    xs = [rand(w.p, b, 12, np.uint32, 7300 + i) for i, b in enumerate(sizes)]
+    hin = [torch.from_numpy(x.view(np.int32)).pin_memory() for x in xs]
+    hout = [torch.empty_like(h).pin_memory() for h in hin]
+    for i, b in enumerate(sizes):
+        dp.exec_host(hin[i].data_ptr(), hout[i].data_ptr(), b, False, st.cuda_stream, True)
+    out = torch.empty_like(hin[2]).pin_memory()
+    dp.exec_host(hin[2].data_ptr(), out.data_ptr(), sizes[2], False)      # synchronous right after
+    st.synchronize()
+    for i in range(len(sizes)):
+        assert np.array_equal(hout[i].numpy().view(np.uint32), O.ntt(xs[i], w.p, w.g, 32, "dit")), i
+    assert np.array_equal(out.numpy(), hout[2].numpy())
+
+
+def test_sharded_host_api_one_device():
+    """ntt(x_host, table, variant, devices=[...]) / ntt_exec_host_sharded: the
+    batch scheduler over devices (one device here; the C ABI rejects duplicate
+    devices and mismatched plans)."""
+    w = CONFIGS[2]
+    params = P.FieldParams(w.p, w.g, w.w)
+    x = seeded_input(w)
+    table = P.build_table(params, w.n)
+    y = P.ntt(x, table, "pease_nc", devices=[0])
+    assert O.sha256_le(y) == GOLDEN[2][1]
+    assert np.array_equal(P.intt(y, P.build_table(params, w.n, P.INVERSE), "pease_nc", devices=[0]), x)
+    plan = P.algorithms.device_plan_for(P.make_plan(params, "dit", w.n), 4, 0)
+    out = np.empty_like(x)
+    from paper_2405_11353_b200 import _lib
+    _lib.exec_host_sharded([plan], x.ctypes.data, out.ctypes.data, w.batch, False)
+    assert O.sha256_le(out) == GOLDEN[2][1]
+    with pytest.raises(ValueError):
+        _lib.exec_host_sharded([plan, plan], x.ctypes.data, out.ctypes.data, w.batch, False)
+    other = P.algorithms.device_plan_for(P.make_plan(params, "dif", w.n), 4, 0)
+    with pytest.raises(ValueError):
+        _lib.exec_host_sharded([plan, other], x.ctypes.data, out.ctypes.data, w.batch, False)
+    with pytest.raises(ValueError):
+        P.ntt(x, table, "dit", devices=[0, 0])
+
+
+def test_polymul_int32_and_length_one():
+    """int32 device operands use a 4-byte inverse plan; n == 1 is the product."""
+    p = 998244353
+    params = P.FieldParams(p, 3)
+    A = rand(p, 4, 10, np.uint32, 11)
+    B = rand(p, 4, 10, np.uint32, 12)
+    ta = torch.from_numpy(A.view(np.int32)).cuda()
+    tb = torch.from_numpy(B.view(np.int32)).cuda()
+    C = P.cyclic_mul_ntt(ta, tb, params, "dit")
+    assert C.dtype == torch.int32
+    got = C.cpu().numpy().view(np.uint32)
+    for r in (0, 3):
+        assert got[r].tolist() == P.schoolbook_cyclic(A[r].tolist(), B[r].tolist(), p)
+    assert P.cyclic_mul_ntt([123456789], [987654321], params) == [123456789 * 987654321 % p]
+    t1 = P.cyclic_mul_ntt(torch.tensor([[5]], dtype=torch.int32).cuda(), torch.tensor([[7]], dtype=torch.int32).cuda(),
+                          params)
+    assert t1.cpu().tolist() == [[35]]

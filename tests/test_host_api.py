@@ -205,3 +205,15 @@ def test_cli_usage_errors():
     from paper_2405_11353_b200 import cli
     assert cli.main(["nonsense"]) == 2
     assert cli.bench_input(1024, 998244353, 42)[:2] == cli.bench_input(1024, 998244353, 42)[:2]
+
+
+def test_field_params_wide_word():
+    """FieldParams accepts any w with p < 2^w (modmath.py:95-96),
+    including w > 64; the table's Shoup words are floor(w * 2^w / p)."""
+    import paper_2405_11353_b200 as P
+    f = P.FieldParams(998244353, 3, 100)
+    t = P.build_table(f, 16, P.INVERSE)
+    assert t.w_shoup == [(v << 100) // 998244353 for v in t.w_pow]
+    assert t.n_inv_shoup == (t.n_inv << 100) // 998244353
+    with pytest.raises(ValueError):
+        P.FieldParams(998244353, 3, 29)
