@@ -68,11 +68,7 @@ NTT_D void mbar_wait(uint64_t* bar, uint32_t phase) {
 NTT_D void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 NTT_D void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// launch with the PDL attribute (NTT_PDL=0 in the environment: plain launch)
-inline bool pdl_enabled() {
-    static const bool on = [] { const char* e = getenv("NTT_PDL"); return !(e && e[0] == '0'); }();
-    return on;
-}
+// launch with the programmatic-stream-serialization (PDL) attribute
 template <class... KArgs, class... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
@@ -84,7 +80,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

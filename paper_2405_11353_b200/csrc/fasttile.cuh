@@ -72,7 +72,6 @@ struct TileArgs {
     const Tw* tw_lo;           // w^j, j < 2^th          (the plan's main table prefix)
     const Tw* tw_hi;           // w^(j*2^th), j < 2^(L-th)
     int th;
-    int diag;                  // diagnostics only: 1 = skip the register groups, 2 = skip gather+scatter
     int l1, l2;                // six-step: gather stride bits (A: local columns n1/G), row bits (B)
     int qoff;                  // six-step A: global index of local column 0 (distributed: rank*n1/G)
     int pb;                    // six-step A: log2 of the row slice per destination (n2/G); = l2 when G = 1
@@ -395,7 +394,6 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
     // issue the cp.async copies of tile tl into the staging buffer (raw order
     // of the gather loops below: vector i -> stage[i*VE], scalar i -> stage[i])
     auto prefetch = [&](uint64_t tl, const uint64_t* Gin) {
-        if (a.diag == 2) return;
         if (a.vec_in && a.in_order == TO_T_FAST) {
             const uint64_t gb = Gin[(threadIdx.x % (TQ / VE)) * VE];
 #pragma unroll 4
@@ -458,8 +456,7 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
             __syncthreads();
         }
         // ---- gather (16-byte vectors along the contiguous run when valid)
-        if (a.diag == 2) {
-        } else if (a.vec_in && a.in_order == TO_T_FAST) {
+        if (a.vec_in && a.in_order == TO_T_FAST) {
             const uint64_t gb = GinB[pbuf][(threadIdx.x % (TQ / VE)) * VE];
 #pragma unroll 4
             for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {
@@ -539,7 +536,6 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
         T* dst = bufB;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            if (a.diag == 1) break;
             T v[16];
 #pragma unroll
             for (int r = 0; r < REP; ++r) {
@@ -662,8 +658,7 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
             if (a.scale) r = ar.mulc(r, a.ninv);
             return r;
         };
-        if (a.diag == 2) {
-        } else if (a.vec_out && a.out_order == TO_T_FAST) {
+        if (a.vec_out && a.out_order == TO_T_FAST) {
             const uint64_t gb = Gout[(threadIdx.x % (TQ / VE)) * VE];
 #pragma unroll 4
             for (uint32_t i = threadIdx.x; i < (uint32_t)(TQ << K) / VE; i += NT) {

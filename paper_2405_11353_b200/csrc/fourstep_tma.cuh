@@ -307,187 +307,5 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
     }
 }
 
-// ---------------------------------------------------------------------------
-// 2^10 passes with 32-residue register blocks (NTT_FS_RB5): two groups of 5
-// stages, so one shared-memory exchange and two barriers per tile instead of
-// two and three; 256 threads (32 per network), TQ = 8 networks per tile.
-// Tile-major (q = tid & 7) in both groups: group-0 in-warp bits on u bits 3,4
-// (rows 0,1 of the dense staging; positions 8,9 when written), last group
-// in-warp bits on u bits 3,4 (positions 3,4 for DIT, 8,9 for Pease): with an
-// odd network stride every access is conflict-free (tools/bank_fs.py model).
-template <class A, int K, int B, int kg>
-NTT_D void bw32(const A& ar, typename A::T (&v)[32], uint32_t pbase, const typename A::Tw* tws) {
-#pragma unroll
-    for (int j = 0; j < kg; ++j) {
-        const int sl = B + j, s = sl + 1;
-        const uint32_t lmask = (1u << sl) - 1;
-        const uint32_t rowi = (1u << (s - 1)) + (pbase & lmask);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-            if (c & (1 << j)) continue;
-            const uint32_t kc = ((uint32_t)c << B) & lmask;
-            const int hi = c | (1 << j);
-            if (s == 1) ar.dit1(v[c], v[hi]);
-            else ar.dit(v[c], v[hi], ftile::lds_tw(tws + rowi + kc));
-        }
-    }
-}
-
-template <class A, int K, int sg, int kg>
-NTT_D void pe32(const A& ar, typename A::T (&v)[32], uint32_t u, const typename A::Tw* tws) {
-    using T = typename A::T;
-    constexpr int H = 1 << (kg - 1);
-    const uint32_t qtop = sg ? (u >> ((K - kg - sg) > 0 ? (K - kg - sg) : 0)) : 0u;
-#pragma unroll
-    for (int m = 0; m < kg; ++m) {
-        const int s = sg + m + 1;
-        T nv[32];
-#pragma unroll
-        for (int i = 0; i < H; ++i) {
-            const uint32_t Bp = (2u * i) >> (kg - m);
-            T x = v[2 * i], y = v[2 * i + 1];
-            if (s == 1) ar.dit1(x, y);
-            else ar.dit(x, y, ftile::lds_tw(tws + (1u << (s - 1)) + ((Bp << sg) | qtop)));
-            nv[i] = x;
-            nv[i + H] = y;
-        }
-#pragma unroll
-        for (int c = 0; c < 32; ++c) v[c] = nv[c];
-    }
-}
-
-constexpr int kNP5 = ((fastk::padded_len<uint32_t, 10>() + 31) / 32) * 32 + 1;
-template <int MODE>
-constexpr size_t fsa5_smem_bytes() {
-    return (size_t)8 * 1024 + 2 * (size_t)(MODE == 0 ? 8192 : 8 * kStgRow) * 4 + (size_t)8 * kNP5 * 4 + 8 +
-           32 * 8 * 8;
-}
-
-template <class A, int V, int MODE, int KO>
-__global__ void __launch_bounds__(256, 2) k_fs_tma5(const __grid_constant__ CUtensorMap tmap, FsTmaArgs<A> a) {
-    using T = typename A::T;
-    using Tw = typename A::Tw;
-    constexpr int K = 10, TQ = 8, NT = 256, NP = kNP5;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t mbar[2];
-    Tw* tws = reinterpret_cast<Tw*>(smem_raw);
-    T* stg = reinterpret_cast<T*>(smem_raw + 8 * 1024);
-    constexpr int STG = MODE == 0 ? 8192 : 8 * kStgRow;
-    T* W = stg + 2 * STG;
-    Tw* twB = reinterpret_cast<Tw*>(W + ((8 * NP + 1) & ~1));          // factored twist [c][q], c < 32
-    A ar;
-    ar.init(a.p);
-    const uint32_t tid = threadIdx.x;
-    for (uint32_t i = tid; i < 1024; i += NT) tws[i] = a.stw[i];
-    constexpr int Kr = MODE == 0 ? K : KO, Kc = MODE == 0 ? KO : K;
-    constexpr uint64_t N = 1ull << (Kr + Kc);
-    constexpr int tpp_log = (MODE == 0 ? Kc : Kr) - 3;
-    const uint64_t ntiles = a.batch << tpp_log;
-    constexpr uint32_t TILE_BYTES = 8192 * 4;
-    auto issue = [&](uint64_t tl, int s) {
-        fastk::mbar_expect_tx(&mbar[s], TILE_BYTES);
-        if (MODE == 0) {
-            const int x = (int)((tl & ((1ull << tpp_log) - 1)) * TQ);
-            const int y = (int)((tl >> tpp_log) << K);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) tma_load_2d(stg + s * STG + j * 256 * TQ, &tmap, x, y + 256 * j, &mbar[s]);
-        } else {
-            const T* src = a.in + (tl >> tpp_log) * N + (((tl & ((1ull << tpp_log) - 1)) * 8) << 10);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) bulk_load(stg + s * STG + j * kStgRow, src + j * 1024, 4096, &mbar[s]);
-        }
-    };
-    if (tid == 0) {
-        fastk::mbar_init(&mbar[0], 1);
-        fastk::mbar_init(&mbar[1], 1);
-        fastk::fence_mbar_init();
-    }
-    __syncthreads();
-    fastk::pdl_trigger();
-    fastk::pdl_wait();
-    if (tid == 0) {
-        if ((uint64_t)blockIdx.x < ntiles) issue(blockIdx.x, 0);
-        if ((uint64_t)blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
-    }
-    const uint32_t q = tid & 7, w = tid >> 3;             // w: 5 bits, the low 2 in-warp
-    // in-warp bits (w bits 0,1) -> u bits 3,4 in both groups
-    const uint32_t u = ((w & 3u) << 3) | (w >> 2);
-    auto xout = [&](int c) -> uint32_t {                  // natural output position of register c
-        return u | ((uint32_t)c << 5);
-    };
-    int it = 0;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int s = it & 1;
-        const T* S = stg + s * STG;
-        const T* Sq = S + (MODE == 0 ? q : q * kStgRow);
-        auto sidx = [&](uint32_t x) -> uint32_t { return MODE == 0 ? x * TQ : x; };
-        T v[32];
-        const uint32_t rb = brev(u << 5, K);               // input index of position u << 5
-        fastk::mbar_wait(&mbar[s], (it >> 1) & 1);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) v[c] = Sq[sidx(rb) + sidx(brev((uint32_t)c, 5) << 5)];
-        if (V == V_DIT) {
-            bw32<A, K, 0, 5>(ar, v, u << 5, tws);          // stages 1..5, positions u << 5 | c
-            __syncthreads();
-            T* wb = W + q * NP + padpos<T>(u << 5);
-#pragma unroll
-            for (int c = 0; c < 32; ++c) wb[padpos<T>((uint32_t)c)] = v[c];
-        } else {
-            pe32<A, K, 0, 5>(ar, v, u, tws);               // outputs at positions u | c << 5
-            __syncthreads();
-            T* wbo = W + q * NP + padpos<T>(u);
-#pragma unroll
-            for (int c = 0; c < 32; ++c) wbo[padpos<T>((uint32_t)c << 5)] = v[c];
-        }
-        Tw twA;
-        if (MODE == 0) {
-            const uint64_t col0 = (tile & ((1ull << tpp_log) - 1)) * TQ;
-            const uint32_t c = tid >> 3, t = tid & 7;        // 32 x 8 factors, one per thread
-            twB[tid] = __ldg(a.tw_main + (col0 + t) * ((uint32_t)c << 5));
-            twA = __ldg(a.tw_main + (col0 + q) * u);
-        }
-        if (tid == 0) {
-            const uint64_t nn = tile + 2 * (uint64_t)gridDim.x;
-            if (nn < ntiles) {
-                fastk::fence_proxy_async();
-                issue(nn, s);
-            }
-        }
-        __syncthreads();
-        {
-            const T* sb = W + q * NP;
-            const uint64_t col = (tile & ((1ull << tpp_log) - 1)) * TQ + q;
-            if (V == V_DIT) {
-                const T* wb = sb + padpos<T>(u);
-#pragma unroll
-                for (int c = 0; c < 32; ++c) v[c] = wb[padpos<T>((uint32_t)c << 5)];
-                bw32<A, K, 5, 5>(ar, v, u, tws);            // stages 6..10
-            } else {
-                const T* rbp = sb + padpos<T>(u << 5);
-#pragma unroll
-                for (int c = 0; c < 32; ++c) v[c] = rbp[padpos<T>((uint32_t)c)];
-                pe32<A, K, 5, 5>(ar, v, u, tws);
-            }
-            T* dst = a.out + (tile >> tpp_log) * N + col;
-            if (MODE == 0) {
-#pragma unroll
-                for (int c = 0; c < 32; ++c)
-                    dst[(uint64_t)xout(c) << Kc] = ar.mull(ar.mull(v[c], ftile::lds_tw(&twB[c * 8 + q])), twA);
-            } else if (a.scale) {
-#pragma unroll
-                for (int c = 0; c < 32; ++c) dst[(uint64_t)xout(c) << Kr] = ar.mulc(v[c], a.ninv);
-            } else {
-#pragma unroll
-                for (int c = 0; c < 32; ++c) dst[(uint64_t)xout(c) << Kr] = ar.fin(v[c]);
-            }
-        }
-        if (a.counters && tid == 0 && (tile & ((1ull << tpp_log) - 1)) == 0) {
-            atomicAdd(a.counters + C_HBM, 1ull);
-            if (MODE == 1) atomicAdd(a.counters + C_TRANSFORMS, 1ull);
-            if (a.count_bitrev) atomicAdd(a.counters + C_BITREV, (unsigned long long)a.count_bitrev);
-        }
-    }
-}
-
 }  // namespace fstep
 }  // namespace nttb200

@@ -8,7 +8,7 @@ cudaError_t fourstep_u32_canon_w(const MultipassReq& r);   // kfs_f32w.cu: 2^31 
 
 cudaError_t fourstep_f32(const MultipassReq& r, bool* ok) {
     *ok = false;
-    if (!fourstep_enabled() || !fourstep_applies(r.L, r.variant, r.p, 4) || !r.fst || !r.stw || !r.ws)
+    if (!fourstep_applies(r.L, r.variant, r.p, 4) || !r.fst || !r.stw || !r.ws)
         return cudaSuccess;
     *ok = true;
     if (r.p < (1ull << 30)) return fourstep_u32_policy<LazyF32>(r);

@@ -5,10 +5,6 @@
 #include "multipass.cuh"
 namespace nttb200 {
 
-static bool fourstep_gold_enabled() {
-    static const bool on = [] { const char* e = getenv("NTT_FOURSTEP"); return !(e && e[0] == '0'); }();
-    return on;
-}
 
 template <int V, int L>
 static cudaError_t fsg_run_l(const MultipassReq& r) {
@@ -51,7 +47,7 @@ static cudaError_t fsg_run(const MultipassReq& r) {
 
 cudaError_t fourstep_gold(const MultipassReq& r, bool* ok) {
     *ok = false;
-    if (!fourstep_gold_enabled() || !fourstep_applies(r.L, r.variant, r.p, 8) || !r.fst || !r.stw || !r.ws)
+    if (!fourstep_applies(r.L, r.variant, r.p, 8) || !r.fst || !r.stw || !r.ws)
         return cudaSuccess;
     *ok = true;
     // Flat's per-stage states are DIT's: DIT sub-transforms

@@ -10,20 +10,9 @@
 #include "lazy.cuh"
 namespace nttb200 {
 
-// NTT_FOURSTEP=0 routes these sizes to the stage-faithful tile passes (A/B experiments)
-inline bool fourstep_enabled() {
-    static const bool on = [] { const char* e = getenv("NTT_FOURSTEP"); return !(e && e[0] == '0'); }();
-    return on;
-}
-
 #ifndef NTT_FSA_L2PROMO
 #define NTT_FSA_L2PROMO 0     // TMA L2 promotion of the 32-byte box rows: 0 none, 1 64B, 2 128B, 3 256B
 #endif
-// NTT_FS_TMA=0 keeps pass A on cp.async copy-in (A/B experiments)
-inline bool fs_tma_enabled() {
-    static const bool on = [] { const char* e = getenv("NTT_FS_TMA"); return !(e && e[0] == '0'); }();
-    return on;
-}
 
 inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
@@ -72,43 +61,6 @@ inline cudaError_t fs_pass_tma_k(const MultipassReq& r, const CUtensorMap& map) 
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-// NTT_FS_RB5=1: the 2^10 passes with 32-residue register blocks (experiment switch)
-inline bool fs_rb5_enabled() {
-    static const bool on = [] { const char* e = getenv("NTT_FS_RB5"); return e && e[0] == '1'; }();
-    return on;
-}
-
-template <class A, int V, int MODE, int KO>
-inline cudaError_t fs_pass_tma5(const MultipassReq& r, const CUtensorMap& map) {
-    constexpr int Kr = MODE == 0 ? 10 : KO, Kc = MODE == 0 ? KO : 10;
-    fstep::FsTmaArgs<A> a{};
-    a.in = static_cast<const uint32_t*>(MODE == 0 ? r.in : r.ws);
-    a.out = static_cast<uint32_t*>(MODE == 0 ? r.ws : r.out);
-    a.batch = r.batch;
-    a.Kr = Kr;
-    a.Kc = Kc;
-    a.stw = static_cast<const uint2*>(r.stw);
-    a.tw_main = static_cast<const uint2*>(r.tw);
-    a.p = r.p;
-    a.scale = MODE == 1 ? r.scale : 0;
-    a.ninv = make_uint2((uint32_t)r.ninv, (uint32_t)r.ninv_shoup);
-    a.count_bitrev = MODE == 0 ? 1 : 0;
-    a.counters = r.counters;
-    constexpr size_t smem = fstep::fsa5_smem_bytes<MODE>();
-    auto kern = fstep::k_fs_tma5<A, V, MODE, KO>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int occ = 0;
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
-    const uint64_t ntiles = r.batch << ((MODE == 0 ? Kc : Kr) - 3);
-    uint64_t grid = (uint64_t)r.num_sms * occ;
-    if (grid > ntiles) grid = ntiles;
-    e = fastk::launch_pdl(kern, dim3((unsigned)grid), dim3(256), smem, r.stream, map, a);
-    if (r.launches) ++*r.launches;
-    return e != cudaSuccess ? e : cudaGetLastError();
-}
-
 // true when the pass ran through the TMA kernel (*err its status)
 template <class A, int V, int MODE>
 inline bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err) {
@@ -117,7 +69,7 @@ inline bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err)
     else {
     const void* src = MODE == 0 ? r.in : r.ws;
     const int K = MODE == 0 ? Kr : Kc;
-    if (!fs_tma_enabled() || (reinterpret_cast<uintptr_t>(src) & 15)) return false;
+    if (reinterpret_cast<uintptr_t>(src) & 15) return false;
     if (MODE == 1 && K != 10) return false;
     if (K < 7 || K > 10) return false;
     CUtensorMap map;
@@ -141,12 +93,6 @@ inline bool fs_pass_tma(const MultipassReq& r, int Kr, int Kc, cudaError_t* err)
     // (K, other dimension) pairs of 2^14 .. 2^20 (Kr = ceil(L/2), Kc = floor(L/2))
 #define NTT_FSTK(KK, KOO) \
     if (K == KK && (MODE == 0 ? Kc : Kr) == KOO) { *err = fs_pass_tma_k<A, V, MODE, KK, KOO>(r, map); return true; }
-    if constexpr (std::is_same<A, LazyF32>::value) {
-        if (K == 10 && fs_rb5_enabled()) {
-            if ((MODE == 0 ? Kc : Kr) == 10) { *err = fs_pass_tma5<A, V, MODE, 10>(r, map); return true; }
-            if (MODE == 0 && Kc == 9) { *err = fs_pass_tma5<A, V, 0, 9>(r, map); return true; }
-        }
-    }
     if constexpr (MODE == 0) {
         NTT_FSTK(7, 7) NTT_FSTK(8, 7) NTT_FSTK(8, 8) NTT_FSTK(9, 8) NTT_FSTK(9, 9) NTT_FSTK(10, 9) NTT_FSTK(10, 10)
     } else {

@@ -23,10 +23,9 @@ cudaError_t tile_sixstep_gold(const MultipassReq& r, bool* ok) {
     using A = GoldPolicy<false>;
     *ok = false;
     if (!r.stw1 || !r.stw2 || !r.cor_lo) return cudaSuccess;
-    // long-run column/row passes + explicit transpose; the column-at-a-time
-    // kernels (TL_SIX_A/B) stay for the distributed steps below
-    static const int legacy = [] { const char* v = getenv("NTT_SIXSTEP_LEGACY"); return v ? atoi(v) : 0; }();
-    if (!legacy) {
+    // long-run column/row passes + explicit transpose (the 2^13 x 2^13 and
+    // 2^7 x 2^7 splits); other splits fall to the column-at-a-time kernels
+    {
         cudaError_t e = ftile::run_sixstep_cols<A>(r, ok);
         if (e != cudaSuccess || *ok) return e;
     }
@@ -43,9 +42,8 @@ cudaError_t tile_sixstep_dist_gold(const MultipassReq& r, int step, int rank, in
     using A = GoldPolicy<false>;
     *ok = false;
     if (!r.stw1 || !r.stw2 || !r.cor_lo) return cudaSuccess;
-    // long-run column passes + per-destination transpose (NTT_SIXSTEP_LEGACY=1: column-at-a-time kernels)
-    static const int legacy = [] { const char* v = getenv("NTT_SIXSTEP_LEGACY"); return v ? atoi(v) : 0; }();
-    if (!legacy || peers) {
+    // long-run column passes + per-destination transpose
+    {
         cudaError_t e = ftile::run_sixstep_cols_dist<A>(r, step, rank, world, in, out, r.ws, ok, peers);
         if (e != cudaSuccess || *ok || peers) return e;      // the peer pack exists on the long-run path only
     }

@@ -633,8 +633,6 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     // 2 chunks (config 2: 1.43 ms/step at 1-2 chunks, 1.55 at 8; the PCIe
     // floor with both directions busy is 1.35 ms, tools/e2e_async.py)
     if (async && resident && bytes >= (16ull << 20)) chunks = 2;
-    static const int env_chunks = [] { const char* v = getenv("NTT_HOST_CHUNKS"); return v ? atoi(v) : 0; }();
-    if (resident && env_chunks > 0) chunks = (uint64_t)env_chunks;     // tuning knob (tools/e2e_sweep.py)
     if (chunks > (uint64_t)ntt_plan_s::kMaxChunks) chunks = ntt_plan_s::kMaxChunks;
     if (chunks > batch) chunks = batch;
     char* d = static_cast<char*>(plan->hbuf) + (size_t)set * plan->hset_bytes;

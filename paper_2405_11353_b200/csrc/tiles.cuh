@@ -78,11 +78,6 @@ cudaError_t pass_any(int K, const TileArgs<A>& a, cudaStream_t s, int sms, int* 
     return cudaSuccess;
 }
 
-// NTT_TILE_DIAG=1|2: diagnostics (skip compute | skip data movement); never set in production
-inline int tile_diag() {
-    static int d = [] { const char* e = getenv("NTT_TILE_DIAG"); return e ? atoi(e) : 0; }();
-    return d;
-}
 
 // Pass plan.  Tiles hold 2^13 (u32) / 2^12 (u64) residues, so a pass of K
 // stages has TQ = 2^(13-K) networks and every strided HBM side moves runs of
@@ -90,12 +85,9 @@ inline int tile_diag() {
 // with 256 B runs (K = 7,7,6) ran 9-11 ms against 4.6 ms for 2 passes of
 // K = 10 with 32 B runs: the TQ >= 32 tiles fit one CTA per SM and their
 // 8-thread networks share warps with bank-conflicting strides.  So: fewest
-// passes, K <= 10 (NTT_TILE_KMAX overrides, for experiments).
+// passes, K <= 10.
 inline int tile_plan(int L, int word, int* K) {
-    int kmax;
-    static const int env_kmax = [] { const char* v = getenv("NTT_TILE_KMAX"); return v ? atoi(v) : 0; }();
-    if (word == 4) kmax = env_kmax ? env_kmax : 10;   // NTT_TILE_KMAX: plan experiments (tools/time_case.py)
-    else kmax = 9;
+    const int kmax = word == 4 ? 10 : 9;
     const int kmin = 6;
     int P = (L + kmax - 1) / kmax;
     if (P < 2) P = 2;
@@ -116,7 +108,6 @@ TileArgs<A> tile_base(const MultipassReq& r) {
     a.ninv = make_tw2<typename A::Field>(r.ninv, r.ninv_shoup);
     a.counters = r.counters;
     a.TA = 1;
-    a.diag = tile_diag();
     return a;
 }
 
