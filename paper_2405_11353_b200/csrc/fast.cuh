@@ -24,15 +24,6 @@
 #include "engine.cuh"
 #include "lazy.cuh"
 
-#ifndef NTT_FAST_DS_LATE
-#define NTT_FAST_DS_LATE 0
-#endif
-#ifndef NTT_FAST_TABLE_TMA
-#define NTT_FAST_TABLE_TMA 0
-#endif
-#ifndef NTT_FAST_TRIGGER_FIRST
-#define NTT_FAST_TRIGGER_FIRST 1
-#endif
 
 namespace nttb200 {
 namespace fastk {
@@ -174,21 +165,38 @@ struct FastArgs {
     unsigned long long* counters;
 };
 
+// Stage twiddles: stages s <= LS read the shared-memory copy of the per-stage
+// table, later stages (only the last stage of 2^14 u32 transforms, whose
+// 2^13-entry row would not fit beside the polynomial and its staging buffer)
+// read the plan's global copy through the read-only path (L1-resident).
+template <class Tw>
+NTT_D Tw twld(const Tw* p, bool global) { return global ? __ldg(p) : *p; }
+template <class Tw>
+NTT_D const Tw* twrow(const Tw* stw, const Tw* gstw, int s, int LS) { return s > LS ? gstw : stw; }
+// shared-memory-resident stages of a single-pass L-stage transform
+template <class T, int L>
+NTT_HD constexpr int fast_smem_stages() { return (sizeof(T) == 4 && L >= 14) ? L - 1 : L; }
+// first-group input through a TMA-prefetched staging buffer (else straight from HBM)
+template <int V, int L, int RB>
+NTT_HD constexpr bool fast_staged() { return RB == 4 && !(V == V_PEASE && L >= 14); }
+
 // DIT-type butterfly of global stage s (1-based) of a single-pass transform:
 // stage 1 sees canonical inputs, stage 2 inputs in [0,2p) (lazy bounds)
 // (s is a compile-time constant after the callers' loops unroll)
 template <class A>
-NTT_D void dit_stage_bf(const A& ar, int s, typename A::T& x, typename A::T& y, const typename A::Tw* w, bool triv) {
+NTT_D void dit_stage_bf(const A& ar, int s, typename A::T& x, typename A::T& y, const typename A::Tw* w, bool triv,
+                        bool g = false) {
     if (s == 1) ar.dit1_c(x, y);
-    else if (s == 2) { if (triv) ar.dit1_2p(x, y); else ar.dit_2p(x, y, *w); }
-    else { if (triv) ar.dit1(x, y); else ar.dit(x, y, *w); }
+    else if (s == 2) { if (triv) ar.dit1_2p(x, y); else ar.dit_2p(x, y, twld(w, g)); }
+    else { if (triv) ar.dit1(x, y); else ar.dit(x, y, twld(w, g)); }
 }
 
 // ---------------------------------------------------------------- DIT/DIF --
 // In-place window [b0, b0+kg) of a register block [B, B+4); pbase = position
 // of register 0.  DIT: stages b0+1.. ascending; DIF: descending.
-template <class A, int L, int B, int b0, int kg, bool DIF, int RB, int RN>
-NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[RN], uint32_t pbase, const typename A::Tw* stw) {
+template <class A, int L, int B, int b0, int kg, bool DIF, int RB, int RN, int LS = L>
+NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[RN], uint32_t pbase, const typename A::Tw* stw,
+                       const typename A::Tw* gstw = nullptr) {
     // (instantiated for every macro-listed geometry; only valid windows emit code)
     if constexpr (b0 >= B && b0 + kg <= B + RB) {
     constexpr int off = b0 - B;
@@ -199,7 +207,8 @@ NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[RN], uint32_t pbase, cons
         const int j = DIF ? kg - 1 - jj : jj;
         const int s = b0 + 1 + j;
         const uint32_t kmask = (1u << (s - 1)) - 1;
-        const typename A::Tw* row = stw + (1u << (s - 1)) + (pbase & kmask);
+        const bool g = s > LS;
+        const typename A::Tw* row = twrow(stw, gstw, s, LS) + (1u << (s - 1)) + (pbase & kmask);
 #pragma unroll
         for (int c = 0; c < RN; ++c) {
             if (c & (1 << (off + j))) continue;
@@ -208,12 +217,12 @@ NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[RN], uint32_t pbase, cons
             const bool triv = (s == 1 || (B == 0 && kc == 0));      // w^0 = 1
             if (DIF) {
                 if (triv) ar.dif1(v[c], v[hi]);
-                else ar.dif(v[c], v[hi], row[kc]);
+                else ar.dif(v[c], v[hi], twld(row + kc, g));
             } else if (B == 0) {
-                dit_stage_bf(ar, s, v[c], v[hi], row + kc, triv);
+                dit_stage_bf(ar, s, v[c], v[hi], row + kc, triv, g);
             } else {
                 if (triv) ar.dit1(v[c], v[hi]);
-                else ar.dit(v[c], v[hi], row[kc]);
+                else ar.dit(v[c], v[hi], twld(row + kc, g));
             }
         }
     }
@@ -225,8 +234,9 @@ NTT_D void bitwin_regs(const A& ar, typename A::T (&v)[RN], uint32_t pbase, cons
 // (network n = registers [n*2^kg, (n+1)*2^kg)).  Constant geometry inside the
 // registers; twiddle k = (B << sg) | (q >> (L - kg - sg)) for butterfly with
 // output-bit prefix B (algorithms.py:216-217 in the rotated frame).
-template <class A, int L, int sg, int kg, int RB, int RN>
-NTT_D void pease_regs(const A& ar, typename A::T (&v)[RN], uint32_t ubase, const typename A::Tw* stw) {
+template <class A, int L, int sg, int kg, int RB, int RN, int LS = L>
+NTT_D void pease_regs(const A& ar, typename A::T (&v)[RN], uint32_t ubase, const typename A::Tw* stw,
+                      const typename A::Tw* gstw = nullptr) {
     using T = typename A::T;
     if constexpr (kg <= RB && sg + kg <= L) {        // (only valid windows emit code)
     constexpr int NB = RN >> kg;
@@ -245,10 +255,11 @@ NTT_D void pease_regs(const A& ar, typename A::T (&v)[RN], uint32_t ubase, const
                 const uint32_t Bp = R >> (kg - m);               // output bits so far (m bits)
                 T x = v[n * (1 << kg) + 2 * i], y = v[n * (1 << kg) + 2 * i + 1];
                 const bool triv = (s == 1 || (sg == 0 && Bp == 0));     // w^0 (k = Bp when sg == 0)
-                const typename A::Tw* wp = stw + (1u << (s - 1)) + ((Bp << sg) | qtop);
-                if (sg == 0) dit_stage_bf(ar, s, x, y, wp, triv);
+                const bool g = s > LS;
+                const typename A::Tw* wp = twrow(stw, gstw, s, LS) + (1u << (s - 1)) + ((Bp << sg) | qtop);
+                if (sg == 0) dit_stage_bf(ar, s, x, y, wp, triv, g);
                 else if (triv) ar.dit1(x, y);
-                else ar.dit(x, y, *wp);
+                else ar.dit(x, y, twld(wp, g));
                 nv[i] = x;
                 nv[i + H] = y;
             }
@@ -265,8 +276,9 @@ NTT_D void pease_regs(const A& ar, typename A::T (&v)[RN], uint32_t ubase, const
 // group only).  Stage s = sg+m pairs the window's top remaining bit; the
 // output bit is inserted above the previous ones ([c_rest | B] layout);
 // twiddle k = j = (B << sg) | hi (algorithms.py:281-299).
-template <class A, int L, int sg, int kg, int RB, int RN>
-NTT_D void stockham_regs(const A& ar, typename A::T (&v)[RN], uint32_t hi, const typename A::Tw* stw) {
+template <class A, int L, int sg, int kg, int RB, int RN, int LS = L>
+NTT_D void stockham_regs(const A& ar, typename A::T (&v)[RN], uint32_t hi, const typename A::Tw* stw,
+                         const typename A::Tw* gstw = nullptr) {
     using T = typename A::T;
     if constexpr (kg <= RB && sg + kg <= L) {        // (only valid windows emit code)
     constexpr int NB = RN >> kg;
@@ -282,10 +294,11 @@ NTT_D void stockham_regs(const A& ar, typename A::T (&v)[RN], uint32_t hi, const
                 const uint32_t Bv = i & ((1u << m) - 1), crest = (uint32_t)i >> m;
                 T a = v[(i << (RB - kg)) | x], b = v[((i + H) << (RB - kg)) | x];
                 const bool triv = (s == 0 || (sg == 0 && Bv == 0));     // w^0 (j = Bv when sg == 0)
-                const typename A::Tw* wp = stw + (1u << s) + ((Bv << sg) | hi);
-                if (sg == 0) dit_stage_bf(ar, s + 1, a, b, wp, triv);
+                const bool g = s + 1 > LS;
+                const typename A::Tw* wp = twrow(stw, gstw, s + 1, LS) + (1u << s) + ((Bv << sg) | hi);
+                if (sg == 0) dit_stage_bf(ar, s + 1, a, b, wp, triv, g);
                 else if (triv) ar.dit1(a, b);
-                else ar.dit(a, b, *wp);
+                else ar.dit(a, b, twld(wp, g));
                 nv[(crest << (m + 1)) | Bv] = a;
                 nv[(crest << (m + 1)) | (1u << m) | Bv] = b;
             }
@@ -316,7 +329,8 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     // no staging -- the first group loads its 64 residues per thread straight
     // from HBM (coalesced 128 B warp rows); the smem saved buys twice the teams,
     // whose interleaved load / compute phases hide the latency instead.
-    constexpr bool STG_ = (RB == 4);
+    // (Pease 2^14: its two work buffers leave no room for staging -- direct loads)
+    constexpr bool STG_ = fast_staged<V, L, RB>();
     constexpr int NBUF = TWO ? 3 : 2;      // staging + work (+ second work buffer for Pease)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // DS: two staging buffers per team, the polynomial after next in flight
@@ -325,29 +339,23 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     constexpr int NSTG = STG_ ? ((DS || PW) ? 2 : 1) : 0;
     static_assert(!PW || (STG_ && !DS), "pointwise-fused kernels stage both operands");
     __shared__ uint64_t mbar[TEAMS * 2];
-    __shared__ uint64_t tbar;              // NTT_FAST_TABLE_TMA: the stage table's bulk copy
+    constexpr int LS = fast_smem_stages<T, L>();     // stages with shared-memory twiddles
+    constexpr int NTS = 1 << LS;                     // table entries held in shared memory
 
     Tw* stw = reinterpret_cast<Tw*>(smem_raw);
+    const Tw* gstw = a.stw;
     const int team = threadIdx.x / TT;
     const uint32_t t = threadIdx.x % TT;
     constexpr int NP = padded_len<T, L>();
-    T* S = reinterpret_cast<T*>(smem_raw + (size_t)N * sizeof(Tw)) + (size_t)team * (NSTG * N + (NBUF - 1) * NP);
+    T* S = reinterpret_cast<T*>(smem_raw + (size_t)NTS * sizeof(Tw)) + (size_t)team * (NSTG * N + (NBUF - 1) * NP);
     T* W0 = S + NSTG * N;
     T* W1 = TWO ? W0 + NP : W0;
     A ar;
     ar.init(a.p);
 
-    // twiddle table once per CTA (one bulk async copy, or a thread loop); barriers
-    if constexpr (NTT_FAST_TABLE_TMA) {
-        if (threadIdx.x == 0) {
-            mbar_init(&tbar, 1);
-            fence_mbar_init();
-            mbar_expect_tx(&tbar, (uint32_t)(N * sizeof(Tw)));
-            tma_load_1d(stw, a.stw, (uint32_t)(N * sizeof(Tw)), &tbar);
-        }
-    } else {
-        for (int i = threadIdx.x; i < N; i += blockDim.x) stw[i] = a.stw[i];
-    }
+    // twiddle table once per CTA (a thread loop: a bulk async copy measured the
+    // same, the prologue overlaps the previous launch's tail under PDL); barriers
+    for (int i = threadIdx.x; i < NTS; i += blockDim.x) stw[i] = a.stw[i];
     if (t == 0) { mbar_init(&mbar[2 * team], 1); mbar_init(&mbar[2 * team + 1], 1); }
     fence_mbar_init();
     __syncthreads();
@@ -355,15 +363,10 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     // overlaps the previous launch's tail; its outputs are visible after the wait.
     // (Issuing the first TMA loads before the table copy moves the copy behind
     // the wait: config 2 37.1 vs 34.6 us per step, measured A/B.)
-    // trigger, then wait; the opposite order (NTT_FAST_TRIGGER_FIRST=0) measured
-    // the same (config 2, 5 x 2 runs of 1000 steps: 34.95 vs 35.07 us/step)
-#if NTT_FAST_TRIGGER_FIRST
+    // trigger, then wait (the opposite order measured the same: config 2,
+    // 5 x 2 runs of 1000 steps, 34.95 vs 35.07 us/step)
     pdl_trigger();
     pdl_wait();
-#else
-    pdl_wait();
-    pdl_trigger();
-#endif
 
     const uint64_t stride = (uint64_t)gridDim.x * TEAMS;
     uint64_t poly = (uint64_t)blockIdx.x * TEAMS + team;
@@ -372,12 +375,11 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
         mbar_expect_tx(&mbar[2 * team], PW ? 2 * bytes : bytes);
         tma_load_1d(S, a.in + poly * N, bytes, &mbar[2 * team]);
         if (PW) tma_load_1d(S + N, a.in2 + poly * N, bytes, &mbar[2 * team]);
-        if (DS && !NTT_FAST_DS_LATE && poly + stride < a.batch) {
+        if (DS && poly + stride < a.batch) {
             mbar_expect_tx(&mbar[2 * team + 1], bytes);
             tma_load_1d(S + N, a.in + (poly + stride) * N, bytes, &mbar[2 * team + 1]);
         }
     }
-    if constexpr (NTT_FAST_TABLE_TMA) mbar_wait(&tbar, 0);   // the table has landed
     uint32_t it = 0;
     int copies = 0;
     const int bar_id = 1 + team;
@@ -386,14 +388,6 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
         T v[RV];
         const uint32_t sb_ = DS ? (it & 1) : 0;     // staging buffer of this polynomial
         if (STG_) mbar_wait(&mbar[2 * team + sb_], DS ? ((it >> 1) & 1) : (it & 1));
-        if constexpr (DS && NTT_FAST_DS_LATE) {
-            // the second polynomial's copy starts once the first has landed, so
-            // the first round's loads do not share HBM with the second round's
-            if (it == 0 && t == 0 && poly + stride < a.batch) {
-                mbar_expect_tx(&mbar[2 * team + 1], bytes);
-                tma_load_1d(S + N, a.in + (poly + stride) * N, bytes, &mbar[2 * team + 1]);
-            }
-        }
         ++it;
         T* Sb = S + sb_ * N;
         const T* S0 = STG_ ? Sb : a.in + poly * N;   // first-group source
@@ -447,7 +441,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                 }
                 // ---- stages
 #define NTT_BW(BB, b0v, kgv)                                                                \
-    if (B == BB && kg == kgv) bitwin_regs<A, L, BB, b0v, kgv, V == V_DIF, RB, RV>(ar, v, pbase, stw);
+    if (B == BB && kg == kgv) bitwin_regs<A, L, BB, b0v, kgv, V == V_DIF, RB, RV, LS>(ar, v, pbase, stw, gstw);
                 if (V == V_DIT) {
                     if (g == 0) {
                         NTT_BW(0, 0, 1) NTT_BW(0, 0, 2) NTT_BW(0, 0, 3) NTT_BW(0, 0, 4) NTT_BW(0, 0, 5)
@@ -455,6 +449,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                     } else if (RB == 4) {
                         NTT_BW(1, 1, 4) NTT_BW(2, 2, 4) NTT_BW(3, 3, 4) NTT_BW(4, 4, 4) NTT_BW(5, 5, 4)
                         NTT_BW(6, 6, 4) NTT_BW(7, 7, 4) NTT_BW(8, 8, 4) NTT_BW(9, 9, 4)
+                        NTT_BW(10, 10, 4)
                     } else {
                         NTT_BW(5, 5, 6) NTT_BW(6, 6, 6)
                     }
@@ -465,6 +460,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                     } else if (RB == 4) {
                         NTT_BW(1, 1, 4) NTT_BW(2, 2, 4) NTT_BW(3, 3, 4) NTT_BW(4, 4, 4) NTT_BW(5, 5, 4)
                         NTT_BW(6, 6, 4) NTT_BW(7, 7, 4) NTT_BW(8, 8, 4) NTT_BW(9, 9, 4)
+                        NTT_BW(10, 10, 4)
                     } else {
                         NTT_BW(5, 5, 6) NTT_BW(6, 6, 6)
                     }
@@ -512,10 +508,10 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                         }
                     }
 #define NTT_PE(SG, KGV) \
-    if (sg == SG && kg == KGV) pease_regs<A, L, SG, KGV, RB, RV>(ar, v, u, stw);
+    if (sg == SG && kg == KGV) pease_regs<A, L, SG, KGV, RB, RV, LS>(ar, v, u, stw, gstw);
                     if (g == 0) { NTT_PE(0, 1) NTT_PE(0, 2) NTT_PE(0, 3) NTT_PE(0, 4) NTT_PE(0, 5) NTT_PE(0, 6) }
                     else if (RB == 4) { NTT_PE(1, 4) NTT_PE(2, 4) NTT_PE(3, 4) NTT_PE(4, 4) NTT_PE(5, 4) NTT_PE(6, 4)
-                           NTT_PE(7, 4) NTT_PE(8, 4) NTT_PE(9, 4) }
+                           NTT_PE(7, 4) NTT_PE(8, 4) NTT_PE(9, 4) NTT_PE(10, 4) }
                     else { NTT_PE(5, 6) NTT_PE(6, 6) }
 #undef NTT_PE
                     if (!TWO && !first && !last) team_sync(bar_id, TT);   // all reads of W0 done
@@ -555,10 +551,10 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                         }
                     }
 #define NTT_ST(SG, KGV) \
-    if (sg == SG && kg == KGV) stockham_regs<A, L, SG, KGV, RB, RV>(ar, v, hi, stw);
+    if (sg == SG && kg == KGV) stockham_regs<A, L, SG, KGV, RB, RV, LS>(ar, v, hi, stw, gstw);
                     if (g == 0) { NTT_ST(0, 1) NTT_ST(0, 2) NTT_ST(0, 3) NTT_ST(0, 4) NTT_ST(0, 5) NTT_ST(0, 6) }
                     else if (RB == 4) { NTT_ST(1, 4) NTT_ST(2, 4) NTT_ST(3, 4) NTT_ST(4, 4) NTT_ST(5, 4) NTT_ST(6, 4)
-                           NTT_ST(7, 4) NTT_ST(8, 4) NTT_ST(9, 4) }
+                           NTT_ST(7, 4) NTT_ST(8, 4) NTT_ST(9, 4) NTT_ST(10, 4) }
                     else { NTT_ST(5, 6) NTT_ST(6, 6) }
 #undef NTT_ST
                     if (!TWO && !first && !last) team_sync(bar_id, TT);   // all reads of W0 done
@@ -622,9 +618,9 @@ struct FastCfg {
     static constexpr int NBUF = (V == V_PEASE) ? 3 : 2;
     // opt-in limit per block (227 KiB, static shared memory included) minus the mbarriers
     static constexpr long kSmemCap = 227 * 1024 - 256;
-    static constexpr long table = (long)N * sizeof(Tw);
+    static constexpr long table = (long)(1 << fast_smem_stages<T, L>()) * sizeof(Tw);
     static constexpr long team_bytes_n(int nstg) {
-        return ((RB == 4 ? (long)N * nstg : 0L) + (long)(NBUF - 1) * padded_len<T, L>()) * sizeof(T);
+        return ((fast_staged<V, L, RB>() ? (long)N * nstg : 0L) + (long)(NBUF - 1) * padded_len<T, L>()) * sizeof(T);
     }
     static constexpr int teams_n(int nstg) {
         const int by_smem = (int)((kSmemCap - table) / team_bytes_n(nstg));
@@ -633,7 +629,7 @@ struct FastCfg {
         return t0 > 8 ? 8 : (t0 < 0 ? 0 : t0);
     }
     // double staging (two polynomials in flight per team) where it costs no team
-    static constexpr bool DS = !PW && NTT_FAST_DS && RB == 4 && teams_n(2) == teams_n(1);
+    static constexpr bool DS = !PW && NTT_FAST_DS && fast_staged<V, L, RB>() && teams_n(2) == teams_n(1);
     static constexpr int TEAMS = (PW && RB != 4) ? 0 : teams_n((DS || PW) ? 2 : 1);
     static constexpr long team_bytes = team_bytes_n((DS || PW) ? 2 : 1);
     static constexpr long smem = table + (long)TEAMS * team_bytes;
@@ -707,6 +703,7 @@ cudaError_t launch_fast(int L, const FastArgs<A>& a, cudaStream_t s, int num_sms
         case 11: return launch_fast_L<A, V, 11>(a, s, num_sms, launches, ok);
         case 12: return launch_fast_L<A, V, 12>(a, s, num_sms, launches, ok);
         case 13: return launch_fast_L<A, V, 13>(a, s, num_sms, launches, ok);
+        case 14: return launch_fast_L<A, V, 14>(a, s, num_sms, launches, ok);
         default: return cudaSuccess;
     }
 }

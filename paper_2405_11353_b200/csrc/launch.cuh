@@ -116,7 +116,7 @@ cudaError_t try_fast(const MultipassReq& r, bool* ok) {
     constexpr int V = V0 == V_FLAT ? V_DIT : V0;
     *ok = false;
     if (V == V_NAIVE || V == V_SIXSTEP) return cudaSuccess;
-    if (r.L < 9 || r.L > 13 || !r.stw) return cudaSuccess;
+    if (r.L < 9 || r.L > (sizeof(typename F::T) == 4 ? 14 : 13) || !r.stw) return cudaSuccess;
     if ((reinterpret_cast<uintptr_t>(r.in) & 15) || (reinterpret_cast<uintptr_t>(r.out) & 15)) return cudaSuccess;
     if constexpr (std::is_same<F, F32S>::value) {
         if (r.p < (1ull << 30)) return run_fast_policy<LazyF32, V>(r, ok);

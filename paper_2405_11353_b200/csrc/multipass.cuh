@@ -334,10 +334,11 @@ cudaError_t mp_launch_f32s(const MultipassReq& r);
 cudaError_t pointwise_inverse_f32(const MultipassReq& r, const void* in2, bool* ok);
 // two-pass four-step for large u32 N (fourstep.cuh, kfs_f32.cu); *ok = false when it does not apply
 cudaError_t fourstep_f32(const MultipassReq& r, bool* ok);
-// four-step: u32 fields DIT / Flat / DIF / Pease_nc / Stockham 14 <= L <= 20, Goldilocks 2^14..2^18
+// four-step: u32 fields DIT / Flat / DIF / Pease_nc / Stockham 15 <= L <= 20, Goldilocks 2^14..2^18
+// (u32 2^14 is one shared-memory pass: the fast kernel, fast.cuh)
 inline bool fourstep_applies(int L, int variant, uint64_t p, int word) {
     if (word == 4)
-        return p < (1ull << 32) && L >= 14 && L <= 20 &&
+        return p < (1ull << 32) && L >= 15 && L <= 20 &&
                (variant == V_DIT || variant == V_PEASE_NC || variant == V_DIF || variant == V_FLAT ||
                 variant == V_STOCKHAM);
     // Goldilocks 2^14..2^18 (config 3: 2^16 = 256 x 256)
@@ -348,10 +349,8 @@ inline bool fourstep_applies(int L, int variant, uint64_t p, int word) {
 inline int fourstep_kr(int L) { return (L + 1) / 2; }
 // u32 (p < 2^31) 2^14 outside the four-step (Pease, Stockham): the compile-time tile
 // passes (2 x 2^7) instead of the generic shared-memory engine
-inline bool tile_2p14_applies(int L, int variant, uint64_t p, int word) {
-    return word == 4 && p < (1ull << 31) && L == 14 && !fourstep_applies(L, variant, p, word) &&
-           variant != V_NAIVE && variant != V_SIXSTEP;
-}
+// (superseded: u32 2^14 now runs every variant in one shared-memory pass)
+inline bool tile_2p14_applies(int, int, uint64_t, int) { return false; }
 cudaError_t fourstep_twist_build(const void* tw, void* out, int L, int word, cudaStream_t s);
 cudaError_t fourstep_gold(const MultipassReq& r, bool* ok);
 cudaError_t mp_launch_f32w(const MultipassReq& r);
