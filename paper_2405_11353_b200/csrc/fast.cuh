@@ -581,7 +581,10 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
                 }
             }
         }
-        team_sync(bar_id, TT);    // work buffers free for the next row
+        // work buffers free for the next row: with a staging buffer the next
+        // row's "staging consumed" barrier (after its first gather, before its
+        // first scatter) already orders every read of this row's last group
+        if (!STG_) team_sync(bar_id, TT);
         if (a.counters && t == 0) {
             atomicAdd(a.counters + C_TRANSFORMS, 1ull);
             atomicAdd(a.counters + C_HBM, 1ull);

@@ -97,10 +97,18 @@ NTT_D uint32_t placeN(uint32_t w) {
 #endif
 // MODE 1 staging rows are skewed by 4 words (tile-major reads: 8 rows x 4 residues hit 32 banks)
 constexpr int kStgRow = 1024 + 4;
+// staging buffers per CTA: 2 = the tile after next in flight (2 CTAs / SM),
+// 1 = the next tile issued once group 0 has read the current one (3 CTAs / SM,
+// 40 registers): config 4 Pease_nc 2.70 -> 2.56 ms, 2^15..2^20 sweep +3..7 %,
+// DIT unchanged (measured A/B, tools/time_case.py / tools/sweep.py)
+#ifndef NTT_FSA_STAGES
+#define NTT_FSA_STAGES 1
+#endif
+constexpr int kFsaStages = NTT_FSA_STAGES;
 template <int V, int K, int MODE>
 constexpr size_t fsa_smem_bytes() {
     using GG = TmaGeo<V, K>;
-    return ((size_t)8 << K) + 2 * (size_t)(MODE == 0 ? 8192 : 8 * kStgRow) * 4 + (size_t)GG::base(GG::TQ) * 4 + 8 +
+    return ((size_t)8 << K) + kFsaStages * (size_t)(MODE == 0 ? 8192 : 8 * kStgRow) * 4 + (size_t)GG::base(GG::TQ) * 4 + 8 +
            16 * (size_t)GG::TQ * 8;
 }
 
@@ -116,7 +124,7 @@ NTT_D void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) 
 // KO = log2 of the other dimension (C for MODE 0, R for MODE 1), compile time so
 // every strided store / twist offset is an immediate
 template <class A, int V, int MODE, int K, int KO>
-__global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUtensorMap tmap, FsTmaArgs<A> a) {
+__global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const __grid_constant__ CUtensorMap tmap, FsTmaArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
     using GG = TmaGeo<V, K>;
@@ -129,7 +137,8 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
     Tw* tws = reinterpret_cast<Tw*>(smem_raw);                           // 2^K stage twiddles
     T* stg = reinterpret_cast<T*>(smem_raw + ((size_t)8 << K));          // 2 staging tiles
     constexpr int STG = MODE == 0 ? 8192 : 8 * kStgRow;                  // MODE 0 [2^K][TQ], MODE 1 [8][kStgRow]
-    T* W = stg + 2 * STG;                                                // TQ networks at GG::base(q)
+    constexpr int NST = kFsaStages;
+    T* W = stg + NST * STG;                                              // TQ networks at GG::base(q)
     Tw* twB = reinterpret_cast<Tw*>(W + ((GG::base(TQ) + 1) & ~1u));     // factored twist [c][q]
     A ar;
     ar.init(a.p);
@@ -165,7 +174,7 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
     fastk::pdl_wait();                       // the previous launch's output (our input) is visible
     if (tid == 0) {
         if ((uint64_t)blockIdx.x < ntiles) issue(blockIdx.x, 0);
-        if ((uint64_t)blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+        if (NST == 2 && (uint64_t)blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
     }
     const uint32_t q = tid & (TQ - 1), w = tid >> LQ;
     // output position of last-group register c (natural order): a(u) + b(c)
@@ -176,7 +185,7 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
     auto apart = [](uint32_t u) -> uint32_t { return V == V_DIT ? u : (u << (4 - GG::KGL)); };
     int it = 0;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int s = it & 1;
+        const int s = NST == 2 ? (it & 1) : 0;
         const T* S = stg + s * STG;
         // staging base of this thread's network (the position part added as an immediate)
         const T* Sq = S + (MODE == 0 ? q : q * kStgRow);
@@ -185,7 +194,7 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
         // ---- group 0 (tile-major): read the dense staging, write the work buffer
         const uint32_t u0 = placeN<UB, AB, GG::I0a, GG::I0b>(w);
         const uint32_t rb = brev(u0 << 4, K);                 // input index of position u0 << 4
-        fastk::mbar_wait(&mbar[s], (it >> 1) & 1);
+        fastk::mbar_wait(&mbar[s], NST == 2 ? ((it >> 1) & 1) : (it & 1));
 #pragma unroll
         for (int c = 0; c < 16; ++c) v[c] = Sq[sidx(rb) + sidx(brev((uint32_t)c, 4) << (K - 4))];
         if (V == V_DIT) {
@@ -218,8 +227,8 @@ __global__ void __launch_bounds__(512, 2) k_fs_tma(const __grid_constant__ CUten
             }
             twA = __ldg(a.tw_main + (col0 + q) * apart(uL));
         }
-        if (tid == 0) {                       // staging s is free: the tile after next
-            const uint64_t nn = tile + 2 * (uint64_t)gridDim.x;
+        if (tid == 0) {                       // staging s is free: the tile NST launches ahead
+            const uint64_t nn = tile + NST * (uint64_t)gridDim.x;
             if (nn < ntiles) {
                 fastk::fence_proxy_async();
                 issue(nn, s);
