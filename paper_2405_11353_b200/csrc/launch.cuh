@@ -139,11 +139,6 @@ cudaError_t run_variant(const MultipassReq& r) {
     const uint64_t N = 1ull << L;
     constexpr int elog = tile_elems_log2<T>();
     if constexpr (std::is_same<F, F32S>::value || std::is_same<F, F32W>::value || std::is_same<F, FGold>::value) {
-        bool ok = false;                                                             // one pass on a cluster (fastclus.cuh)
-        cudaError_t ce = std::is_same<F, FGold>::value ? fastc_gold(r, &ok) : fastc_f32(r, &ok);
-        if (ce != cudaSuccess || ok) return ce;
-    }
-    if constexpr (std::is_same<F, F32S>::value || std::is_same<F, F32W>::value || std::is_same<F, FGold>::value) {
         bool ok = false;                                                             // four-step (fourstep.cuh)
         cudaError_t fe = std::is_same<F, FGold>::value ? fourstep_gold(r, &ok) : fourstep_f32(r, &ok);
         if (fe != cudaSuccess || ok) return fe;

@@ -326,11 +326,9 @@ struct MultipassReq {
     const void* fst;           // four-step twist table [k1][n2] = w^(k1*n2) (fourstep.cuh), or null
 };
 
-// pass count / workspace of a plan (single pass: shared-memory resident, no workspace);
-// in_aligned = false: the input is not 16-byte aligned (cluster plans then fall
-// back to the two-pass four-step and need its workspace)
+// pass count / workspace of a plan (single pass: shared-memory resident, no workspace)
 int mp_num_passes(int L, int word, int variant, uint64_t p);
-uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch, uint64_t p, bool in_aligned = true);
+uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch, uint64_t p);
 cudaError_t mp_launch_f32s(const MultipassReq& r);
 // intt(in .* in2) fused into one fast-kernel launch (u32 p < 2^30, 2^9..2^13); *ok = false otherwise
 cudaError_t pointwise_inverse_f32(const MultipassReq& r, const void* in2, bool* ok);
@@ -349,16 +347,6 @@ inline bool fourstep_applies(int L, int variant, uint64_t p, int word) {
             variant == V_STOCKHAM);
 }
 inline int fourstep_kr(int L) { return (L + 1) / 2; }
-// single pass on a thread-block cluster (fastclus.cuh): u32 2^15 / 2^16 and
-// Goldilocks 2^14 .. 2^16, DIT / Flat / DIF / Pease_nc (the four-step stays the
-// fallback for misaligned inputs, so its tables are still built)
-inline bool clus_applies(int L, int variant, uint64_t p, int word) {
-    const bool v = variant == V_DIT || variant == V_FLAT || variant == V_DIF || variant == V_PEASE_NC;
-    if (word == 4) return v && p < (1ull << 32) && (L == 15 || L == 16);
-    return v && word == 8 && p == 0xFFFFFFFF00000001ull && L >= 14 && L <= 16;
-}
-cudaError_t fastc_f32(const MultipassReq& r, bool* ok);
-cudaError_t fastc_gold(const MultipassReq& r, bool* ok);
 // u32 (p < 2^31) 2^14 outside the four-step (Pease, Stockham): the compile-time tile
 // passes (2 x 2^7) instead of the generic shared-memory engine
 // (superseded: u32 2^14 now runs every variant in one shared-memory pass)

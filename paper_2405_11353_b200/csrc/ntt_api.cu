@@ -524,10 +524,7 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
     if (batch == 0) return NTT_OK;
     if (!d_in || !d_out) return fail(NTT_E_INVALID, "NULL buffer");
     unsigned long long* ctr = dev_counters(plan->device);
-    uint64_t need = plan->variant == NTT_SIXSTEP
-                        ? ntt_plan_workspace_bytes(plan, batch)
-                        : mp_workspace_bytes(plan->L, plan->word, plan->variant, batch, plan->p,
-                                             (reinterpret_cast<uintptr_t>(d_in) & 15) == 0);
+    uint64_t need = ntt_plan_workspace_bytes(plan, batch);
     // the O(N^2) naive DFT reads every input while writing: in place it first
     // copies the input aside (the reference is pure, algorithms.py:52-79)
     const bool naive_inplace = plan->variant == NTT_NAIVE && d_in == d_out;

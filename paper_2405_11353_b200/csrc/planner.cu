@@ -9,7 +9,6 @@ cudaError_t pointwise_f64(uint64_t, const void*, const void*, void*, uint64_t, c
 
 int mp_num_passes(int L, int word, int variant, uint64_t p) {
     if (variant == V_SIXSTEP) return 2;
-    if (clus_applies(L, variant, p, word)) return 1;
     if (fourstep_applies(L, variant, p, word)) return 2;
     if (tile_2p14_applies(L, variant, p, word)) return variant == V_FLAT ? 3 : 2;
     if (variant == V_NAIVE || L <= single_pass_max_log2(word)) return 1;
@@ -18,11 +17,10 @@ int mp_num_passes(int L, int word, int variant, uint64_t p) {
     return P + (variant == V_FLAT ? 1 : 0);
 }
 
-uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch, uint64_t p, bool in_aligned) {
+uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch, uint64_t p) {
     const uint64_t row = (1ull << L) * (uint64_t)word;
     if (variant == V_SIXSTEP) return 2 * batch * row;      // column / row passes ping-pong (tiles.cuh)
-    if (in_aligned && clus_applies(L, variant, p, word)) return 0;
-    if (fourstep_applies(L, variant, p, word)) return batch * row;       // pass A -> workspace -> pass B
+    if (fourstep_applies(L, variant, p, word)) return 2 * batch * row;   // (NTT_FOURSTEP=0 falls back to tile passes)
     if (tile_2p14_applies(L, variant, p, word)) return 2 * batch * row;
     if (variant == V_NAIVE || L <= single_pass_max_log2(word)) return 0;
     return 2 * batch * row;

@@ -678,39 +678,3 @@ def test_polymul_int32_and_length_one():
     t1 = P.cyclic_mul_ntt(torch.tensor([[5]], dtype=torch.int32).cuda(), torch.tensor([[7]], dtype=torch.int32).cuda(),
                           params)
     assert t1.cpu().tolist() == [[35]]
-
-
-@pytest.mark.parametrize("variant", ["dit", "dif", "pease_nc", "flat"])
-@pytest.mark.parametrize("field,L", [("p998", 15), ("p998", 16), ("default", 15), ("default", 16),
-                                     ("babybear", 16), ("goldilocks", 14), ("goldilocks", 15),
-                                     ("goldilocks", 16)])
-def test_cluster_single_pass(fields, variant, field, L):
-    """One pass on a thread-block cluster (fastclus.cuh: the CTAs exchange
-    through distributed shared memory): a batch larger than the co-resident
-    clusters (every cluster loops), forward / unscaled inverse / intt, in place
-    and 4-byte-aligned (the two-pass fallback) against the oracle."""
-    _, p, g, w, dt, _ = fields[field]
-    B = 300 if L <= 15 else 150
-    x = rand(p, B, L, dt, 9000 + L)
-    want = O.ntt(x, p, g, w, variant)
-    assert np.array_equal(gpu_ntt(x, p, g, w, variant), want), (field, variant, L)
-    assert np.array_equal(gpu_ntt(x[:5], p, g, w, variant, inverse=True),
-                          O.ntt(x[:5], p, g, w, variant, inverse=True)), (field, variant, L)
-    assert np.array_equal(gpu_ntt(x[:5], p, g, w, variant, inverse=True, scale=True),
-                          O.ntt(x[:5], p, g, w, variant, inverse=True, scale=True)), (field, variant, L)
-    plan = P.make_plan(P.FieldParams(p, g, w), variant, 1 << L)
-    dp = P.algorithms.device_plan_for(plan, np.dtype(dt).itemsize, 0)
-    assert dp.info.passes == 1
-    s = torch.cuda.current_stream().cuda_stream
-    d = to_dev(x[:7])
-    dp.exec_device(d.data_ptr(), d.data_ptr(), 7, False, s)
-    assert np.array_equal(to_host(d), want[:7]), ("in-place", field, variant, L)
-    W = np.dtype(dt).itemsize
-    idt = torch.int32 if W == 4 else torch.int64
-    big = torch.zeros(3 * (1 << L) + 1, dtype=idt, device="cuda")
-    big[1:] = torch.from_numpy(x[:3].view(np.int32 if W == 4 else np.int64).reshape(-1)).cuda()
-    out = torch.zeros_like(big)
-    dp.exec_device(big.data_ptr() + W, out.data_ptr() + W, 3, False, s)
-    torch.cuda.synchronize()
-    got = out[1:].cpu().numpy().view(dt).reshape(3, -1)
-    assert np.array_equal(got, want[:3]), ("misaligned", field, variant, L)
