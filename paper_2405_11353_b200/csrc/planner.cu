@@ -20,7 +20,7 @@ int mp_num_passes(int L, int word, int variant, uint64_t p) {
 uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch, uint64_t p) {
     const uint64_t row = (1ull << L) * (uint64_t)word;
     if (variant == V_SIXSTEP) return 2 * batch * row;      // column / row passes ping-pong (tiles.cuh)
-    if (fourstep_applies(L, variant, p, word)) return 2 * batch * row;   // (NTT_FOURSTEP=0 falls back to tile passes)
+    if (fourstep_applies(L, variant, p, word)) return batch * row;       // pass A -> workspace -> pass B
     if (tile_2p14_applies(L, variant, p, word)) return 2 * batch * row;
     if (variant == V_NAIVE || L <= single_pass_max_log2(word)) return 0;
     return 2 * batch * row;
