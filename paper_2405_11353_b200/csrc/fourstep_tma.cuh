@@ -68,8 +68,10 @@ struct TmaGeo {
     static constexpr int KG0 = (V == V_DIT) ? K0 : 4;
     static constexpr int KGL = (V == V_DIT) ? 4 : K0;
     static constexpr int NPM = (K == 10 && V != V_DIT) ? 2 : 1;       // network stride mod 32
-    static constexpr int NP = ((fastk::padded_len<uint32_t, K>() + 8 + 31) / 32) * 32 + NPM;
     static constexpr bool NLIN = (K == 9 && V == V_DIT);              // base(q) = q*NP + 8*(q >> 3)
+    // (the +8 only where the non-linear base needs it: at K = 10 the 32 words saved per
+    // network are what lets a third 512-thread CTA fit the SM's shared memory)
+    static constexpr int NP = ((fastk::padded_len<uint32_t, K>() + (NLIN ? 8 : 0) + 31) / 32) * 32 + NPM;
     static constexpr int I0a = 4, I0b = 5;                            // group-0 in-warp -> u bits
     static constexpr int ILa = (V == V_DIT) ? (K == 10 ? 3 : 3) : 0;  // last group
     static constexpr int ILb = (V == V_DIT) ? 4 : 1;

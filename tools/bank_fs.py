@@ -33,8 +33,8 @@ def geometry(V, K):
     KG0 = K0 if V == "dit" else 4
     KGL = 4 if V == "dit" else K0
     NPM = 2 if (K == 10 and V != "dit") else 1
-    NP = ((padded_len(K) + 8 + 31) // 32) * 32 + NPM
     nlin = (K == 9 and V == "dit")
+    NP = ((padded_len(K) + (8 if nlin else 0) + 31) // 32) * 32 + NPM
     I0 = (4, 5)
     IL = (3, 4) if V == "dit" else (0, 1)
     return dict(TQ=TQ, LQ=LQ, AB=AB, KG0=KG0, KGL=KGL, NP=NP, nlin=nlin, I0=I0, IL=IL,

@@ -2,7 +2,7 @@
 launches (rotating input/output sets > L2) inside a cudaProfilerStart/Stop
 range, for `ncu --replay-mode range` (a single-launch capture under-reads the
 writes still sitting in L2 when the launch ends).
-    ncu --profile-from-start off --replay-mode range --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+    ncu --replay-mode app-range --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
         python tools/traffic_range.py CFG VARIANT [K]"""
 import os, sys
 import numpy as np, torch
