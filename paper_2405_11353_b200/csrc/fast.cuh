@@ -24,8 +24,13 @@
 #include "engine.cuh"
 #include "lazy.cuh"
 
+#ifndef NTT_FAST_EARLY_LOAD
+#define NTT_FAST_EARLY_LOAD 1   // deferred-wait launches issue their first rows before the table copy
+#endif
 
 namespace nttb200 {
+// launch window (planner.cu): may this fast-kernel launch defer its dependency wait?
+bool window_admit(cudaStream_t stream, const void* in, const void* out, uint64_t bytes, bool exclusive);
 namespace fastk {
 
 NTT_D uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -74,6 +79,16 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+
+// per-SM phase timestamps (tools/fast_timeline.py; experiment builds only)
+#ifdef NTT_FAST_TIMELINE
+static __device__ unsigned long long g_tl[256 * 64];
+NTT_D unsigned smid() { unsigned sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); return sm; }
+NTT_D unsigned long long gtime() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
+#define NTT_TL(team, k) g_tl[fastk::smid() * 64 + (team) * 8 + (k)] = fastk::gtime()
+#else
+#define NTT_TL(team, k) ((void)0)
+#endif
 
 NTT_D void team_sync(int id, int nthreads) {
     if (nthreads == 32) __syncwarp();
@@ -163,6 +178,7 @@ struct FastArgs {
     int scale;
     Tw ninv;
     unsigned long long* counters;
+    int defer = 0;         // dependency wait at the kernel's end (see k_fast)
 };
 
 // Stage twiddles: stages s <= LS read the shared-memory copy of the per-stage
@@ -353,33 +369,47 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
     A ar;
     ar.init(a.p);
 
-    // twiddle table once per CTA (a thread loop: a bulk async copy measured the
-    // same, the prologue overlaps the previous launch's tail under PDL); barriers
-    for (int i = threadIdx.x; i < NTS; i += blockDim.x) stw[i] = a.stw[i];
-    if (t == 0) { mbar_init(&mbar[2 * team], 1); mbar_init(&mbar[2 * team + 1], 1); }
-    fence_mbar_init();
-    __syncthreads();
-    // programmatic dependent launch: the prologue above (plan-owned tables only)
-    // overlaps the previous launch's tail; its outputs are visible after the wait.
-    // (Issuing the first TMA loads before the table copy moves the copy behind
-    // the wait: config 2 37.1 vs 34.6 us per step, measured A/B.)
-    // trigger, then wait (the opposite order measured the same: config 2,
-    // 5 x 2 runs of 1000 steps, 34.95 vs 35.07 us/step)
-    pdl_trigger();
-    pdl_wait();
-
+#ifdef NTT_FAST_TIMELINE
+    if (t == 0) { g_tl[smid() * 64 + team * 8 + 7] = g_tl[smid() * 64 + team * 8 + 5]; NTT_TL(team, 0); }
+#endif
     const uint64_t stride = (uint64_t)gridDim.x * TEAMS;
     uint64_t poly = (uint64_t)blockIdx.x * TEAMS + team;
     const uint32_t bytes = N * sizeof(T);
-    if (STG_ && t == 0 && poly < a.batch) {
-        mbar_expect_tx(&mbar[2 * team], PW ? 2 * bytes : bytes);
-        tma_load_1d(S, a.in + poly * N, bytes, &mbar[2 * team]);
-        if (PW) tma_load_1d(S + N, a.in2 + poly * N, bytes, &mbar[2 * team]);
-        if (DS && poly + stride < a.batch) {
-            mbar_expect_tx(&mbar[2 * team + 1], bytes);
-            tma_load_1d(S + N, a.in + (poly + stride) * N, bytes, &mbar[2 * team + 1]);
+    auto first_loads = [&]() {          // this team's first row (and the one after it)
+        if (STG_ && t == 0 && poly < a.batch) {
+            mbar_expect_tx(&mbar[2 * team], PW ? 2 * bytes : bytes);
+            tma_load_1d(S, a.in + poly * N, bytes, &mbar[2 * team]);
+            if (PW) tma_load_1d(S + N, a.in2 + poly * N, bytes, &mbar[2 * team]);
+            if (DS && poly + stride < a.batch) {
+                mbar_expect_tx(&mbar[2 * team + 1], bytes);
+                tma_load_1d(S + N, a.in + (poly + stride) * N, bytes, &mbar[2 * team + 1]);
+            }
         }
+    };
+    if (t == 0) { mbar_init(&mbar[2 * team], 1); mbar_init(&mbar[2 * team + 1], 1); }
+    fence_mbar_init();
+    // Programmatic dependent launch.  a.defer (host-checked, ntt_api.cu launch_window: this
+    // launch's buffers are disjoint from those of every launch on the stream that may still
+    // be running): the rows start loading at once, under the previous launch's tail, and the
+    // dependency wait moves to the kernel's end (a grid never completes before its
+    // predecessor, so stream order holds for whatever follows).  Otherwise the prologue
+    // (plan-owned tables only) overlaps the previous launch's tail, the wait precedes the
+    // first input read and the trigger follows the wait (a dependent of a waiting launch
+    // never overlaps the launch before it).
+    if (a.defer) {
+        pdl_trigger();
+        if (NTT_FAST_EARLY_LOAD) first_loads();
     }
+    // twiddle table once per CTA (a thread loop: a bulk async copy measured the same)
+    for (int i = threadIdx.x; i < NTS; i += blockDim.x) stw[i] = a.stw[i];
+    __syncthreads();
+    if (t == 0) NTT_TL(team, 1);
+    if (!a.defer) {
+        pdl_wait();
+        pdl_trigger();
+    }
+    if (t == 0) NTT_TL(team, 2);
+    if (!a.defer || !NTT_FAST_EARLY_LOAD) first_loads();
     uint32_t it = 0;
     int copies = 0;
     const int bar_id = 1 + team;
@@ -388,6 +418,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
         T v[RV];
         const uint32_t sb_ = DS ? (it & 1) : 0;     // staging buffer of this polynomial
         if (STG_) mbar_wait(&mbar[2 * team + sb_], DS ? ((it >> 1) & 1) : (it & 1));
+        if (it == 0 && t == 0) NTT_TL(team, 3);
         ++it;
         T* Sb = S + sb_ * N;
         const T* S0 = STG_ ? Sb : a.in + poly * N;   // first-group source
@@ -584,6 +615,7 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
         // work buffers free for the next row: with a staging buffer the next
         // row's "staging consumed" barrier (after its first gather, before its
         // first scatter) already orders every read of this row's last group
+        if (it == 1 && t == 0) NTT_TL(team, 4);
         if (!STG_) team_sync(bar_id, TT);
         if (a.counters && t == 0) {
             atomicAdd(a.counters + C_TRANSFORMS, 1ull);
@@ -592,6 +624,8 @@ __global__ void __launch_bounds__(TEAMS*(1 << (L - RB)), 1) k_fast(FastArgs<A> a
             if (V == V_PEASE) { atomicAdd(a.counters + C_COPIES, (unsigned long long)copies); copies = 0; }
         }
     }
+    if (t == 0) NTT_TL(team, 5);
+    if (a.defer && threadIdx.x == 0) pdl_wait();
 }
 
 // ------------------------------------------------------------- launcher --
@@ -638,6 +672,8 @@ struct FastCfg {
     static constexpr long smem = table + (long)TEAMS * team_bytes;
 };
 
+template <class A, int L>
+constexpr uint64_t N_BYTES() { return (uint64_t)sizeof(typename A::T) << L; }
 template <class A, int V, int L>
 cudaError_t launch_fast_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int* launches, bool* ok) {
     using C = FastCfg<A, V, L>;
@@ -656,7 +692,12 @@ cudaError_t launch_fast_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int
         uint64_t grid = ctas < cap ? ctas : cap;
         *ok = true;
         if (grid == 0) return cudaSuccess;
-        cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(C::TEAMS * C::TT), C::smem, s, a);
+        // launch window (planner.cu): defer the dependency wait when the buffers are disjoint from
+        // every launch that may still run; a launch of one CTA per SM on every SM is exclusive
+        FastArgs<A> al = a;
+        al.defer = nttb200::window_admit(s, a.in, a.out, a.batch * N_BYTES<A, L>(), occ == 1 && 2 * C::smem > 228 * 1024 &&
+                                                                            grid == (uint64_t)num_sms) ? 1 : 0;
+        cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(C::TEAMS * C::TT), C::smem, s, al);
         if (launches) ++*launches;
         return le != cudaSuccess ? le : cudaGetLastError();
     }

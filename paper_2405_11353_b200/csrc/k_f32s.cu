@@ -21,3 +21,8 @@ cudaError_t pointwise_f32s(uint64_t p, const void* a, const void* b, void* c, ui
     return pointwise_field<F32S>(p, a, b, c, n, s, num_sms, launches);
 }
 }  // namespace nttb200
+#ifdef NTT_FAST_TIMELINE
+extern "C" int ntt_debug_timeline(unsigned long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, nttb200::fastk::g_tl, sizeof(unsigned long long) * n);
+}
+#endif

@@ -326,6 +326,13 @@ struct MultipassReq {
     const void* fst;           // four-step twist table [k1][n2] = w^(k1*n2) (fourstep.cuh), or null
 };
 
+// Launch window (planner.cu): may a fast-kernel launch defer its dependency wait
+// to its end?  window_admit registers a launch on the current device's `stream`
+// (exclusive: one CTA per SM on every SM); window_break ends the run (any launch
+// the window does not model).
+bool window_admit(cudaStream_t stream, const void* in, const void* out, uint64_t bytes, bool exclusive);
+void window_break(cudaStream_t stream);
+
 // pass count / workspace of a plan (single pass: shared-memory resident, no workspace)
 int mp_num_passes(int L, int word, int variant, uint64_t p);
 uint64_t mp_workspace_bytes(int L, int word, int variant, uint64_t batch, uint64_t p);

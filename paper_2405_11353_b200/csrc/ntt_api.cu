@@ -549,6 +549,11 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
     r.ninv = plan->table->n_inv; r.ninv_shoup = plan->table->n_inv_dev_shoup;
     r.counters = ctr; r.stream = stream; r.num_sms = plan->num_sms; r.launches = &launches;
     r.ws = ws;
+    // launch window (planner.cu): single-pass launches register themselves in the fast
+    // kernel's launcher; every other launch on the stream ends the run of deferred waits
+    if (plan->variant == NTT_SIXSTEP || plan->variant == NTT_NAIVE ||
+        mp_num_passes(plan->L, plan->word, plan->variant, plan->p) != 1)
+        window_break(stream);
     r.twh = plan->twh;
     r.twh_bits = plan->twh_bits;
     r.fst = plan->fst;
@@ -784,6 +789,7 @@ static int dist_step(ntt_plan_t plan, int step, int rank, int world, const void*
         r.ws = slot.first;
     }
     bool ok = false;
+    window_break(r.stream);
     cudaError_t e = tile_sixstep_dist_gold(r, step, rank, world, d_in, d_out, &ok, d_peers);
     g_launches += launches;
     if (cur != plan->device) cudaSetDevice(cur);
@@ -824,6 +830,7 @@ int ntt_exec_pointwise_inverse(ntt_plan_t plan, const void* d_a, const void* d_b
         r.tw = plan->table->tw; r.stw = plan->table->stw; r.p = plan->p; r.scale = 1;
         r.ninv = ninv_m; r.ninv_shoup = shoup_word(ninv_m, plan->p, 32);
         r.counters = dev_counters(plan->device); r.stream = s; r.num_sms = plan->num_sms; r.launches = &launches;
+        window_break(s);
         cudaError_t e = pointwise_inverse_f32(r, d_b, &done);
         g_launches += launches;
         if (e != cudaSuccess) st = cuda_fail(e, "pointwise-inverse");
@@ -846,6 +853,7 @@ int ntt_exec_pointwise_inverse(ntt_plan_t plan, const void* d_a, const void* d_b
 int ntt_pointwise_mul(ntt_plan_t plan, const void* d_a, const void* d_b, void* d_c, uint64_t count, void* stream) {
     if (!plan) return fail(NTT_E_INVALID, "NULL plan");
     int launches = 0;
+    window_break(static_cast<cudaStream_t>(stream));
     cudaError_t e = pointwise_launch(plan->kind, plan->p, d_a, d_b, d_c, count,
                                      static_cast<cudaStream_t>(stream), plan->num_sms, &launches);
     g_launches += launches;

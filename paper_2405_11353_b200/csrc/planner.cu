@@ -1,7 +1,60 @@
 // Host-side plan queries shared by the C ABI (pass counts, workspace sizes)
 // and the field-dispatched pointwise multiply.
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
+#include <vector>
 #include "launch.cuh"
 namespace nttb200 {
+
+// ---- launch window: may a single-pass launch defer its dependency wait? ----
+// Every fast / tile / four-step kernel is launched with programmatic stream
+// serialisation.  A fast-kernel launch whose buffers are disjoint from those of
+// every launch that may still be running on its stream loads its first rows at
+// once, under its predecessor's tail, and waits for the predecessor only at its
+// end (fast.cuh k_fast, a.defer), so grids still complete in stream order.
+// What may still be running when launch m starts: launch m - 1 and -- when
+// m - 1 deferred its wait too -- whatever m - 1 could overlap: the run of
+// deferred launches before m back to the waiting launch that started it (a
+// waiting launch triggers its dependents after its wait, so nothing older
+// overlaps them).  An EXCLUSIVE launch (one CTA per SM by shared memory, on
+// every SM) cuts the run short: m starts only after every CTA of m - 1 has
+// started, i.e. after every CTA of the launches before m - 1 has left its SM.
+// Launches the window does not model (multi-pass, pointwise, distributed
+// steps) end the run; the next single-pass launch waits at its start.
+namespace {
+struct LaunchSpan { const char *in0, *in1, *out0, *out1; bool exclusive; };
+std::mutex g_run_mu;
+std::map<std::pair<int, cudaStream_t>, std::vector<LaunchSpan>> g_runs;
+constexpr size_t kMaxRun = 16;
+inline bool overlap(const char* a0, const char* a1, const char* b0, const char* b1) { return a0 < b1 && b0 < a1; }
+inline int current_device() { int d = 0; cudaGetDevice(&d); return d; }
+}  // namespace
+
+void window_break(cudaStream_t stream) {
+    std::lock_guard<std::mutex> lk(g_run_mu);
+    auto it = g_runs.find({current_device(), stream});
+    if (it != g_runs.end()) it->second.clear();
+}
+
+bool window_admit(cudaStream_t stream, const void* in, const void* out, uint64_t bytes, bool exclusive) {
+    static const bool on = [] { const char* e = getenv("NTT_PDL_DEFER"); return !e || atoi(e) != 0; }();
+    const LaunchSpan me{static_cast<const char*>(in), static_cast<const char*>(in) + bytes,
+                        static_cast<const char*>(out), static_cast<const char*>(out) + bytes, exclusive};
+    std::lock_guard<std::mutex> lk(g_run_mu);
+    std::vector<LaunchSpan>& run = g_runs[{current_device(), stream}];
+    if (!run.empty() && run.back().exclusive) run.erase(run.begin(), run.end() - 1);
+    bool defer = on && !run.empty() && run.size() < kMaxRun;
+    for (const LaunchSpan& o : run)
+        if (overlap(me.in0, me.in1, o.out0, o.out1) || overlap(me.out0, me.out1, o.out0, o.out1) ||
+            overlap(me.out0, me.out1, o.in0, o.in1))
+            defer = false;
+    if (!defer) run.clear();            // this launch waits at its start: it begins a new run
+    run.push_back(me);
+    return defer;
+}
+
 cudaError_t pointwise_f32s(uint64_t, const void*, const void*, void*, uint64_t, cudaStream_t, int, int*);
 cudaError_t pointwise_f32w(uint64_t, const void*, const void*, void*, uint64_t, cudaStream_t, int, int*);
 cudaError_t pointwise_gold(uint64_t, const void*, const void*, void*, uint64_t, cudaStream_t, int, int*);

@@ -678,3 +678,50 @@ def test_polymul_int32_and_length_one():
     t1 = P.cyclic_mul_ntt(torch.tensor([[5]], dtype=torch.int32).cuda(), torch.tensor([[7]], dtype=torch.int32).cuda(),
                           params)
     assert t1.cpu().tolist() == [[35]]
+
+
+@pytest.mark.parametrize("variant", ["pease_nc", "dit", "dif"])
+def test_launch_window_dependencies(variant):
+    """Back-to-back single-pass launches on one stream, with no host sync in
+    between: independent launches defer their dependency wait (ntt_api.cu launch
+    window), launches that read, overwrite or alias a buffer of a launch that may
+    still be running must not.  Chains (out -> in), write-after-read, write-after-write,
+    in-place and a multi-pass launch in the middle, all bit-exact."""
+    p, g, L, B = 998244353, 3, 12, 2048
+    n = 1 << L
+    params = P.FieldParams(p, g)
+    dpf = P.algorithms.device_plan_for(P.make_plan(params, variant, n), 4, 0)
+    dpi = P.algorithms.device_plan_for(P.make_plan(params, variant, n, P.INVERSE), 4, 0)
+    dpl = P.algorithms.device_plan_for(P.make_plan(params, "pease_nc", 1 << 15), 4, 0)   # multi-pass
+    x = [rand(p, B, L, np.uint32, 7100 + i) for i in range(3)]
+    X = [O.ntt(v, p, g, 32, variant) for v in x]
+    st = torch.cuda.Stream()
+    s = st.cuda_stream
+    with torch.cuda.stream(st):
+        a = [to_dev(v) for v in x]
+        b = [torch.empty_like(a[0]) for _ in range(3)]
+        c = torch.empty_like(a[0])
+        big = to_dev(rand(p, 8, 15, np.uint32, 7200))
+        bigo = torch.empty_like(big)
+        st.synchronize()
+        for rep in range(6):
+            # independent launches (disjoint buffers): deferred waits
+            for i in range(3):
+                dpf.exec_device(a[i].data_ptr(), b[i].data_ptr(), B, False, s)
+            # read-after-write chain: c = intt(b[0]) must see launch 0's output
+            dpi.exec_device(b[0].data_ptr(), c.data_ptr(), B, True, s)
+            # write-after-read: overwrite b[0] (still being read by the inverse) with X[1]
+            dpf.exec_device(a[1].data_ptr(), b[0].data_ptr(), B, False, s)
+            # write-after-write on b[0], then in place on b[2] (forward of X[2] twice... inverse restores)
+            dpf.exec_device(a[2].data_ptr(), b[0].data_ptr(), B, False, s)
+            dpi.exec_device(b[2].data_ptr(), b[2].data_ptr(), B, True, s)
+            # a multi-pass launch ends the run; the next single-pass launch reads its neighbour's output
+            dpl.exec_device(big.data_ptr(), bigo.data_ptr(), 8, False, s)
+            dpf.exec_device(b[2].data_ptr(), b[2].data_ptr(), B, False, s)
+            st.synchronize()
+            assert np.array_equal(to_host(c), x[0]), ("raw", rep)
+            assert np.array_equal(to_host(b[0]), X[2]), ("waw", rep)
+            assert np.array_equal(to_host(b[1]), X[1]), ("independent", rep)
+            assert np.array_equal(to_host(b[2]), X[2]), ("in place", rep)
+            for i in range(3):
+                assert np.array_equal(to_host(a[i]), x[i]), ("inputs untouched", rep)
