@@ -1,0 +1,282 @@
+// colpass.cuh -- column passes of the six-step for 64-bit fields (config 5:
+// the 2^13 x 2^13 Goldilocks split), the TL_COLS passes of fasttile.cuh
+// rebuilt around TMA tensor boxes.
+//
+// One pass = K consecutive DIT stages (S0+1 .. S0+K) of the length-2^L
+// transforms down EVERY column of a row-major [2^L][2^l1] matrix (element
+// (j, i) at j * 2^l1 + i; algorithms.py:371-389 reads x[j*n1 + i] this way).
+// A tile is one network id Qj (the position bits outside [S0, S0+K)) times TQ
+// consecutive columns: 2^K rows x TQ columns = 2^12 residues = 32 KiB.
+//
+//  * the tile is ONE 4-D tensor box [1][2^K][1][TQ] in (cp.async.bulk.tensor,
+//    mbarrier completion) and one out; the bit reversal of a sub-transform's
+//    input (pass 1) is a tensor-map view: j = jh * 2^(L-K) + jl puts the rows
+//    of a network 2^(L-K) apart, and the box delivers them ordered by
+//    jh = brev_K(x);
+//  * work layout = the dense box [row][column]: a warp's lanes run along the
+//    columns, so every shared-memory access of every register group is
+//    conflict-free without padding (the network-major layout of k_tile
+//    showed 37-40 % conflicting wavefronts here, profiles/r2);
+//  * the stage twiddles of a thread depend on its rows only, never on its
+//    column: warp-uniform 8-byte broadcasts from a 2^K-entry table that is
+//    rebuilt per tile for the later pass (T[2^(s-1) + qlo + 2^S0 m], 63
+//    entries) -- no twiddle ever comes from global memory inside a group;
+//  * the six-step correction w_N^(i k2) of a thread's 16 outputs is a
+//    geometric sequence in the register index (k2 = k2_0 + c 2^(S0+K-4)): two
+//    table look-ups per THREAD (first term, ratio) instead of two per residue;
+//  * 64 registers, 34 KiB: four to six 256-thread CTAs per SM overlap one
+//    another's tile loads / stores.
+//
+// Stage-faithful and interchangeable with the k_tile passes: the HBM buffer
+// after a pass holds the same (canonical) residues.
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include "fasttile.cuh"
+
+#ifndef NTT_COLS_MINB
+#define NTT_COLS_MINB 4        // resident CTAs the column-pass kernel is compiled for (64 registers)
+#endif
+
+namespace nttb200 {
+namespace cpass {
+
+NTT_D void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+            "r"(fastk::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(fastk::smem_u32(bar))
+        : "memory");
+}
+NTT_D void tma_store_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3, const void* src) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(fastk::smem_u32(src))
+                 : "memory");
+}
+NTT_D void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+NTT_D void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+NTT_D void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <class A>
+struct ColArgs {
+    using T = typename A::T;
+    using Tw = typename A::Tw;
+    uint64_t batch;
+    int L, S0, l1;             // sub-transform length 2^L, stages done before this pass, log2 columns
+    const Tw* gstw;            // per-stage table of the length-2^L transform
+    int cor_on;                // multiply by w_N^(i * k2) (the last pass of step A)
+    const T* cor_lo;           // w_N^e = cor_hi[e >> cor_lb] * cor_lo[e mod 2^cor_lb]
+    const T* cor_hi;
+    int cor_lb, cor_lgn;       // log2 N of the correction root
+    uint32_t qoff;             // global index of local column 0 (distributed slabs)
+    int scale;
+    Tw ninv;
+    int count_row, count_bitrev;
+    unsigned long long* counters;
+    uint64_t p;
+};
+
+template <int K, int TQ>
+constexpr size_t cols_smem_bytes() { return ((size_t)8 << K) * TQ + 128; }
+
+// FIRST: S0 == 0 (stage 1's twiddles are 1, the input rows arrive bit-reversed)
+template <class A, int K, int TQ, bool FIRST>
+__global__ void __launch_bounds__(256, NTT_COLS_MINB)
+    k_cols(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUtensorMap mout, ColArgs<A> a) {
+    using T = typename A::T;
+    using Tw = typename A::Tw;
+    static_assert(sizeof(T) == 8 && sizeof(Tw) == 8, "64-bit residues with bare-power twiddles");
+    constexpr int NT = 256, TT = 1 << (K - 4), LTQ = ftile::ilog2c(TQ);
+    static_assert(TT * TQ == NT && TQ >= 16, "2^12-residue tiles, lanes along the columns");
+    constexpr int G = (K + 3) / 4, K0 = K - 4 * (G - 1);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ Tw TL[1 << K];                 // TL[2^sl + m]: twiddle of local stage sl + 1, local index m
+    __shared__ __align__(8) uint64_t mbar;
+    T* S = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+    A ar;
+    ar.init(a.p);
+    const uint32_t tid = threadIdx.x, t = tid % TQ, u = tid / TQ;
+    const int L = a.L, S0 = FIRST ? 0 : a.S0, l1 = a.l1;
+    const int ltpr = l1 + L - K - LTQ;                    // log2 tiles per matrix
+    const uint64_t ntiles = a.batch << ltpr;
+    const int lrest = L - K - S0;                         // bits of the network id above the pass's window
+    if (FIRST)
+        for (uint32_t e = tid; e < (1u << K); e += NT) TL[e] = a.gstw[e];
+    if (tid == 0) {
+        fastk::mbar_init(&mbar, 1);
+        fastk::fence_mbar_init();
+    }
+    __syncthreads();
+    fastk::pdl_trigger();
+    fastk::pdl_wait();                       // the previous pass's output (our input) is visible
+
+    uint32_t phase = 0;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t b = tile >> ltpr;
+        const uint32_t tr = (uint32_t)(tile & ((1ull << ltpr) - 1));
+        const uint32_t Qj = tr >> (l1 - LTQ), col0 = (tr << LTQ) & ((1u << l1) - 1);
+        const uint32_t qlo = Qj & ((1u << S0) - 1), qhi = Qj >> S0;
+        const int c3 = (int)((b << lrest) + qhi);
+        if (tid == 0) {
+            bulk_wait_read();                // the previous tile's store has read the buffer
+            fastk::mbar_expect_tx(&mbar, (uint32_t)(sizeof(T) << K) * TQ);
+            if (FIRST) tma_load_4d(S, &min, (int)col0, (int)brev(Qj, L - K), 0, (int)b, &mbar);
+            else tma_load_4d(S, &min, (int)col0, (int)qlo, 0, c3, &mbar);
+        }
+        if (!FIRST) {                        // this tile's twiddles: stage S0+sl+1, index qlo + 2^S0 m
+            for (uint32_t e = tid + 1; e < (1u << K); e += NT) {
+                const int sl = 31 - __clz(e);
+                TL[e] = __ldg(a.gstw + ((1u << (S0 + sl)) + qlo + ((e - (1u << sl)) << S0)));
+            }
+            __syncthreads();
+        }
+        T v[16];
+        fastk::mbar_wait(&mbar, phase);
+        phase ^= 1;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int B = g == 0 ? 0 : K0 + 4 * (g - 1);          // register block [B, B+4) of the row index
+            const int kg = g == 0 ? K0 : 4, b0 = g == 0 ? 0 : B;  // stages b0+1 .. b0+kg (local)
+            const uint32_t pbase = (u & ((1u << B) - 1)) | ((u >> B) << (B + 4));
+            if (g == 0 && FIRST) {
+                // staged row r holds x = brev_K(r); x = u << 4 | c  ->  r = brev4(c) << (K-4) | brev(u)
+                const T* sp = S + (size_t)brev(u, K - 4) * TQ + t;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) v[c] = sp[(size_t)(brev((uint32_t)c, 4) << (K - 4)) * TQ];
+                __syncthreads();             // every row read before the rows are rewritten in natural order
+            } else {
+                const T* sp = S + (size_t)pbase * TQ + t;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) v[c] = sp[(size_t)((uint32_t)c << B) * TQ];
+            }
+#pragma unroll
+            for (int jj = 0; jj < kg; ++jj) {
+                const int sl = b0 + jj, j = sl - B;                // local stage bit, its register bit
+                const uint32_t lmask = (1u << sl) - 1;
+                const Tw* row = TL + (1u << sl) + (pbase & lmask);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    if (c & (1 << j)) continue;
+                    const int hi = c | (1 << j);
+                    if (FIRST && sl == 0) ar.dit1(v[c], v[hi]);
+                    else ar.dit(v[c], v[hi], ftile::lds_tw(row + (((uint32_t)c << B) & lmask)));
+                }
+            }
+            if (g == G - 1) {
+                // ---- outputs: correction / n^-1 / canonical form, back into the tile for the store
+                if (a.cor_on) {
+                    // k2(c) = qlo | x << S0 | qhi << (S0+K), x = pbase | c << B; w_N^(i k2(c)) = f0 * r^c
+                    const uint64_t nm = (1ull << a.cor_lgn) - 1, lm = (1ull << a.cor_lb) - 1;
+                    const uint64_t i = (uint64_t)a.qoff + col0 + t;
+                    const uint64_t k20 = (uint64_t)qlo | ((uint64_t)pbase << S0) | ((uint64_t)qhi << (S0 + K));
+                    const uint64_t e0 = (i * k20) & nm, es = (i << (S0 + B)) & nm;
+                    T f = ar.mulfull(__ldg(a.cor_hi + (e0 >> a.cor_lb)), __ldg(a.cor_lo + (e0 & lm)));
+                    const T r = ar.mulfull(__ldg(a.cor_hi + (es >> a.cor_lb)), __ldg(a.cor_lo + (es & lm)));
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        v[c] = ar.mulfull(v[c], f);
+                        if (c < 15) f = ar.mulfull(f, r);
+                    }
+                } else if (a.scale) {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) v[c] = ar.mulc(v[c], a.ninv);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) v[c] = ar.fin(v[c]);
+                }
+            }
+            T* dp = S + (size_t)pbase * TQ + t;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) dp[(size_t)((uint32_t)c << B) * TQ] = v[c];
+            if (g == G - 1) fastk::fence_proxy_async();     // generic writes -> the bulk store's reads
+            __syncthreads();
+        }
+        if (tid == 0) {
+            tma_store_4d(&mout, (int)col0, (int)qlo, 0, c3, S);
+            bulk_commit();
+        }
+        if (a.counters && tid == 0 && tr == 0) {
+            atomicAdd(a.counters + C_HBM, 1ull);
+            if (a.count_row) atomicAdd(a.counters + C_TRANSFORMS, 1ull);
+            if (a.count_bitrev) atomicAdd(a.counters + C_BITREV, (unsigned long long)a.count_bitrev);
+        }
+    }
+    if (tid == 0) bulk_wait_all();
+}
+
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// 4-D view [d3][2^K rows][d1][2^l1 columns] of a matrix, boxes [1][2^K][1][TQ]
+inline bool cols_map(CUtensorMap* m, const void* base, int l1, uint64_t d1, int K, uint64_t d3, int TQ) {
+    auto enc = tensor_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)1 << l1, d1, (cuuint64_t)1 << K, d3};
+    cuuint64_t strides[3] = {((cuuint64_t)8 << l1), ((cuuint64_t)8 << l1) * d1, (((cuuint64_t)8 << l1) * d1) << K};
+    cuuint32_t box[4] = {(cuuint32_t)TQ, 1, (cuuint32_t)1 << K, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// *ok = false when the pass is not covered (the caller falls back to k_tile)
+template <class A, int K>
+cudaError_t launch_cols(const ftile::TileArgs<A>& ta, cudaStream_t s, int num_sms, int* launches, bool* ok) {
+    using T = typename A::T;
+    *ok = false;
+    if constexpr (sizeof(T) != 8 || sizeof(typename A::Tw) != 8 || K < 6 || K > 8) return cudaSuccess;
+    else {
+        constexpr int TQ = 1 << (12 - K);
+        static const bool on = [] { const char* e = getenv("NTT_COLS_TMA"); return !e || atoi(e) != 0; }();
+        const int L = ta.L, S0 = ta.S0, l1 = ta.l1;
+        if (!on || l1 < 12 - K || L < K + S0 || (S0 == 0) != (ta.rev_in != 0) || ta.twist) return cudaSuccess;
+        if ((reinterpret_cast<uintptr_t>(ta.in) | reinterpret_cast<uintptr_t>(ta.out)) & 15) return cudaSuccess;
+        const int lrest = L - K - S0;
+        if ((ta.batch << lrest) >= (1ull << 31)) return cudaSuccess;
+        CUtensorMap min, mout;
+        // pass 1 reads j = brev_L(pos): rows of a network 2^(L-K) apart, networks by brev(Qj)
+        const bool mi = S0 == 0 ? cols_map(&min, ta.in, l1, 1ull << (L - K), K, ta.batch, TQ)
+                                : cols_map(&min, ta.in, l1, 1ull << S0, K, ta.batch << lrest, TQ);
+        if (!mi || !cols_map(&mout, ta.out, l1, 1ull << S0, K, ta.batch << lrest, TQ)) return cudaSuccess;
+        ColArgs<A> a{};
+        a.batch = ta.batch; a.L = L; a.S0 = S0; a.l1 = l1;
+        a.gstw = ta.gstw;
+        a.cor_on = ta.cor_on; a.cor_lo = ta.cor_lo; a.cor_hi = ta.cor_hi; a.cor_lb = ta.cor_lb;
+        a.cor_lgn = ta.cor_lgn ? ta.cor_lgn : L + l1;
+        a.qoff = (uint32_t)ta.qoff;
+        a.scale = ta.scale; a.ninv = ta.ninv;
+        a.count_row = ta.count_row; a.count_bitrev = ta.count_bitrev; a.counters = ta.counters;
+        a.p = ta.p;
+        constexpr size_t smem = cols_smem_bytes<K, TQ>();
+        auto launch = [&](auto kern) -> cudaError_t {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int occ = 0;
+            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+            if (e != cudaSuccess) return e;
+            if (occ < 1) occ = 1;
+            const uint64_t ntiles = ta.batch << (l1 + L - K - (12 - K));
+            uint64_t grid = (uint64_t)num_sms * occ;
+            if (grid > ntiles) grid = ntiles;
+            if (grid == 0) return cudaSuccess;
+            e = fastk::launch_pdl(kern, dim3((unsigned)grid), dim3(256), smem, s, min, mout, a);
+            if (launches) ++*launches;
+            return e != cudaSuccess ? e : cudaGetLastError();
+        };
+        *ok = true;
+        return S0 == 0 ? launch(k_cols<A, K, TQ, true>) : launch(k_cols<A, K, TQ, false>);
+    }
+}
+
+}  // namespace cpass
+}  // namespace nttb200

@@ -26,6 +26,10 @@
 #define NTT_TILE_PF_U64 0
 #endif
 
+#ifndef NTT_TILE_MINB256
+#define NTT_TILE_MINB256 3      // resident CTAs the 256-thread tile kernels are compiled for
+#endif
+
 namespace nttb200 {
 namespace ftile {
 
@@ -315,7 +319,7 @@ constexpr size_t tile_smem_bytes() {
 
 
 template <class A, int V, int K, int TQ, int NT, int LAY, int SMB, int TWB>
-__global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT >= 1024) ? 1 : (NT <= 256 ? 3 : 2))) k_tile(TileArgs<A> a) {
+__global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT >= 1024) ? 1 : (NT <= 256 ? NTT_TILE_MINB256 : 2))) k_tile(TileArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
     using GG = TileGeo<K, TQ>;

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include "fasttile.cuh"
+#include "colpass.cuh"
 #include "multipass.cuh"
 
 namespace nttb200 {
@@ -326,6 +327,11 @@ inline int cols_split(int b, int* K) {
 template <class A, int K>
 cudaError_t cols_pass(const TileArgs<A>& a, const MultipassReq& r) {
     using T = typename A::T;
+    {   // 64-bit fields: the tensor-box column pass (colpass.cuh) where it applies
+        bool ok = false;
+        cudaError_t e = cpass::launch_cols<A, K>(a, r.stream, r.num_sms, r.launches, &ok);
+        if (e != cudaSuccess || ok) return e;
+    }
     constexpr int TQ = 1 << (tile_e<T, K>() - K);
     constexpr int NT = (TQ << (K - 4)) < 1024 ? (TQ << (K - 4)) : 1024;
     return launch_tile<A, V_DIT, K, TQ, NT, TL_COLS, kSmb, 0>(a, r.stream, r.num_sms, r.launches);
