@@ -8,8 +8,11 @@
 // A tile is one network id Qj (the position bits outside [S0, S0+K)) times TQ
 // consecutive columns: 2^K rows x TQ columns = 2^12 residues = 32 KiB.
 //
-//  * the tile is ONE 4-D tensor box [1][2^K][1][TQ] in (cp.async.bulk.tensor,
-//    mbarrier completion) and one out; the bit reversal of a sub-transform's
+//  * the tile comes in as ONE 4-D tensor box [1][2^K][1][TQ] (cp.async.bulk.tensor,
+//    mbarrier completion), issued as soon as the previous tile's last register
+//    group holds its residues, so the load runs under that group's butterflies and
+//    stores; outputs go straight from registers to HBM (a warp row = a run of TQ
+//    consecutive columns); the bit reversal of a sub-transform's
 //    input (pass 1) is a tensor-map view: j = jh * 2^(L-K) + jl puts the rows
 //    of a network 2^(L-K) apart, and the box delivers them ordered by
 //    jh = brev_K(x);
@@ -48,20 +51,11 @@ NTT_D void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(fastk::smem_u32(bar))
         : "memory");
 }
-NTT_D void tma_store_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3, const void* src) {
-    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(fastk::smem_u32(src))
-                 : "memory");
-}
-NTT_D void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-NTT_D void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-NTT_D void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 template <class A>
 struct ColArgs {
     using T = typename A::T;
     using Tw = typename A::Tw;
+    T* out;
     uint64_t batch;
     int L, S0, l1;             // sub-transform length 2^L, stages done before this pass, log2 columns
     const Tw* gstw;            // per-stage table of the length-2^L transform
@@ -82,16 +76,16 @@ constexpr size_t cols_smem_bytes() { return ((size_t)8 << K) * TQ + 128; }
 
 // FIRST: S0 == 0 (stage 1's twiddles are 1, the input rows arrive bit-reversed)
 template <class A, int K, int TQ, bool FIRST>
-__global__ void __launch_bounds__(256, NTT_COLS_MINB)
-    k_cols(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUtensorMap mout, ColArgs<A> a) {
+__global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_constant__ CUtensorMap min, ColArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
     static_assert(sizeof(T) == 8 && sizeof(Tw) == 8, "64-bit residues with bare-power twiddles");
     constexpr int NT = 256, TT = 1 << (K - 4), LTQ = ftile::ilog2c(TQ);
     static_assert(TT * TQ == NT && TQ >= 16, "2^12-residue tiles, lanes along the columns");
     constexpr int G = (K + 3) / 4, K0 = K - 4 * (G - 1);
+    static_assert(G >= 2, "two register groups or more");
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ Tw TL[1 << K];                 // TL[2^sl + m]: twiddle of local stage sl + 1, local index m
+    __shared__ Tw TLs[2][1 << K];             // TL[2^sl + m]: twiddle of local stage sl + 1, local index m
     __shared__ __align__(8) uint64_t mbar;
     T* S = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
     A ar;
@@ -101,8 +95,33 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB)
     const int ltpr = l1 + L - K - LTQ;                    // log2 tiles per matrix
     const uint64_t ntiles = a.batch << ltpr;
     const int lrest = L - K - S0;                         // bits of the network id above the pass's window
+    // tile -> (matrix b, network Qj = qlo | qhi << S0, first column)
+    struct Tile { uint64_t b; uint32_t tr, Qj, col0, qlo, qhi; };
+    auto decode = [&](uint64_t tile) {
+        Tile d;
+        d.b = tile >> ltpr;
+        d.tr = (uint32_t)(tile & ((1ull << ltpr) - 1));
+        d.Qj = d.tr >> (l1 - LTQ);
+        d.col0 = (d.tr << LTQ) & ((1u << l1) - 1);
+        d.qlo = d.Qj & ((1u << S0) - 1);
+        d.qhi = d.Qj >> S0;
+        return d;
+    };
+    auto load_tile = [&](const Tile& d) {                  // one thread: the tile's box into S
+        fastk::mbar_expect_tx(&mbar, (uint32_t)(sizeof(T) << K) * TQ);
+        if (FIRST) tma_load_4d(S, &min, (int)d.col0, (int)brev(d.Qj, L - K), 0, (int)d.b, &mbar);
+        else tma_load_4d(S, &min, (int)d.col0, (int)d.qlo, 0, (int)((d.b << lrest) + d.qhi), &mbar);
+    };
+    // the later pass's twiddles of a tile: stage S0+sl+1, index qlo + 2^S0 m (63 / 127 / 255 entries)
+    auto fill_tl = [&](Tw* TL, uint32_t qlo) {
+        for (uint32_t e = tid + 1; e < (1u << K); e += NT) {
+            const int sl = 31 - __clz(e);
+            TL[e] = __ldg(a.gstw + ((1u << (S0 + sl)) + qlo + ((e - (1u << sl)) << S0)));
+        }
+    };
     if (FIRST)
-        for (uint32_t e = tid; e < (1u << K); e += NT) TL[e] = a.gstw[e];
+        for (uint32_t e = tid; e < (1u << K); e += NT) TLs[0][e] = a.gstw[e];
+    else if ((uint64_t)blockIdx.x < ntiles) fill_tl(TLs[0], decode(blockIdx.x).qlo);
     if (tid == 0) {
         fastk::mbar_init(&mbar, 1);
         fastk::fence_mbar_init();
@@ -110,30 +129,15 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB)
     __syncthreads();
     fastk::pdl_trigger();
     fastk::pdl_wait();                       // the previous pass's output (our input) is visible
+    if (tid == 0 && (uint64_t)blockIdx.x < ntiles) load_tile(decode(blockIdx.x));
 
-    uint32_t phase = 0;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t b = tile >> ltpr;
-        const uint32_t tr = (uint32_t)(tile & ((1ull << ltpr) - 1));
-        const uint32_t Qj = tr >> (l1 - LTQ), col0 = (tr << LTQ) & ((1u << l1) - 1);
-        const uint32_t qlo = Qj & ((1u << S0) - 1), qhi = Qj >> S0;
-        const int c3 = (int)((b << lrest) + qhi);
-        if (tid == 0) {
-            bulk_wait_read();                // the previous tile's store has read the buffer
-            fastk::mbar_expect_tx(&mbar, (uint32_t)(sizeof(T) << K) * TQ);
-            if (FIRST) tma_load_4d(S, &min, (int)col0, (int)brev(Qj, L - K), 0, (int)b, &mbar);
-            else tma_load_4d(S, &min, (int)col0, (int)qlo, 0, c3, &mbar);
-        }
-        if (!FIRST) {                        // this tile's twiddles: stage S0+sl+1, index qlo + 2^S0 m
-            for (uint32_t e = tid + 1; e < (1u << K); e += NT) {
-                const int sl = 31 - __clz(e);
-                TL[e] = __ldg(a.gstw + ((1u << (S0 + sl)) + qlo + ((e - (1u << sl)) << S0)));
-            }
-            __syncthreads();
-        }
+    uint32_t it = 0;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const Tile d = decode(tile);
+        const Tw* TL = FIRST ? TLs[0] : TLs[it & 1];
         T v[16];
-        fastk::mbar_wait(&mbar, phase);
-        phase ^= 1;
+        if (!FIRST) __syncthreads();         // this tile's twiddle table (filled during the previous tile) is visible
+        fastk::mbar_wait(&mbar, it & 1);
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             const int B = g == 0 ? 0 : K0 + 4 * (g - 1);          // register block [B, B+4) of the row index
@@ -150,6 +154,18 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB)
 #pragma unroll
                 for (int c = 0; c < 16; ++c) v[c] = sp[(size_t)((uint32_t)c << B) * TQ];
             }
+            if (g == G - 1) {
+                // the tile is in registers: its buffer takes the next tile's box while the last
+                // group computes and stores (the next tile's twiddles are fetched alongside)
+                fastk::fence_proxy_async();  // this tile's generic-proxy accesses before the bulk copy's writes
+                __syncthreads();
+                const uint64_t nxt = tile + gridDim.x;
+                if (nxt < ntiles) {
+                    const Tile dn = decode(nxt);
+                    if (tid == 0) load_tile(dn);
+                    if (!FIRST) fill_tl(TLs[(it + 1) & 1], dn.qlo);
+                }
+            }
 #pragma unroll
             for (int jj = 0; jj < kg; ++jj) {
                 const int sl = b0 + jj, j = sl - B;                // local stage bit, its register bit
@@ -163,46 +179,46 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB)
                     else ar.dit(v[c], v[hi], ftile::lds_tw(row + (((uint32_t)c << B) & lmask)));
                 }
             }
-            if (g == G - 1) {
-                // ---- outputs: correction / n^-1 / canonical form, back into the tile for the store
+            if (g < G - 1) {
+                T* dp = S + (size_t)pbase * TQ + t;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) dp[(size_t)((uint32_t)c << B) * TQ] = v[c];
+                __syncthreads();
+            } else {
+                // ---- outputs: correction / n^-1 / canonical form, straight to HBM (a warp row is a
+                // run of TQ consecutive columns: 128..512 contiguous bytes)
+                const uint64_t pos0 = (uint64_t)d.qlo | ((uint64_t)pbase << S0) | ((uint64_t)d.qhi << (S0 + K));
+                T* gp = a.out + (((d.b << L) + pos0) << l1) + d.col0 + t;
+                const uint64_t gs = 1ull << (B + S0 + l1);          // register c -> row pos0 + (c << (B + S0))
                 if (a.cor_on) {
-                    // k2(c) = qlo | x << S0 | qhi << (S0+K), x = pbase | c << B; w_N^(i k2(c)) = f0 * r^c
+                    // k2(c) = pos0 + (c << (S0 + B));  w_N^(i k2(c)) = f0 * r^c
+                    // (four interleaved sequences instead of one chain measured the same: the
+                    // pass is bound by the integer pipe, not by the chain's latency)
                     const uint64_t nm = (1ull << a.cor_lgn) - 1, lm = (1ull << a.cor_lb) - 1;
-                    const uint64_t i = (uint64_t)a.qoff + col0 + t;
-                    const uint64_t k20 = (uint64_t)qlo | ((uint64_t)pbase << S0) | ((uint64_t)qhi << (S0 + K));
-                    const uint64_t e0 = (i * k20) & nm, es = (i << (S0 + B)) & nm;
+                    const uint64_t i = (uint64_t)a.qoff + d.col0 + t;
+                    const uint64_t e0 = (i * pos0) & nm, es = (i << (S0 + B)) & nm;
                     T f = ar.mulfull(__ldg(a.cor_hi + (e0 >> a.cor_lb)), __ldg(a.cor_lo + (e0 & lm)));
                     const T r = ar.mulfull(__ldg(a.cor_hi + (es >> a.cor_lb)), __ldg(a.cor_lo + (es & lm)));
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
-                        v[c] = ar.mulfull(v[c], f);
+                        gp[c * gs] = ar.mulfull(v[c], f);
                         if (c < 15) f = ar.mulfull(f, r);
                     }
                 } else if (a.scale) {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) v[c] = ar.mulc(v[c], a.ninv);
+                    for (int c = 0; c < 16; ++c) gp[c * gs] = ar.mulc(v[c], a.ninv);
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) v[c] = ar.fin(v[c]);
+                    for (int c = 0; c < 16; ++c) gp[c * gs] = ar.fin(v[c]);
                 }
             }
-            T* dp = S + (size_t)pbase * TQ + t;
-#pragma unroll
-            for (int c = 0; c < 16; ++c) dp[(size_t)((uint32_t)c << B) * TQ] = v[c];
-            if (g == G - 1) fastk::fence_proxy_async();     // generic writes -> the bulk store's reads
-            __syncthreads();
         }
-        if (tid == 0) {
-            tma_store_4d(&mout, (int)col0, (int)qlo, 0, c3, S);
-            bulk_commit();
-        }
-        if (a.counters && tid == 0 && tr == 0) {
+        if (a.counters && tid == 0 && d.tr == 0) {
             atomicAdd(a.counters + C_HBM, 1ull);
             if (a.count_row) atomicAdd(a.counters + C_TRANSFORMS, 1ull);
             if (a.count_bitrev) atomicAdd(a.counters + C_BITREV, (unsigned long long)a.count_bitrev);
         }
     }
-    if (tid == 0) bulk_wait_all();
 }
 
 inline PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
@@ -244,13 +260,13 @@ cudaError_t launch_cols(const ftile::TileArgs<A>& ta, cudaStream_t s, int num_sm
         if ((reinterpret_cast<uintptr_t>(ta.in) | reinterpret_cast<uintptr_t>(ta.out)) & 15) return cudaSuccess;
         const int lrest = L - K - S0;
         if ((ta.batch << lrest) >= (1ull << 31)) return cudaSuccess;
-        CUtensorMap min, mout;
+        CUtensorMap min;
         // pass 1 reads j = brev_L(pos): rows of a network 2^(L-K) apart, networks by brev(Qj)
         const bool mi = S0 == 0 ? cols_map(&min, ta.in, l1, 1ull << (L - K), K, ta.batch, TQ)
                                 : cols_map(&min, ta.in, l1, 1ull << S0, K, ta.batch << lrest, TQ);
-        if (!mi || !cols_map(&mout, ta.out, l1, 1ull << S0, K, ta.batch << lrest, TQ)) return cudaSuccess;
+        if (!mi) return cudaSuccess;
         ColArgs<A> a{};
-        a.batch = ta.batch; a.L = L; a.S0 = S0; a.l1 = l1;
+        a.out = ta.out; a.batch = ta.batch; a.L = L; a.S0 = S0; a.l1 = l1;
         a.gstw = ta.gstw;
         a.cor_on = ta.cor_on; a.cor_lo = ta.cor_lo; a.cor_hi = ta.cor_hi; a.cor_lb = ta.cor_lb;
         a.cor_lgn = ta.cor_lgn ? ta.cor_lgn : L + l1;
@@ -269,7 +285,7 @@ cudaError_t launch_cols(const ftile::TileArgs<A>& ta, cudaStream_t s, int num_sm
             uint64_t grid = (uint64_t)num_sms * occ;
             if (grid > ntiles) grid = ntiles;
             if (grid == 0) return cudaSuccess;
-            e = fastk::launch_pdl(kern, dim3((unsigned)grid), dim3(256), smem, s, min, mout, a);
+            e = fastk::launch_pdl(kern, dim3((unsigned)grid), dim3(256), smem, s, min, a);
             if (launches) ++*launches;
             return e != cudaSuccess ? e : cudaGetLastError();
         };

@@ -21,7 +21,7 @@ for c in "$@"; do
     c2) cap c2_pease_nc k_fast 2 pease_nc ;;
     c3) cap c3_dif k_fs 3 dif "" 2 ;;
     c4) cap c4_pease_nc k_fs 4 pease_nc "" 2 ;;
-    c5) cap c5_sixstep "k_tile|k_transpose" 5 sixstep "" 5 5 ;;
+    c5) cap c5_sixstep "k_cols|k_tile|k_transpose" 5 sixstep "" 5 5 ;;
   esac
 done
 echo prof_r2 done
