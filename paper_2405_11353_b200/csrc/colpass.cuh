@@ -75,7 +75,10 @@ template <int K, int TQ>
 constexpr size_t cols_smem_bytes() { return ((size_t)8 << K) * TQ + 128; }
 
 // FIRST: S0 == 0 (stage 1's twiddles are 1, the input rows arrive bit-reversed)
-template <class A, int K, int TQ, bool FIRST>
+// TR: the pass writes the TRANSPOSED matrix out[i][k2] (the six-step's transpose folded into step A's
+// last pass): a tile is then 2^QB consecutive network ids x 2^IB columns, so that the transposed
+// side moves runs of 2^QB residues; the box is [1][2^K][2^QB][2^IB] of the same tensor map
+template <class A, int K, int TQ, bool FIRST, bool TR = false>
 __global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_constant__ CUtensorMap min, ColArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
@@ -84,8 +87,11 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_consta
     static_assert(TT * TQ == NT && TQ >= 16, "2^12-residue tiles, lanes along the columns");
     constexpr int G = (K + 3) / 4, K0 = K - 4 * (G - 1);
     static_assert(G >= 2, "two register groups or more");
+    static_assert(!TR || !FIRST, "the transposing pass is a later pass (network ids carry low position bits)");
+    constexpr int QB = TR ? 4 : 0, IB = LTQ - QB;   // tile columns = 2^QB network ids x 2^IB matrix columns
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ Tw TLs[2][1 << K];             // TL[2^sl + m]: twiddle of local stage sl + 1, local index m
+    // TL[(2^sl + m) << QB | ql]: twiddle of local stage sl + 1, local index m, network qlo0 + ql
+    __shared__ Tw TLs[2][(1 << K) << QB];
     __shared__ __align__(8) uint64_t mbar;
     T* S = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
     A ar;
@@ -96,13 +102,14 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_consta
     const uint64_t ntiles = a.batch << ltpr;
     const int lrest = L - K - S0;                         // bits of the network id above the pass's window
     // tile -> (matrix b, network Qj = qlo | qhi << S0, first column)
+    // (qlo = the first of the tile's 2^QB network ids, col0 = the first of its 2^IB columns)
     struct Tile { uint64_t b; uint32_t tr, Qj, col0, qlo, qhi; };
     auto decode = [&](uint64_t tile) {
         Tile d;
         d.b = tile >> ltpr;
         d.tr = (uint32_t)(tile & ((1ull << ltpr) - 1));
-        d.Qj = d.tr >> (l1 - LTQ);
-        d.col0 = (d.tr << LTQ) & ((1u << l1) - 1);
+        d.Qj = (d.tr >> (l1 - IB)) << QB;
+        d.col0 = (d.tr << IB) & ((1u << l1) - 1);
         d.qlo = d.Qj & ((1u << S0) - 1);
         d.qhi = d.Qj >> S0;
         return d;
@@ -112,11 +119,13 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_consta
         if (FIRST) tma_load_4d(S, &min, (int)d.col0, (int)brev(d.Qj, L - K), 0, (int)d.b, &mbar);
         else tma_load_4d(S, &min, (int)d.col0, (int)d.qlo, 0, (int)((d.b << lrest) + d.qhi), &mbar);
     };
-    // the later pass's twiddles of a tile: stage S0+sl+1, index qlo + 2^S0 m (63 / 127 / 255 entries)
+    // the later pass's twiddles of a tile: stage S0+sl+1, index qlo + 2^S0 m (63 / 127 / 255 entries
+    // per network id)
     auto fill_tl = [&](Tw* TL, uint32_t qlo) {
-        for (uint32_t e = tid + 1; e < (1u << K); e += NT) {
+        for (uint32_t i = tid + (1u << QB); i < ((1u << K) << QB); i += NT) {
+            const uint32_t e = i >> QB, ql = i & ((1u << QB) - 1);
             const int sl = 31 - __clz(e);
-            TL[e] = __ldg(a.gstw + ((1u << (S0 + sl)) + qlo + ((e - (1u << sl)) << S0)));
+            TL[i] = __ldg(a.gstw + ((1u << (S0 + sl)) + qlo + ql + ((e - (1u << sl)) << S0)));
         }
     };
     if (FIRST)
@@ -170,13 +179,13 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_consta
             for (int jj = 0; jj < kg; ++jj) {
                 const int sl = b0 + jj, j = sl - B;                // local stage bit, its register bit
                 const uint32_t lmask = (1u << sl) - 1;
-                const Tw* row = TL + (1u << sl) + (pbase & lmask);
+                const Tw* row = TL + (((1u << sl) + (pbase & lmask)) << QB) + (TR ? (t >> IB) : 0u);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
                     if (c & (1 << j)) continue;
                     const int hi = c | (1 << j);
                     if (FIRST && sl == 0) ar.dit1(v[c], v[hi]);
-                    else ar.dit(v[c], v[hi], ftile::lds_tw(row + (((uint32_t)c << B) & lmask)));
+                    else ar.dit(v[c], v[hi], ftile::lds_tw(row + ((((uint32_t)c << B) & lmask) << QB)));
                 }
             }
             if (g < G - 1) {
@@ -187,15 +196,19 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_consta
             } else {
                 // ---- outputs: correction / n^-1 / canonical form, straight to HBM (a warp row is a
                 // run of TQ consecutive columns: 128..512 contiguous bytes)
-                const uint64_t pos0 = (uint64_t)d.qlo | ((uint64_t)pbase << S0) | ((uint64_t)d.qhi << (S0 + K));
-                T* gp = a.out + (((d.b << L) + pos0) << l1) + d.col0 + t;
-                const uint64_t gs = 1ull << (B + S0 + l1);          // register c -> row pos0 + (c << (B + S0))
+                // (TR: out[i][k2] -- lanes along the network ids, runs of 2^QB residues)
+                const uint32_t ql = TR ? (t >> IB) : 0u, il = TR ? (t & ((1u << IB) - 1)) : t;
+                const uint64_t pos0 =
+                    (uint64_t)(d.qlo + ql) | ((uint64_t)pbase << S0) | ((uint64_t)d.qhi << (S0 + K));
+                T* gp = TR ? a.out + (((d.b << l1) + d.col0 + il) << L) + pos0
+                           : a.out + (((d.b << L) + pos0) << l1) + d.col0 + il;
+                const uint64_t gs = 1ull << (B + S0 + (TR ? 0 : l1));   // register c -> row pos0 + (c << (B + S0))
                 if (a.cor_on) {
                     // k2(c) = pos0 + (c << (S0 + B));  w_N^(i k2(c)) = f0 * r^c
                     // (four interleaved sequences instead of one chain measured the same: the
                     // pass is bound by the integer pipe, not by the chain's latency)
                     const uint64_t nm = (1ull << a.cor_lgn) - 1, lm = (1ull << a.cor_lb) - 1;
-                    const uint64_t i = (uint64_t)a.qoff + d.col0 + t;
+                    const uint64_t i = (uint64_t)a.qoff + d.col0 + il;
                     const uint64_t e0 = (i * pos0) & nm, es = (i << (S0 + B)) & nm;
                     T f = ar.mulfull(__ldg(a.cor_hi + (e0 >> a.cor_lb)), __ldg(a.cor_lo + (e0 & lm)));
                     const T r = ar.mulfull(__ldg(a.cor_hi + (es >> a.cor_lb)), __ldg(a.cor_lo + (es & lm)));
@@ -234,20 +247,22 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
 }
 
 // 4-D view [d3][2^K rows][d1][2^l1 columns] of a matrix, boxes [1][2^K][1][TQ]
-inline bool cols_map(CUtensorMap* m, const void* base, int l1, uint64_t d1, int K, uint64_t d3, int TQ) {
+// (qb: the box spans 2^qb entries of dimension 1 and TQ / 2^qb columns)
+inline bool cols_map(CUtensorMap* m, const void* base, int l1, uint64_t d1, int K, uint64_t d3, int TQ, int qb = 0) {
     auto enc = tensor_encoder();
     if (!enc) return false;
     cuuint64_t dims[4] = {(cuuint64_t)1 << l1, d1, (cuuint64_t)1 << K, d3};
     cuuint64_t strides[3] = {((cuuint64_t)8 << l1), ((cuuint64_t)8 << l1) * d1, (((cuuint64_t)8 << l1) * d1) << K};
-    cuuint32_t box[4] = {(cuuint32_t)TQ, 1, (cuuint32_t)1 << K, 1};
+    cuuint32_t box[4] = {(cuuint32_t)TQ >> qb, (cuuint32_t)1 << qb, (cuuint32_t)1 << K, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(base), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// *ok = false when the pass is not covered (the caller falls back to k_tile)
-template <class A, int K>
+// *ok = false when the pass is not covered (the caller falls back to k_tile);
+// TR: write the transposed matrix (later passes with S0 >= 4 only)
+template <class A, int K, bool TR = false>
 cudaError_t launch_cols(const ftile::TileArgs<A>& ta, cudaStream_t s, int num_sms, int* launches, bool* ok) {
     using T = typename A::T;
     *ok = false;
@@ -257,13 +272,16 @@ cudaError_t launch_cols(const ftile::TileArgs<A>& ta, cudaStream_t s, int num_sm
         static const bool on = [] { const char* e = getenv("NTT_COLS_TMA"); return !e || atoi(e) != 0; }();
         const int L = ta.L, S0 = ta.S0, l1 = ta.l1;
         if (!on || l1 < 12 - K || L < K + S0 || (S0 == 0) != (ta.rev_in != 0) || ta.twist) return cudaSuccess;
+        if (TR && S0 == 0) return cudaSuccess;
         if ((reinterpret_cast<uintptr_t>(ta.in) | reinterpret_cast<uintptr_t>(ta.out)) & 15) return cudaSuccess;
+        constexpr int QB = TR ? 4 : 0;
+        if (TR && (S0 < QB || l1 < 12 - K - QB)) return cudaSuccess;
         const int lrest = L - K - S0;
         if ((ta.batch << lrest) >= (1ull << 31)) return cudaSuccess;
         CUtensorMap min;
         // pass 1 reads j = brev_L(pos): rows of a network 2^(L-K) apart, networks by brev(Qj)
         const bool mi = S0 == 0 ? cols_map(&min, ta.in, l1, 1ull << (L - K), K, ta.batch, TQ)
-                                : cols_map(&min, ta.in, l1, 1ull << S0, K, ta.batch << lrest, TQ);
+                                : cols_map(&min, ta.in, l1, 1ull << S0, K, ta.batch << lrest, TQ, QB);
         if (!mi) return cudaSuccess;
         ColArgs<A> a{};
         a.out = ta.out; a.batch = ta.batch; a.L = L; a.S0 = S0; a.l1 = l1;
@@ -290,7 +308,8 @@ cudaError_t launch_cols(const ftile::TileArgs<A>& ta, cudaStream_t s, int num_sm
             return e != cudaSuccess ? e : cudaGetLastError();
         };
         *ok = true;
-        return S0 == 0 ? launch(k_cols<A, K, TQ, true>) : launch(k_cols<A, K, TQ, false>);
+        if constexpr (TR) return S0 == 0 ? cudaErrorInvalidValue : launch(k_cols<A, K, TQ, false, true>);
+        else return S0 == 0 ? launch(k_cols<A, K, TQ, true>) : launch(k_cols<A, K, TQ, false>);
     }
 }
 

@@ -367,6 +367,7 @@ cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
     // step A: columns (length n2, inner i)
     const T* cur = static_cast<const T*>(r.in);
     int done = 0;
+    bool transposed = false;
     for (int p = 0; p < PA; ++p) {
         TileArgs<A> a = tile_base<A>(r);
         a.L = K2; a.l1 = K1; a.S0 = done;
@@ -381,12 +382,21 @@ cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
         a.cor_lb = r.cor_lb;
         a.in = cur;
         a.out = (p == PA - 1) ? ws1 : ws0;
+        if (p == PA - 1 && PA == 2 && cur == ws0) {
+            // the transpose folded into this pass: it writes [n1][n2] itself (colpass.cuh, TR tiles)
+            static const bool fuse = [] { const char* v = getenv("NTT_COLS_TR"); return !v || atoi(v) != 0; }();
+            bool ok = false;
+            a.out = ws1;
+            if (fuse && KA[p] == 6 && (e = cpass::launch_cols<A, 6, true>(a, r.stream, r.num_sms, r.launches, &ok)) != cudaSuccess)
+                return e;
+            if (ok) { transposed = true; cur = ws1; done += KA[p]; continue; }
+        }
         if ((e = cols_pass_any<A>(KA[p], a, r)) != cudaSuccess) return e;
         cur = a.out;
         done += KA[p];
     }
     // transpose [n2][n1] -> [n1][n2]
-    {
+    if (!transposed) {
         const uint64_t blocks = r.batch << (K1 + K2 - 10);
         const uint64_t cap = (uint64_t)r.num_sms * 8;
         e = fastk::launch_pdl(k_transpose<T>, dim3((unsigned)(blocks < cap ? blocks : cap)), dim3(256), 0, r.stream,
@@ -395,7 +405,7 @@ cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
         if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return e;
     }
     // step B: rows (length n1, inner k2); output = out[k1*n2 + k2]
-    cur = ws0;
+    cur = transposed ? ws1 : ws0;
     done = 0;
     for (int p = 0; p < PB; ++p) {
         const bool last = (p == PB - 1);
@@ -409,7 +419,7 @@ cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
         a.count_row = last;
         a.scale = last ? r.scale : 0;
         a.in = cur;
-        a.out = last ? static_cast<T*>(r.out) : ws1;
+        a.out = last ? static_cast<T*>(r.out) : (cur == ws1 ? ws0 : ws1);
         if ((e = cols_pass_any<A>(KB[p], a, r)) != cudaSuccess) return e;
         cur = a.out;
         done += KB[p];
