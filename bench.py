@@ -63,15 +63,17 @@ def _peaks():
 
 def _ncu_traffic(key: str):
     """DRAM bytes per launch of the dominant kernel: the steady-state ranged
-    capture (profiles/r1/traffic_steady.json) when present, else the
-    single-launch ncu summary (which under-reads writes still in L2)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1", "traffic_steady.json")) as fh:
-            d = json.load(fh).get(key)
-        if d:
-            return d["dram_bytes_per_step"] / d.get("launches_per_step", 1)
-    except Exception:
-        pass
+    capture (profiles/<latest round>/traffic_steady.json, tools/traffic_all.sh)
+    when present, else the single-launch ncu summary (which under-reads writes
+    still in L2)."""
+    for rnd in ("r2", "r1"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "traffic_steady.json")) as fh:
+                d = json.load(fh).get(key)
+            if d:
+                return d["dram_bytes_per_step"] / d.get("launches_per_step", 1)
+        except Exception:
+            pass
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:

@@ -72,7 +72,7 @@ struct ColArgs {
 };
 
 template <int K, int TQ>
-constexpr size_t cols_smem_bytes() { return ((size_t)8 << K) * TQ + 128; }
+constexpr size_t cols_smem_bytes() { return ((size_t)8 << K) * TQ; }
 
 // FIRST: S0 == 0 (stage 1's twiddles are 1, the input rows arrive bit-reversed)
 // TR: the pass writes the TRANSPOSED matrix out[i][k2] (the six-step's transpose folded into step A's
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_consta
     // TL[(2^sl + m) << QB | ql]: twiddle of local stage sl + 1, local index m, network qlo0 + ql
     __shared__ Tw TLs[2][(1 << K) << QB];
     __shared__ __align__(8) uint64_t mbar;
-    T* S = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+    T* S = reinterpret_cast<T*>(smem_raw);   // (128-byte aligned: the box's destination)
     A ar;
     ar.init(a.p);
     const uint32_t tid = threadIdx.x, t = tid % TQ, u = tid / TQ;

@@ -24,5 +24,5 @@ cap c2_pease_nc k_fast 2 pease_nc
 cap c2_dit k_fast 2 dit
 cap c3_dif k_fs 3 dif "" 2
 cap c4_pease_nc "k_fs" 4 pease_nc "" 2
-cap c5_sixstep k_tile 5 sixstep "" 2
+cap c5_sixstep "k_cols|k_tile" 5 sixstep "" 4
 echo profile_round done

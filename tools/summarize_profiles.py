@@ -26,7 +26,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3,
         "msecond": 1e-3, "nsecond": 1e-9}
 CASES = {"c2_pease_nc": (2, "config2_pease_nc", 1), "c2_dit": (2, "config2_dit", 1), "c3_dif": (3, "config3_dif", 2),
-         "c4_pease_nc": (4, "config4_pease_nc", 2), "c5_sixstep": (5, "config5_sixstep", 5)}
+         "c4_pease_nc": (4, "config4_pease_nc", 2), "c5_sixstep": (5, "config5_sixstep", 4)}
 
 
 def load_raw(path):
