@@ -354,8 +354,11 @@ __global__ void __launch_bounds__(NT, ((LAY == TL_SIX_A || LAY == TL_SIX_B || NT
     T* bufB = (PP && !ONEBUF) ? bufA + nb(TQ) : bufA;
     // staging buffer: the next tile's input, raw gather order, filled by
     // cp.async while the current tile runs its register groups
-    T* stage = !PF ? nullptr : reinterpret_cast<T*>(
-        (reinterpret_cast<uintptr_t>(bufA + ((PP && !ONEBUF) ? 2 : 1) * nb(TQ)) + 15) & ~(uintptr_t)15);
+    // (offset rounded at compile time: an integer round trip of the pointer would turn every
+    // staging access into a generic LD instead of LDS)
+    constexpr size_t kStageOff = (((size_t)sizeof(Tw) << SMB) + (TWB ? (size_t)sizeof(Tw) * TQ * tw_row<K>() : 0) +
+                                  ((PP && !ONEBUF) ? 2 : 1) * (size_t)tile_nbase<T, K, TQ, LAY>(TQ) * sizeof(T) + 15) & ~(size_t)15;
+    T* stage = !PF ? nullptr : reinterpret_cast<T*>(smem_raw + kStageOff);
     A ar;
     ar.init(a.p);
     const int L = a.L, S0 = a.S0;
