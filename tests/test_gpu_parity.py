@@ -725,3 +725,17 @@ def test_launch_window_dependencies(variant):
             assert np.array_equal(to_host(b[2]), X[2]), ("in place", rep)
             for i in range(3):
                 assert np.array_equal(to_host(a[i]), x[i]), ("inputs untouched", rep)
+
+
+@pytest.mark.parametrize("L,n1,B", [(12, 1 << 6, 3), (13, 1 << 7, 2), (14, 1 << 7, 2), (15, 1 << 8, 2), (16, 1 << 8, 2),
+                                    (24, 1 << 12, 1), (25, 1 << 13, 1), (25, 1 << 12, 1)])
+def test_sixstep_goldilocks_column_passes(L, n1, B):
+    """The tensor-box column passes (csrc/colpass.cuh) in every tile shape: one pass per side
+    (2^6 x 64, 2^7 x 32, 2^8 x 16 tiles, first pass with the correction), two passes per side with
+    the transpose folded into step A's second pass (2^12 / 2^13 sub-transforms), batches of
+    matrices, forward and intt, against the oracle."""
+    p, g = GOLD, 7
+    x = rand(p, B, L, np.uint64, 8100 + L)
+    assert np.array_equal(gpu_ntt(x, p, g, 64, "sixstep", n1=n1), O.ntt(x, p, g, 64, "sixstep", n1=n1))
+    assert np.array_equal(gpu_ntt(x, p, g, 64, "sixstep", inverse=True, scale=True, n1=n1),
+                          O.ntt(x, p, g, 64, "sixstep", inverse=True, scale=True, n1=n1))
