@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_consta
                     const uint64_t e0 = (i * pos0) & nm, es = (i << (S0 + B)) & nm;
                     T f = ar.mulfull(__ldg(a.cor_hi + (e0 >> a.cor_lb)), __ldg(a.cor_lo + (e0 & lm)));
                     const T r = ar.mulfull(__ldg(a.cor_hi + (es >> a.cor_lb)), __ldg(a.cor_lo + (es & lm)));
+                    if (a.scale) f = ar.mulfull(f, a.ninv);        // intt: n^-1 rides the sequence's first term
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
                         gp[c * gs] = ar.mulfull(v[c], f);
@@ -269,9 +270,8 @@ cudaError_t launch_cols(const ftile::TileArgs<A>& ta, cudaStream_t s, int num_sm
     if constexpr (sizeof(T) != 8 || sizeof(typename A::Tw) != 8 || K < 6 || K > 8) return cudaSuccess;
     else {
         constexpr int TQ = 1 << (12 - K);
-        static const bool on = [] { const char* e = getenv("NTT_COLS_TMA"); return !e || atoi(e) != 0; }();
         const int L = ta.L, S0 = ta.S0, l1 = ta.l1;
-        if (!on || l1 < 12 - K || L < K + S0 || (S0 == 0) != (ta.rev_in != 0) || ta.twist) return cudaSuccess;
+        if (l1 < 12 - K || L < K + S0 || (S0 == 0) != (ta.rev_in != 0) || ta.twist) return cudaSuccess;
         if (TR && S0 == 0) return cudaSuccess;
         if ((reinterpret_cast<uintptr_t>(ta.in) | reinterpret_cast<uintptr_t>(ta.out)) & 15) return cudaSuccess;
         constexpr int QB = TR ? 4 : 0;

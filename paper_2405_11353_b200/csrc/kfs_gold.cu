@@ -20,6 +20,10 @@ static cudaError_t fsg_run_l(const MultipassReq& r) {
     a.p = r.p;
     a.ninv = r.ninv;
     a.counters = r.counters;
+    // intt: n^-1 rides the twist (a second [k1][n2] table holding w^(k1 n2) * n^-1, built with the
+    // inverse plan), so pass B's stores skip their scaling product -- where pass A reads the table
+    const bool fold = r.scale && r.fst_scaled && V == V_DIF;
+    if (fold) a.twist = static_cast<const uint64_t*>(r.fst_scaled);
     a.in = static_cast<const uint64_t*>(r.in);
     a.out = static_cast<uint64_t*>(r.ws);
     a.scale = 0;
@@ -28,7 +32,7 @@ static cudaError_t fsg_run_l(const MultipassReq& r) {
     if (e != cudaSuccess) return e;
     a.in = static_cast<const uint64_t*>(r.ws);
     a.out = static_cast<uint64_t*>(r.out);
-    a.scale = r.scale;
+    a.scale = fold ? 0 : r.scale;
     a.count_bitrev = 0;
     return fstep::fs_launch<A, V, KC, 1, KR>(a, r.stream, r.num_sms, r.launches);
 }
@@ -43,6 +47,16 @@ static cudaError_t fsg_run(const MultipassReq& r) {
         case 18: return fsg_run_l<V, 18>(r);
         default: return cudaErrorInvalidValue;
     }
+}
+
+__global__ void k_twist_scale_gold(uint64_t* t, uint64_t n, uint64_t c) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        t[i] = FGoldC::mul_m(t[i], c);
+}
+// t[i] *= c (the n^-1-carrying copy of the twist table)
+cudaError_t fourstep_twist_scale_gold(void* t, uint64_t n, uint64_t c, cudaStream_t s) {
+    k_twist_scale_gold<<<1024, 256, 0, s>>>(static_cast<uint64_t*>(t), n, c);
+    return cudaGetLastError();
 }
 
 cudaError_t fourstep_gold(const MultipassReq& r, bool* ok) {

@@ -324,6 +324,7 @@ struct MultipassReq {
     int* launches;
     void* ws;                  // workspace: 2 x batch x N residues
     const void* fst;           // four-step twist table [k1][n2] = w^(k1*n2) (fourstep.cuh), or null
+    const void* fst_scaled = nullptr;   // Goldilocks inverse plans: the same table times n^-1 (intt folds its scaling)
 };
 
 // Launch window (planner.cu): may a fast-kernel launch defer its dependency wait
@@ -341,6 +342,7 @@ cudaError_t mp_launch_f32s(const MultipassReq& r);
 cudaError_t pointwise_inverse_f32(const MultipassReq& r, const void* in2, bool* ok);
 // two-pass four-step for large u32 N (fourstep.cuh, kfs_f32.cu); *ok = false when it does not apply
 cudaError_t fourstep_f32(const MultipassReq& r, bool* ok);
+cudaError_t fourstep_twist_scale_gold(void* t, uint64_t n, uint64_t c, cudaStream_t s);
 // four-step: u32 fields DIT / Flat / DIF / Pease_nc / Stockham 15 <= L <= 20, Goldilocks 2^14..2^18
 // (u32 2^14 is one shared-memory pass: the fast kernel, fast.cuh)
 inline bool fourstep_applies(int L, int variant, uint64_t p, int word) {

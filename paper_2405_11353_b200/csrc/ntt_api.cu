@@ -241,6 +241,7 @@ struct ntt_plan_s {
     int twh_bits = 0;
     // four-step twist table (fourstep.cuh): [k1][n2] = w^(k1*n2) + Shoup word
     void* fst = nullptr;
+    void* fst_inv = nullptr;      // Goldilocks inverse plans: fst * n^-1
     int num_sms = 148;
     // workspace for multi-pass plans and host-buffer execution
     // multi-pass workspace, one per CUDA stream: a plan is immutable and may run
@@ -291,6 +292,7 @@ struct ntt_plan_s {
         if (cor_hi) cudaFree(cor_hi);
         if (twh) cudaFree(twh);
         if (fst) cudaFree(fst);
+        if (fst_inv) cudaFree(fst_inv);
         cudaSetDevice(cur);
     }
 };
@@ -476,6 +478,11 @@ int ntt_plan_create(uint64_t p, uint64_t g, int w_bits, uint64_t n, int variant,
         cudaSetDevice(device);
         cudaError_t e = cudaMalloc(&pl->fst, n * 8);
         if (e == cudaSuccess) e = fourstep_twist_build(pl->table->tw, pl->fst, L, word_bytes, 0);
+        if (e == cudaSuccess && pl->kind == 2 && direction == NTT_INVERSE) {      // intt: n^-1 folded into the twist
+            e = cudaMalloc(&pl->fst_inv, n * 8);
+            if (e == cudaSuccess) e = fourstep_twist_build(pl->table->tw, pl->fst_inv, L, word_bytes, 0);
+            if (e == cudaSuccess) e = fourstep_twist_scale_gold(pl->fst_inv, n, pl->table->n_inv, 0);
+        }
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         cudaSetDevice(cur);
         if (e != cudaSuccess) { if (pl->fst) cudaFree(pl->fst); pl->fst = nullptr; return cuda_fail(e, "four-step twist table"); }
@@ -557,6 +564,7 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
     r.twh = plan->twh;
     r.twh_bits = plan->twh_bits;
     r.fst = plan->fst;
+    r.fst_scaled = plan->fst_inv;
     if (plan->variant == NTT_SIXSTEP) {
         r.n1 = plan->n1; r.n2 = plan->n2;
         r.tw1 = plan->table1 ? plan->table1->tw : nullptr;

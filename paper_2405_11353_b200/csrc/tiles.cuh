@@ -380,14 +380,14 @@ cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
         a.cor_lo = static_cast<const T*>(r.cor_lo);
         a.cor_hi = static_cast<const T*>(r.cor_hi);
         a.cor_lb = r.cor_lb;
+        a.scale = (p == PA - 1) ? r.scale : 0;     // intt: n^-1 folded into the correction (one product per residue less)
         a.in = cur;
         a.out = (p == PA - 1) ? ws1 : ws0;
         if (p == PA - 1 && PA == 2 && cur == ws0) {
             // the transpose folded into this pass: it writes [n1][n2] itself (colpass.cuh, TR tiles)
-            static const bool fuse = [] { const char* v = getenv("NTT_COLS_TR"); return !v || atoi(v) != 0; }();
             bool ok = false;
             a.out = ws1;
-            if (fuse && KA[p] == 6 && (e = cpass::launch_cols<A, 6, true>(a, r.stream, r.num_sms, r.launches, &ok)) != cudaSuccess)
+            if (KA[p] == 6 && (e = cpass::launch_cols<A, 6, true>(a, r.stream, r.num_sms, r.launches, &ok)) != cudaSuccess)
                 return e;
             if (ok) { transposed = true; cur = ws1; done += KA[p]; continue; }
         }
@@ -417,7 +417,7 @@ cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
         a.gstw = static_cast<const typename A::Tw*>(r.stw1);
         a.smb = K1 < kSmb ? K1 : kSmb;
         a.count_row = last;
-        a.scale = last ? r.scale : 0;
+        a.scale = 0;                               // (step A's correction carried n^-1)
         a.in = cur;
         a.out = last ? static_cast<T*>(r.out) : (cur == ws1 ? ws0 : ws1);
         if ((e = cols_pass_any<A>(KB[p], a, r)) != cudaSuccess) return e;
