@@ -158,10 +158,17 @@ NTT_D Tw twld(const Tw* p, uint32_t idx) {
 }
 
 // ---------------------------------------------------------------- DIT/DIF --
-template <class A, int K, int B, int b0, int kg, bool DIF, bool GL>
+// IN (first group of a LOCAL transform only: S0 = 0, qlow = 0, the thread's low position bits
+// zero, so a butterfly's twiddle index is the compile-time kc): 1 = canonical inputs (caller data,
+// modmath.py:112), 2 = inputs in [0,2p) (a lazy twist's outputs).  Stage 1 / 2 then take the
+// bounded forms and every w^0 butterfly skips its multiply, as in the single-pass kernel.
+// (The same forms in the Pease first group measured 1.3 % SLOWER on config 4 in three
+// interleaved A/Bs -- 2.66-2.68 vs 2.63 ms -- so t_pease keeps the general butterflies.)
+template <class A, int K, int B, int b0, int kg, bool DIF, bool GL, int IN = 0>
 NTT_D void t_bitwin(const A& ar, typename A::T (&v)[16], uint32_t pbase, uint32_t qlow, int S0,
                     const typename A::Tw* tw) {
     constexpr int off = b0 - B;
+    static_assert(IN == 0 || (!DIF && B == 0 && b0 == 0), "bounded first stages: DIT-type first groups");
 #pragma unroll
     for (int jj = 0; jj < kg; ++jj) {
         const int j = DIF ? kg - 1 - jj : jj;
@@ -176,7 +183,14 @@ NTT_D void t_bitwin(const A& ar, typename A::T (&v)[16], uint32_t pbase, uint32_
             if (c & (1 << (off + j))) continue;
             const uint32_t kc = ((uint32_t)c << B) & lmask;
             const int hi = c | (1 << (off + j));
-            if (triv) {
+            if (IN != 0) {
+                const bool one = kc == 0;              // w^0
+                if (sl == 0) { if (IN == 1) ar.dit1_c(v[c], v[hi]); else ar.dit1_2p(v[c], v[hi]); }
+                else if (sl == 1 && IN == 1) {
+                    if (one) ar.dit1_2p(v[c], v[hi]); else ar.dit_2p(v[c], v[hi], twld<GL>(tw, rowi + kc));
+                } else if (one) ar.dit1(v[c], v[hi]);
+                else ar.dit(v[c], v[hi], twld<GL>(tw, rowi + kc));
+            } else if (triv) {
                 if (DIF) ar.dif1(v[c], v[hi]); else ar.dit1(v[c], v[hi]);
             } else {
                 const typename A::Tw w = twld<GL>(tw, rowi + (kc << S0));

@@ -94,6 +94,10 @@ NTT_D uint32_t placeN(uint32_t w) {
     return u;
 }
 
+#ifndef NTT_FS_BOUNDED
+#define NTT_FS_BOUNDED 1       // DIT first groups: bounded stage-1/2 forms and w^0 butterflies without a multiply
+                               // (config 4 DIT 2.59 -> 2.49 ms)
+#endif
 #ifndef NTT_FSA_TWF
 #define NTT_FSA_TWF 1          // factored twist (per-tile [c][t] table in shared memory + one w^(n2 u) per thread)
 #endif
@@ -134,6 +138,7 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
     constexpr int TQ = GG::TQ, NT = GG::NT, TT = GG::TT, LQ = GG::LQ, AB = GG::AB, G = GG::G, K0 = GG::K0;
     constexpr int UB = K - 4;
     constexpr int CW = fastk::lane_bits<T>();
+    constexpr int kIn = !NTT_FS_BOUNDED ? 0 : MODE == 0 ? 1 : ((NTT_FSA_TWF && A::lazy) ? 2 : 1);   // value range of a pass's input
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t mbar[2];
     Tw* tws = reinterpret_cast<Tw*>(smem_raw);                           // 2^K stage twiddles
@@ -202,7 +207,8 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
         if (V == V_DIT) {
             // block [0,4): positions u0 << 4 | c
             const uint32_t pbase = u0 << 4;
-            ftile::t_bitwin<A, K, 0, 0, GG::KG0, false, false>(ar, v, pbase, 0u, 0, tws);
+            // (pass A reads caller data: canonical; pass B the lazy twist's outputs in [0,2p))
+            ftile::t_bitwin<A, K, 0, 0, GG::KG0, false, false, kIn>(ar, v, pbase, 0u, 0, tws);
             __syncthreads();                  // staging consumed; previous tile's last group done with W
             T* wb = W + GG::base(q) + padpos<T>(pbase);
 #pragma unroll
