@@ -9,7 +9,10 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns"
         "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
 out = {"_method": "ncu --replay-mode app-range over 16 back-to-back steps (tools/traffic_all.sh, tools/traffic_range.py, "
                   "rotating buffer sets > L2), divided by 16: steady-state DRAM bytes and time per step.  A single-launch "
-                  "capture under-reads the writes still in L2 when the launch ends and times a cold launch."}
+                  "capture under-reads the writes still in L2 when the launch ends and times a cold launch.  "
+                  "range_time_us_per_step is the whole range / 16 and so includes the eager Python launch gaps "
+                  "(~8 us per launch): it matches the bench's graph replays for the millisecond steps (configs 4, 5), "
+                  "not for config 2, whose 32 us steps bench.py times as CUDA-graph replays."}
 for name, nl in LAUNCHES.items():
     p = f"gpurun_out/traffic/{name}.csv"
     if not os.path.exists(p):
