@@ -90,9 +90,11 @@ struct FsGeo {
     static constexpr int AB = LQ >= 5 ? 0 : 5 - LQ;      // lane bits above the network id (tile-major)
 };
 
-template <class T, class TwT, int K, int TQ>
+// (NB tile buffers: two -- the next tile's copy-in lands beside the current one -- and for Pease a third,
+// the stage output that is copied back)
+template <class T, class TwT, int K, int TQ, int NB = 2>
 constexpr size_t fs_smem_bytes() {
-    return ((size_t)sizeof(TwT) << K) + (size_t)sizeof(TwT) * 16 * TQ + 2 * (size_t)TQ * ftile::tile_stride<T, K, TQ>() * sizeof(T);
+    return ((size_t)sizeof(TwT) << K) + (size_t)sizeof(TwT) * 16 * TQ + NB * (size_t)TQ * ftile::tile_stride<T, K, TQ>() * sizeof(T);
 }
 
 // tile-major last group: sub-network id u from the thread's u' so that the AB
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         T* X = buf0 + (it & 1) * (TQ * NP);
         T* Y = buf0 + ((it + 1) & 1) * (TQ * NP);
+        T* Z = buf0 + 2 * (TQ * NP);         // Pease only: the stage output before its copy-back
         cp_async_wait_all();
         __syncthreads();                     // X landed for every thread; Y free (previous tile done)
         auto prefetch_next = [&]() {
@@ -272,12 +275,17 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
                 if (g == 0) { NTT_FSPE(0, 1) NTT_FSPE(0, 2) NTT_FSPE(0, 3) NTT_FSPE(0, 4) }
                 else { NTT_FSPE(1, 4) NTT_FSPE(2, 4) NTT_FSPE(3, 4) NTT_FSPE(4, 4) NTT_FSPE(5, 4) }
 #undef NTT_FSPE
-                __syncthreads();             // every read of the (single) work buffer done
-                T* wbo = sb + padpos<T>(u << (4 - kg));
+                if (V != V_PEASE) __syncthreads();   // every read of the (single) work buffer done
+                // Pease: the stage output goes to Z and is copied back (_stage_copy, algorithms.py:242)
+                T* wbo = (V == V_PEASE ? Z + t * NP : sb) + padpos<T>(u << (4 - kg));
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
                     const uint32_t n = c >> kg, Rb = c & ((1u << kg) - 1);
                     wbo[padpos<T>(n | (Rb << (K - kg)))] = v[c];
+                }
+                if (V == V_PEASE) {
+                    __syncthreads();
+                    for (uint32_t i = tid; i < (uint32_t)(TQ * NP); i += NT) X[i] = Z[i];
                 }
             }
             __syncthreads();
@@ -362,6 +370,7 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
         if (a.counters && tid == 0 && (tile & ((1ull << tpp_log) - 1)) == 0) {
             atomicAdd(a.counters + C_HBM, 1ull);
             if (MODE == 1) atomicAdd(a.counters + C_TRANSFORMS, 1ull);
+            if (V == V_PEASE) atomicAdd(a.counters + C_COPIES, (unsigned long long)(G - 1));
             if (MODE == 0 && a.count_bitrev) atomicAdd(a.counters + C_BITREV, (unsigned long long)a.count_bitrev);
         }
     }
@@ -381,7 +390,7 @@ cudaError_t fs_launch(const FsArgs<A>& a, cudaStream_t s, int num_sms, int* laun
     using T = typename A::T;
     constexpr int TQ = fs_tq<T, K>();
     constexpr int NT = FsGeo<K, TQ>::NT;
-    constexpr size_t smem = fs_smem_bytes<T, typename A::Tw, K, TQ>();
+    constexpr size_t smem = fs_smem_bytes<T, typename A::Tw, K, TQ, V == V_PEASE ? 3 : 2>();
     auto kern = k_fs<A, V, K, TQ, MODE, KO>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -114,8 +114,9 @@ constexpr int kFsaStages = NTT_FSA_STAGES;
 template <int V, int K, int MODE>
 constexpr size_t fsa_smem_bytes() {
     using GG = TmaGeo<V, K>;
-    return ((size_t)8 << K) + kFsaStages * (size_t)(MODE == 0 ? 8192 : 8 * kStgRow) * 4 + (size_t)GG::base(GG::TQ) * 4 + 8 +
-           16 * (size_t)GG::TQ * 8;
+    // (Pease: a second work buffer -- the stage output that is copied back, algorithms.py:242)
+    return ((size_t)8 << K) + kFsaStages * (size_t)(MODE == 0 ? 8192 : 8 * kStgRow) * 4 +
+           (V == V_PEASE ? 2 : 1) * (size_t)((GG::base(GG::TQ) + 1) & ~1u) * 4 + 8 + 16 * (size_t)GG::TQ * 8;
 }
 
 NTT_D void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -146,10 +147,18 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
     constexpr int STG = MODE == 0 ? 8192 : 8 * kStgRow;                  // MODE 0 [2^K][TQ], MODE 1 [8][kStgRow]
     constexpr int NST = kFsaStages;
     T* W = stg + NST * STG;                                              // TQ networks at GG::base(q)
-    Tw* twB = reinterpret_cast<Tw*>(W + ((GG::base(TQ) + 1) & ~1u));     // factored twist [c][q]
+    constexpr uint32_t WLEN = (GG::base(TQ) + 1) & ~1u;
+    // Pease: groups write the stage output to W2 and copy it back into W (_stage_copy,
+    // algorithms.py:242); Pease_nc writes W itself after a barrier (no copy)
+    T* W2 = V == V_PEASE ? W + WLEN : W;
+    Tw* twB = reinterpret_cast<Tw*>(W2 + WLEN);                          // factored twist [c][q]
     A ar;
     ar.init(a.p);
     const uint32_t tid = threadIdx.x;
+    auto copy_back = [&]() {
+        __syncthreads();
+        for (uint32_t i = tid; i < WLEN; i += NT) W[i] = W2[i];
+    };
     for (uint32_t i = tid; i < (1u << K); i += NT) tws[i] = a.stw[i];
     constexpr int Kr = MODE == 0 ? K : KO, Kc = MODE == 0 ? KO : K;
     constexpr uint64_t N = 1ull << (Kr + Kc);
@@ -216,12 +225,13 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
         } else {
             ftile::t_pease<A, K, 0, GG::KG0, false>(ar, v, u0, 0u, 0, tws);
             __syncthreads();
-            T* wbo = W + GG::base(q) + padpos<T>(u0 << (4 - GG::KG0));
+            T* wbo = W2 + GG::base(q) + padpos<T>(u0 << (4 - GG::KG0));
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
                 const uint32_t n = c >> GG::KG0, Rb = c & ((1u << GG::KG0) - 1);
                 wbo[padpos<T>(n | (Rb << (K - GG::KG0)))] = v[c];
             }
+            if (V == V_PEASE) copy_back();
         }
         // factored twist of the last group: w^(k1 n2) = w^(n2 a(u)) * w^(n2 b(c)), k1 = a(u) + b(c)
         Tw twA;
@@ -276,10 +286,11 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
     if (sg == SG) ftile::t_pease<A, K, SG, 4, false>(ar, v, u, 0u, 0, tws);
                 NTT_TPEM(4) NTT_TPEM(8)
 #undef NTT_TPEM
-                __syncthreads();              // every read of the single work buffer done
-                T* wbo = sb + padpos<T>(u);
+                if (V != V_PEASE) __syncthreads();   // every read of the single work buffer done
+                T* wbo = (V == V_PEASE ? W2 + GG::base(t) : sb) + padpos<T>(u);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) wbo[padpos<T>((uint32_t)c << (K - 4))] = v[c];
+                if (V == V_PEASE) copy_back();
             }
             __syncthreads();
         }
@@ -319,6 +330,7 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
         if (a.counters && tid == 0 && (tile & ((1ull << tpp_log) - 1)) == 0) {
             atomicAdd(a.counters + C_HBM, 1ull);
             if (MODE == 1) atomicAdd(a.counters + C_TRANSFORMS, 1ull);
+            if (V == V_PEASE) atomicAdd(a.counters + C_COPIES, (unsigned long long)(G - 1));
             if (a.count_bitrev) atomicAdd(a.counters + C_BITREV, (unsigned long long)a.count_bitrev);
         }
     }

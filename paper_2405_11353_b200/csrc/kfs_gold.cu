@@ -68,6 +68,7 @@ cudaError_t fourstep_gold(const MultipassReq& r, bool* ok) {
     if (r.variant == V_DIT || r.variant == V_FLAT) return fsg_run<V_DIT>(r);
     if (r.variant == V_DIF) return fsg_run<V_DIF>(r);
     if (r.variant == V_STOCKHAM) return fsg_run<V_STOCKHAM>(r);
+    if (r.variant == V_PEASE) return fsg_run<V_PEASE>(r);
     return fsg_run<V_PEASE_NC>(r);
 }
 

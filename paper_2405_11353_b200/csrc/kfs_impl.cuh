@@ -144,6 +144,8 @@ cudaError_t fourstep_u32_policy(const MultipassReq& r) {
     if (r.variant == V_DIT || r.variant == V_FLAT) return fs_run<A, V_DIT>(r, Kr, Kc);
     if (r.variant == V_DIF) return fs_run<A, V_DIF>(r, Kr, Kc);
     if (r.variant == V_STOCKHAM) return fs_run<A, V_STOCKHAM>(r, Kr, Kc);
+    // Pease: Pease_nc's constant geometry with the stage output copied back (a second work buffer)
+    if (r.variant == V_PEASE) return fs_run<A, V_PEASE>(r, Kr, Kc);
     return fs_run<A, V_PEASE_NC>(r, Kr, Kc);
 }
 

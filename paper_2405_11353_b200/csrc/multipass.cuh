@@ -343,17 +343,17 @@ cudaError_t pointwise_inverse_f32(const MultipassReq& r, const void* in2, bool* 
 // two-pass four-step for large u32 N (fourstep.cuh, kfs_f32.cu); *ok = false when it does not apply
 cudaError_t fourstep_f32(const MultipassReq& r, bool* ok);
 cudaError_t fourstep_twist_scale_gold(void* t, uint64_t n, uint64_t c, cudaStream_t s);
-// four-step: u32 fields DIT / Flat / DIF / Pease_nc / Stockham 15 <= L <= 20, Goldilocks 2^14..2^18
+// four-step: u32 fields DIT / Flat / DIF / Pease / Pease_nc / Stockham 15 <= L <= 20, Goldilocks 2^14..2^18
 // (u32 2^14 is one shared-memory pass: the fast kernel, fast.cuh)
 inline bool fourstep_applies(int L, int variant, uint64_t p, int word) {
     if (word == 4)
         return p < (1ull << 32) && L >= 15 && L <= 20 &&
                (variant == V_DIT || variant == V_PEASE_NC || variant == V_DIF || variant == V_FLAT ||
-                variant == V_STOCKHAM);
+                variant == V_STOCKHAM || variant == V_PEASE);
     // Goldilocks 2^14..2^18 (config 3: 2^16 = 256 x 256)
     return word == 8 && p == 0xFFFFFFFF00000001ull && L >= 14 && L <= 18 &&
            (variant == V_DIT || variant == V_DIF || variant == V_PEASE_NC || variant == V_FLAT ||
-            variant == V_STOCKHAM);
+            variant == V_STOCKHAM || variant == V_PEASE);
 }
 inline int fourstep_kr(int L) { return (L + 1) / 2; }
 // u32 (p < 2^31) 2^14 outside the four-step (Pease, Stockham): the compile-time tile
