@@ -267,7 +267,7 @@ template <class A, int K, bool TR = false>
 cudaError_t launch_cols(const ftile::TileArgs<A>& ta, cudaStream_t s, int num_sms, int* launches, bool* ok) {
     using T = typename A::T;
     *ok = false;
-    if constexpr (sizeof(T) != 8 || sizeof(typename A::Tw) != 8 || K < 6 || K > 8) return cudaSuccess;
+    if constexpr (sizeof(T) != 8 || sizeof(typename A::Tw) != 8 || K < 5 || K > 8 || (TR && K > 7)) return cudaSuccess;
     else {
         constexpr int TQ = 1 << (12 - K);
         const int L = ta.L, S0 = ta.S0, l1 = ta.l1;

@@ -70,6 +70,7 @@ cudaError_t pass_any(int K, const TileArgs<A>& a, cudaStream_t s, int sms, int* 
         }
     } else {
         switch (K) {
+            case 6: return pass_k<A, V, 6>(a, s, sms, launches);     // (2^19, 2^20: three passes of 7 / 6 stages)
             case 7: return pass_k<A, V, 7>(a, s, sms, launches);
             case 8: return pass_k<A, V, 8>(a, s, sms, launches);
             case 9: return pass_k<A, V, 9>(a, s, sms, launches);
@@ -311,8 +312,13 @@ cudaError_t run_sixstep_tiles_k(const MultipassReq& r) {
 //   step B: DIT over i (length n1) for every k2, TL_COLS again (inner k2),
 //           whose natural-order output IS out[k1*n2 + k2].
 // Each length-2^b step is one pass (b <= 9) or two (b = 12, 13: 6+6, 7+6).
-inline int cols_split(int b, int* K) {
+inline int cols_split(int b, int* K, int word = 4) {
     if (b >= 6 && b <= 9) { K[0] = b; return 1; }
+    if (word == 8) {       // 64-bit fields (colpass.cuh tiles of 2^5..2^8 rows): every length up to 2^16
+        if (b == 10) { K[0] = 5; K[1] = 5; return 2; }
+        if (b == 11) { K[0] = 6; K[1] = 5; return 2; }
+        if (b >= 14 && b <= 16) { K[0] = (b + 1) / 2; K[1] = b / 2; return 2; }
+    }
 #ifndef NTT_COLS_SPLIT_SWAP
 #define NTT_COLS_SPLIT_SWAP 0
 #endif
@@ -340,6 +346,7 @@ cudaError_t cols_pass(const TileArgs<A>& a, const MultipassReq& r) {
 template <class A>
 cudaError_t cols_pass_any(int K, const TileArgs<A>& a, const MultipassReq& r) {
     switch (K) {
+        case 5: return cols_pass<A, 5>(a, r);
         case 6: return cols_pass<A, 6>(a, r);
         case 7: return cols_pass<A, 7>(a, r);
         case 8: return cols_pass<A, 8>(a, r);
@@ -356,7 +363,7 @@ cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
     while ((1ull << K1) < r.n1) ++K1;
     while ((1ull << K2) < r.n2) ++K2;
     int KA[2], KB[2];
-    const int PA = cols_split(K2, KA), PB = cols_split(K1, KB);
+    const int PA = cols_split(K2, KA, (int)sizeof(T)), PB = cols_split(K1, KB, (int)sizeof(T));
     if (!PA || !PB || K1 < 5 || K2 < 5) return cudaSuccess;
     *ok = true;
     const uint64_t N = 1ull << (K1 + K2);
@@ -387,8 +394,11 @@ cudaError_t run_sixstep_cols(const MultipassReq& r, bool* ok) {
             // the transpose folded into this pass: it writes [n1][n2] itself (colpass.cuh, TR tiles)
             bool ok = false;
             a.out = ws1;
-            if (KA[p] == 6 && (e = cpass::launch_cols<A, 6, true>(a, r.stream, r.num_sms, r.launches, &ok)) != cudaSuccess)
-                return e;
+            e = KA[p] == 5   ? cpass::launch_cols<A, 5, true>(a, r.stream, r.num_sms, r.launches, &ok)
+                : KA[p] == 6 ? cpass::launch_cols<A, 6, true>(a, r.stream, r.num_sms, r.launches, &ok)
+                : KA[p] == 7 ? cpass::launch_cols<A, 7, true>(a, r.stream, r.num_sms, r.launches, &ok)
+                             : cudaSuccess;
+            if (e != cudaSuccess) return e;
             if (ok) { transposed = true; cur = ws1; done += KA[p]; continue; }
         }
         if ((e = cols_pass_any<A>(KA[p], a, r)) != cudaSuccess) return e;
@@ -447,7 +457,7 @@ cudaError_t run_sixstep_cols_dist(const MultipassReq& r, int step, int rank, int
     while ((1ull << K2) < r.n2) ++K2;
     while ((1 << lg) < world) ++lg;
     int KA[2], KB[2];
-    const int PA = cols_split(K2, KA), PB = cols_split(K1, KB);
+    const int PA = cols_split(K2, KA, (int)sizeof(T)), PB = cols_split(K1, KB, (int)sizeof(T));
     const int lc = K1 - lg, lk = K2 - lg;             // local columns (step A), local k2 (step B)
     if (!PA || !PB || lc < 6 || lk < 6 || !wsv) return cudaSuccess;   // TL_COLS tiles span up to 64 columns
     *ok = true;

@@ -728,14 +728,28 @@ def test_launch_window_dependencies(variant):
 
 
 @pytest.mark.parametrize("L,n1,B", [(12, 1 << 6, 3), (13, 1 << 7, 2), (14, 1 << 7, 2), (15, 1 << 8, 2), (16, 1 << 8, 2),
-                                    (24, 1 << 12, 1), (25, 1 << 13, 1), (25, 1 << 12, 1)])
+                                    (24, 1 << 12, 1), (25, 1 << 13, 1), (25, 1 << 12, 1),
+                                    (20, 1 << 10, 2), (21, 1 << 11, 1), (22, 1 << 11, 1), (20, 1 << 14, 1),
+                                    (21, 1 << 6, 1), (22, 1 << 16, 1)])
 def test_sixstep_goldilocks_column_passes(L, n1, B):
     """The tensor-box column passes (csrc/colpass.cuh) in every tile shape: one pass per side
     (2^6 x 64, 2^7 x 32, 2^8 x 16 tiles, first pass with the correction), two passes per side with
-    the transpose folded into step A's second pass (2^12 / 2^13 sub-transforms), batches of
-    matrices, forward and intt, against the oracle."""
+    the transpose folded into step A's second pass (2^10 .. 2^13 sub-transforms; 2^14 .. 2^16
+    ones with the separate transpose), batches of matrices, forward and intt, against the oracle."""
     p, g = GOLD, 7
     x = rand(p, B, L, np.uint64, 8100 + L)
     assert np.array_equal(gpu_ntt(x, p, g, 64, "sixstep", n1=n1), O.ntt(x, p, g, 64, "sixstep", n1=n1))
     assert np.array_equal(gpu_ntt(x, p, g, 64, "sixstep", inverse=True, scale=True, n1=n1),
                           O.ntt(x, p, g, 64, "sixstep", inverse=True, scale=True, n1=n1))
+
+
+@pytest.mark.parametrize("variant", ["dit", "dif", "flat", "pease", "pease_nc", "stockham"])
+@pytest.mark.parametrize("L", [19, 20, 21])
+def test_goldilocks_beyond_the_fourstep(variant, L):
+    """Goldilocks past the four-step's range (2^19 ..): three tile passes of 6 / 7 stages
+    (2^19 and 2^20 need the 2^6-stage pass), forward and intt against the oracle."""
+    p, g = GOLD, 7
+    x = rand(p, 1, L, np.uint64, 8300 + L)
+    assert np.array_equal(gpu_ntt(x, p, g, 64, variant), O.ntt(x, p, g, 64, variant))
+    assert np.array_equal(gpu_ntt(x, p, g, 64, variant, inverse=True, scale=True),
+                          O.ntt(x, p, g, 64, variant, inverse=True, scale=True))

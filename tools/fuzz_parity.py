@@ -18,7 +18,7 @@ def generic64():
 
 g64 = generic64()
 FIELDS = [(998244353, 3, 32, 4, 20), (3221225473, 5, 32, 4, 20), (2013265921, 31, 32, 4, 20),
-          (GOLD, 7, 64, 8, 18), (g64[0], g64[1], 64, 8, 12), (998244353, 3, 64, 8, 12)]
+          (GOLD, 7, 64, 8, 21), (g64[0], g64[1], 64, 8, 12), (998244353, 3, 64, 8, 12)]
 VARIANTS = ("dit", "dif", "flat", "pease", "pease_nc", "stockham", "sixstep", "naive")
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
