@@ -424,14 +424,14 @@ def main() -> None:
             roundtrip = all_ranks(roundtrip)
         with torch.cuda.stream(stream):
             for i in range(warmup):
-                dp.exec_device(xs[i % nset].data_ptr(), ys[i % nset].data_ptr(), B, inverse, sp)
+                dp.exec_device(xs[i % nset].data_ptr(), ys[i % nset].data_ptr(), B, inverse, sp, independent=True)
             if sampler is not None:     # sustained load while clocks are sampled
                 sampler.start()
                 t_end = time.perf_counter() + 1.0
                 i = 0
                 while time.perf_counter() < t_end:
                     for _ in range(20):
-                        dp.exec_device(xs[i % nset].data_ptr(), ys[i % nset].data_ptr(), B, inverse, sp)
+                        dp.exec_device(xs[i % nset].data_ptr(), ys[i % nset].data_ptr(), B, inverse, sp, independent=True)
                         i += 1
                     stream.synchronize()
             # the K timed steps are captured once into a CUDA graph and replayed:
@@ -441,7 +441,7 @@ def main() -> None:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=stream):
                 for i in range(steps):
-                    dp.exec_device(xs[i % nset].data_ptr(), ys[i % nset].data_ptr(), B, inverse, sp)
+                    dp.exec_device(xs[i % nset].data_ptr(), ys[i % nset].data_ptr(), B, inverse, sp, independent=True)
             launches = _lib.counters_read()["kernel_launches"]     # kernels inside the graph
             graph.replay()                                         # one untimed replay
             stream.synchronize()
@@ -547,7 +547,7 @@ def main() -> None:
             sp = stream.cuda_stream
             reps = max(3, min(args.steps, 20))
             def pm(i):
-                pf.exec_device(ab[i % nset].data_ptr(), spec.data_ptr(), 2 * B, False, sp)
+                pf.exec_device(ab[i % nset].data_ptr(), spec.data_ptr(), 2 * B, False, sp, independent=True)
                 pi.pointwise_inverse(spec[0].data_ptr(), spec[1].data_ptr(), cc[i % nset].data_ptr(), B, sp)
             with torch.cuda.stream(stream):
                 for i in range(3):
@@ -590,11 +590,11 @@ def main() -> None:
                 reps = 6
                 with torch.cuda.stream(stream):
                     for i in range(3):
-                        dp.exec_device(xa[i % 2].data_ptr(), ya[i % 2].data_ptr(), B, False, sp)
+                        dp.exec_device(xa[i % 2].data_ptr(), ya[i % 2].data_ptr(), B, False, sp, independent=True)
                     g = torch.cuda.CUDAGraph()
                     with torch.cuda.graph(g, stream=stream):
                         for i in range(reps):
-                            dp.exec_device(xa[i % 2].data_ptr(), ya[i % 2].data_ptr(), B, False, sp)
+                            dp.exec_device(xa[i % 2].data_ptr(), ya[i % 2].data_ptr(), B, False, sp, independent=True)
                     g.replay()
                     barrier()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

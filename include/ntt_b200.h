@@ -57,6 +57,13 @@ typedef enum { NTT_FORWARD = 0, NTT_INVERSE = 1 } ntt_direction_t;
                                    (synchronise it before touching h_out or reusing h_in; h_in must be
                                    ready on the host at the call).  Successive calls pipeline: the
                                    copy-out of one overlaps the copy-in of the next. */
+#define NTT_FLAG_INDEPENDENT 4u /* ntt_exec: the caller guarantees that nothing it enqueued on `stream` since its
+                                   previous call into this library on that stream produces this call's input or
+                                   touches its output (inputs resident, or produced by earlier library calls).
+                                   Consecutive single-pass calls with disjoint buffers may then overlap in time
+                                   (programmatic dependent launch, dependency wait at the kernel's end; the
+                                   library itself checks the buffers of its own calls that may still be running).
+                                   Calls still take effect and complete in stream order. */
 
 typedef struct ntt_plan_s* ntt_plan_t;
 

@@ -36,6 +36,7 @@ VARIANT_IDS = {"naive": 0, "dit": 1, "dif": 2, "flat": 3, "pease": 4, "pease_nc"
                "sixstep": 7}
 NTT_FLAG_SCALE = 1
 NTT_FLAG_HOST_ASYNC = 2
+NTT_FLAG_INDEPENDENT = 4
 
 # every symbol include/ntt_b200.h declares
 EXPORTS = (
@@ -145,8 +146,13 @@ class DevicePlan:
     def handle(self):
         return self._h
 
-    def exec_device(self, in_ptr: int, out_ptr: int, batch: int, scale: bool, stream: int) -> None:
-        check(load().ntt_exec(self._h, in_ptr, out_ptr, batch, NTT_FLAG_SCALE if scale else 0, stream))
+    def exec_device(self, in_ptr: int, out_ptr: int, batch: int, scale: bool, stream: int,
+                    independent: bool = False) -> None:
+        """independent (NTT_FLAG_INDEPENDENT): nothing enqueued on `stream` since the previous
+        library call on it produces this call's input or touches its output, so consecutive
+        single-pass calls on disjoint buffers may overlap (the launch window, csrc/planner.cu)."""
+        flags = (NTT_FLAG_SCALE if scale else 0) | (NTT_FLAG_INDEPENDENT if independent else 0)
+        check(load().ntt_exec(self._h, in_ptr, out_ptr, batch, flags, stream))
 
     def exec_host(self, in_ptr: int, out_ptr: int, batch: int, scale: bool, stream: int = 0,
                   asynchronous: bool = False) -> None:

@@ -695,8 +695,11 @@ cudaError_t launch_fast_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int
         // launch window (planner.cu): defer the dependency wait when the buffers are disjoint from
         // every launch that may still run; a launch of one CTA per SM on every SM is exclusive
         FastArgs<A> al = a;
-        al.defer = nttb200::window_admit(s, a.in, a.out, a.batch * N_BYTES<A, L>(), occ == 1 && 2 * C::smem > 228 * 1024 &&
-                                                                            grid == (uint64_t)num_sms) ? 1 : 0;
+        // (every launch registers its spans; only calls flagged NTT_FLAG_INDEPENDENT -- a.defer preset --
+        // may defer: a foreign kernel on the stream could have produced this call's input)
+        const bool admit = nttb200::window_admit(s, a.in, a.out, a.batch * N_BYTES<A, L>(),
+                                                 occ == 1 && 2 * C::smem > 228 * 1024 && grid == (uint64_t)num_sms);
+        al.defer = (a.defer && admit) ? 1 : 0;
         cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(C::TEAMS * C::TT), C::smem, s, al);
         if (launches) ++*launches;
         return le != cudaSuccess ? le : cudaGetLastError();

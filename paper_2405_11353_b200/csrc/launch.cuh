@@ -87,6 +87,7 @@ cudaError_t run_fast_policy(const MultipassReq& r, bool* ok) {
     a.scale = r.scale;
     a.ninv = make_tw<typename A::Field>(r.ninv, r.ninv_shoup);
     a.counters = r.counters;
+    a.defer = r.independent;       // allowed; the launcher's window check decides
     return fastk::launch_fast<A, V>(r.L, a, r.stream, r.num_sms, r.launches, ok);
 }
 

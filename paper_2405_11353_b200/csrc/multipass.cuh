@@ -325,6 +325,7 @@ struct MultipassReq {
     void* ws;                  // workspace: 2 x batch x N residues
     const void* fst;           // four-step twist table [k1][n2] = w^(k1*n2) (fourstep.cuh), or null
     const void* fst_scaled = nullptr;   // Goldilocks inverse plans: the same table times n^-1 (intt folds its scaling)
+    int independent = 0;       // NTT_FLAG_INDEPENDENT: the launch window may defer this call's dependency wait
 };
 
 // Launch window (planner.cu): may a fast-kernel launch defer its dependency wait

@@ -527,6 +527,7 @@ uint64_t ntt_plan_workspace_bytes(ntt_plan_t plan, uint64_t batch) {
 static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t batch, unsigned flags,
                        cudaStream_t stream) {
     const bool scale = (flags & NTT_FLAG_SCALE) != 0;
+    const bool independent = (flags & NTT_FLAG_INDEPENDENT) != 0;
     if (scale && plan->dir != NTT_INVERSE) return fail(NTT_E_INVALID, "intt requires an inverse-direction table");
     if (batch == 0) return NTT_OK;
     if (!d_in || !d_out) return fail(NTT_E_INVALID, "NULL buffer");
@@ -556,6 +557,7 @@ static int exec_device(ntt_plan_t plan, const void* d_in, void* d_out, uint64_t 
     r.ninv = plan->table->n_inv; r.ninv_shoup = plan->table->n_inv_dev_shoup;
     r.counters = ctr; r.stream = stream; r.num_sms = plan->num_sms; r.launches = &launches;
     r.ws = ws;
+    r.independent = independent ? 1 : 0;
     // launch window (planner.cu): single-pass launches register themselves in the fast
     // kernel's launcher; every other launch on the stream ends the run of deferred waits
     if (plan->variant == NTT_SIXSTEP || plan->variant == NTT_NAIVE ||
@@ -688,7 +690,8 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
         const uint64_t rows = span(c, r0, off, nb);
         e = cudaStreamWaitEvent(sC, plan->hev[2 * c], 0);
         if (e != cudaSuccess) { st = cuda_fail(e, "stream wait"); break; }
-        st = exec_device(plan, d + off, d + off, rows, flags, sC);
+        // (the chunk's input comes from the library's own copy, ordered by an event: independent)
+        st = exec_device(plan, d + off, d + off, rows, flags | NTT_FLAG_INDEPENDENT, sC);
         if (!st && (e = cudaEventRecord(plan->hev[2 * c + 1], sC)) != cudaSuccess) st = cuda_fail(e, "event");
     }
     for (uint64_t c = 0; !st && c < chunks; ++c) {

@@ -682,7 +682,8 @@ def test_polymul_int32_and_length_one():
 
 @pytest.mark.parametrize("variant", ["pease_nc", "dit", "dif"])
 def test_launch_window_dependencies(variant):
-    """Back-to-back single-pass launches on one stream, with no host sync in
+    """Back-to-back single-pass launches on one stream (NTT_FLAG_INDEPENDENT: no foreign
+    work in between), with no host sync in
     between: independent launches defer their dependency wait (ntt_api.cu launch
     window), launches that read, overwrite or alias a buffer of a launch that may
     still be running must not.  Chains (out -> in), write-after-read, write-after-write,
@@ -707,17 +708,17 @@ def test_launch_window_dependencies(variant):
         for rep in range(6):
             # independent launches (disjoint buffers): deferred waits
             for i in range(3):
-                dpf.exec_device(a[i].data_ptr(), b[i].data_ptr(), B, False, s)
+                dpf.exec_device(a[i].data_ptr(), b[i].data_ptr(), B, False, s, independent=True)
             # read-after-write chain: c = intt(b[0]) must see launch 0's output
-            dpi.exec_device(b[0].data_ptr(), c.data_ptr(), B, True, s)
+            dpi.exec_device(b[0].data_ptr(), c.data_ptr(), B, True, s, independent=True)
             # write-after-read: overwrite b[0] (still being read by the inverse) with X[1]
-            dpf.exec_device(a[1].data_ptr(), b[0].data_ptr(), B, False, s)
+            dpf.exec_device(a[1].data_ptr(), b[0].data_ptr(), B, False, s, independent=True)
             # write-after-write on b[0], then in place on b[2] (forward of X[2] twice... inverse restores)
-            dpf.exec_device(a[2].data_ptr(), b[0].data_ptr(), B, False, s)
-            dpi.exec_device(b[2].data_ptr(), b[2].data_ptr(), B, True, s)
+            dpf.exec_device(a[2].data_ptr(), b[0].data_ptr(), B, False, s, independent=True)
+            dpi.exec_device(b[2].data_ptr(), b[2].data_ptr(), B, True, s, independent=True)
             # a multi-pass launch ends the run; the next single-pass launch reads its neighbour's output
             dpl.exec_device(big.data_ptr(), bigo.data_ptr(), 8, False, s)
-            dpf.exec_device(b[2].data_ptr(), b[2].data_ptr(), B, False, s)
+            dpf.exec_device(b[2].data_ptr(), b[2].data_ptr(), B, False, s, independent=True)
             st.synchronize()
             assert np.array_equal(to_host(c), x[0]), ("raw", rep)
             assert np.array_equal(to_host(b[0]), X[2]), ("waw", rep)
@@ -753,3 +754,28 @@ def test_goldilocks_beyond_the_fourstep(variant, L):
     assert np.array_equal(gpu_ntt(x, p, g, 64, variant), O.ntt(x, p, g, 64, variant))
     assert np.array_equal(gpu_ntt(x, p, g, 64, variant, inverse=True, scale=True),
                           O.ntt(x, p, g, 64, variant, inverse=True, scale=True))
+
+
+def test_default_calls_wait_for_foreign_producers():
+    """Without NTT_FLAG_INDEPENDENT every call waits for its stream predecessor before its first
+    load: a torch kernel that produces the input right before each call (alternating buffers, no
+    host sync) is always seen, over many iterations."""
+    p, g, L, B = 998244353, 3, 12, 4096
+    params = P.FieldParams(p, g)
+    dp = P.algorithms.device_plan_for(P.make_plan(params, "pease_nc", 1 << L), 4, 0)
+    x = rand(p, B, L, np.uint32, 7300)
+    want = O.ntt(x, p, g, 32, "pease_nc")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        src = to_dev(x).view(torch.int32)
+        bufs = [torch.zeros_like(src) for _ in range(2)]
+        outs = [torch.empty_like(src).view(torch.uint32) for _ in range(2)]
+        st.synchronize()
+        for it in range(40):
+            b = bufs[it % 2]
+            b.zero_()                      # stale content unless the copy below is seen
+            b.copy_(src)                   # the "foreign" producer kernel
+            dp.exec_device(b.data_ptr(), outs[it % 2].data_ptr(), B, False, st.cuda_stream)
+        st.synchronize()
+    for o in outs:
+        assert np.array_equal(to_host(o), want)

@@ -20,11 +20,11 @@ ys = [torch.empty_like(x0) for _ in range(4)]
 st = torch.cuda.Stream()
 K = 12
 with torch.cuda.stream(st):
-    for i in range(4): dp.exec_device(xs[i % 4].data_ptr(), ys[i % 4].data_ptr(), w.batch, False, st.cuda_stream)
+    for i in range(4): dp.exec_device(xs[i % 4].data_ptr(), ys[i % 4].data_ptr(), w.batch, False, st.cuda_stream, independent=True)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=st):
-        for i in range(K): dp.exec_device(xs[i % 4].data_ptr(), ys[i % 4].data_ptr(), w.batch, False, st.cuda_stream)
+        for i in range(K): dp.exec_device(xs[i % 4].data_ptr(), ys[i % 4].data_ptr(), w.batch, False, st.cuda_stream, independent=True)
     g.replay(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st); g.replay(); e1.record(st); torch.cuda.synchronize()
