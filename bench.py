@@ -693,6 +693,8 @@ def main() -> None:
             "config": headline_config(world),
             "l2_policy": f"rotating {m['nset']} in/out buffer sets, footprint "
                          f"{m['footprint_bytes'] >> 20} MiB > 2 x L2 {l2 >> 20} MiB",
+            "api": "ntt_exec on resident device buffers, NTT_FLAG_INDEPENDENT (consecutive steps use disjoint "
+                   "buffer sets: the launch window may overlap them; NTT_PDL_DEFER=0 times the plain ordering)",
             "roundtrip_parity_all_ranks": m["roundtrip"],
             "gbutterfly_per_s": world * w.butterflies() / step_s / 1e9,
             "sha256_parity": m["parity"],
