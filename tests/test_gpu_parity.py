@@ -779,3 +779,22 @@ def test_default_calls_wait_for_foreign_producers():
         st.synchronize()
     for o in outs:
         assert np.array_equal(to_host(o), want)
+
+
+@pytest.mark.parametrize("L,n1", [(12, 1 << 6), (20, 1 << 10), (21, 1 << 11)])
+def test_sixstep_goldilocks_element_aligned_buffers(L, n1):
+    """Caller buffers that are only element-aligned (8 bytes): the tensor-box column passes need
+    16-byte bases, so these run the k_tile column passes (2^5 / 2^6-row tiles included)."""
+    p, g = GOLD, 7
+    x = rand(p, 1, L, np.uint64, 8400 + L)
+    want = O.ntt(x, p, g, 64, "sixstep", n1=n1)
+    dp = P.algorithms.device_plan_for(P.make_plan(P.FieldParams(p, g, 64), "sixstep", 1 << L, n1=n1), 8, 0)
+    big_in = torch.zeros((1 << L) + 2, dtype=torch.int64, device=dev())
+    big_out = torch.zeros((1 << L) + 2, dtype=torch.int64, device=dev())
+    s = torch.cuda.current_stream().cuda_stream
+    for oi, oo in ((1, 0), (0, 1), (1, 1)):
+        big_in[oi:oi + (1 << L)] = torch.from_numpy(x.view(np.int64)).to(dev()).view(-1)
+        dp.exec_device(big_in.data_ptr() + 8 * oi, big_out.data_ptr() + 8 * oo, 1, False, s)
+        torch.cuda.synchronize()
+        got = big_out[oo:oo + (1 << L)].cpu().numpy().view(np.uint64).reshape(1, -1)
+        assert np.array_equal(got, want), (oi, oo)
