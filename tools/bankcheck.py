@@ -45,15 +45,23 @@ def brev(x, n):
 
 
 def wavefronts(addrs, word):
-    """addrs: word addresses (in units of `word` bytes) of the 32 lanes."""
-    banks = {}
-    for a in addrs:
-        if a is None:
-            continue
-        for k in range(word // 4):
-            byte_word = a * (word // 4) + k
-            banks.setdefault(byte_word % 32, set()).add(byte_word)
-    return max((len(v) for v in banks.values()), default=0)
+    """addrs: word addresses (in units of `word` bytes) of the 32 lanes.
+    4-byte accesses: one pass over the warp, a wavefront per distinct word of the worst bank.
+    8-byte accesses: the hardware serves the two HALF-warps one after the other (measured on
+    B200, ncu source counters of k_tile's u64 column passes: 4 wavefronts per access where a
+    whole-warp model promised 2), so the count is the sum of the two halves' worst banks."""
+    def worst(lanes):
+        banks = {}
+        for a in lanes:
+            if a is None:
+                continue
+            for k in range(word // 4):
+                byte_word = a * (word // 4) + k
+                banks.setdefault(byte_word % 32, set()).add(byte_word)
+        return max((len(v) for v in banks.values()), default=0)
+    if word == 8 and len(addrs) == 32:
+        return worst(addrs[:16]) + worst(addrs[16:])
+    return worst(addrs)
 
 
 def geo(K):
