@@ -92,9 +92,17 @@ struct FsGeo {
 
 // (NB tile buffers: two -- the next tile's copy-in lands beside the current one -- and for Pease a third,
 // the stage output that is copied back)
+// 64-bit residues: ONE tile buffer per CTA (the copy-in of a tile is followed by its own wait; other
+// resident CTAs cover it) -- 39 KiB instead of 74 and 64 registers: four CTAs per SM instead of three
+#ifndef NTT_FS_U64_SINGLE
+#define NTT_FS_U64_SINGLE 1
+#endif
+template <class T>
+constexpr bool fs_single_buf() { return NTT_FS_U64_SINGLE && sizeof(T) == 8; }
 template <class T, class TwT, int K, int TQ, int NB = 2>
 constexpr size_t fs_smem_bytes() {
-    return ((size_t)sizeof(TwT) << K) + (size_t)sizeof(TwT) * 16 * TQ + NB * (size_t)TQ * ftile::tile_stride<T, K, TQ>() * sizeof(T);
+    return ((size_t)sizeof(TwT) << K) + (size_t)sizeof(TwT) * 16 * TQ +
+           (NB - (fs_single_buf<T>() ? 1 : 0)) * (size_t)TQ * ftile::tile_stride<T, K, TQ>() * sizeof(T);
 }
 
 // tile-major last group: sub-network id u from the thread's u' so that the AB
@@ -109,7 +117,7 @@ NTT_D uint32_t last_u(uint32_t up) {
 }
 
 template <class A, int V, int K, int TQ, int MODE, int KO>
-__global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3 : (FsGeo<K, TQ>::NT <= 512 ? 2 : 1))) k_fs(FsArgs<A> a) {
+__global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? (fs_single_buf<typename A::T>() ? 4 : 3) : (FsGeo<K, TQ>::NT <= 512 ? 2 : 1))) k_fs(FsArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
     using GG = FsGeo<K, TQ>;
@@ -187,13 +195,19 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
     __syncthreads();                         // twiddle table in place (before the PDL wait)
     fastk::pdl_trigger();
     fastk::pdl_wait();
-    if ((uint64_t)blockIdx.x < ntiles) copy_in(blockIdx.x, buf0);
+    constexpr bool SB = fs_single_buf<T>();
+    if (!SB && (uint64_t)blockIdx.x < ntiles) copy_in(blockIdx.x, buf0);
     cp_async_commit();
     int it = 0;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        T* X = buf0 + (it & 1) * (TQ * NP);
+        T* X = SB ? buf0 : buf0 + (it & 1) * (TQ * NP);
         T* Y = buf0 + ((it + 1) & 1) * (TQ * NP);
-        T* Z = buf0 + 2 * (TQ * NP);         // Pease only: the stage output before its copy-back
+        T* Z = buf0 + (SB ? 1 : 2) * (TQ * NP);   // Pease only: the stage output before its copy-back
+        if (SB) {                            // single buffer: the previous tile's last group is done with it
+            __syncthreads();
+            copy_in(tile, X);
+            cp_async_commit();
+        }
         cp_async_wait_all();
         __syncthreads();                     // X landed for every thread; Y free (previous tile done)
         auto prefetch_next = [&]() {
@@ -201,7 +215,7 @@ __global__ void __launch_bounds__(FsGeo<K, TQ>::NT, (FsGeo<K, TQ>::NT <= 256 ? 3
             if (nxt < ntiles) copy_in(nxt, Y);
             cp_async_commit();
         };
-        prefetch_next();          // the next tile's copy-in overlaps this tile's groups
+        if (!SB) prefetch_next();          // the next tile's copy-in overlaps this tile's groups
         // factored pass-A twist: the tile's [c][t] table and this thread's w^(n2 u)
         Tw twA;
         if (MODE == 0 && !NTT_FS_TWIST_TAB) {
