@@ -1,6 +1,7 @@
 """Host-buffer throughput of config 2 through ntt_exec_host, synchronous vs
 NTT_FLAG_HOST_ASYNC (steps pipelined): python tools/e2e_async.py [steps]
-(NTT_HOST_CHUNKS=k overrides the chunk count)."""
+(the chunk counts are fixed in ntt_exec_host: 8 synchronous, 2 asynchronous; the sweep that chose them
+used an NTT_HOST_CHUNKS override that has since been removed)."""
 import os, sys, time
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

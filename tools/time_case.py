@@ -18,4 +18,4 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 e0.record()
 for _ in range(steps): dp.exec_device(x.data_ptr(), y.data_ptr(), w.batch, False, s)
 e1.record(); torch.cuda.synchronize()
-print(f"cfg{cfg} {variant} diag={os.environ.get('NTT_TILE_DIAG','0')}: {e0.elapsed_time(e1)/steps*1000:.1f} us/step")
+print(f"cfg{cfg} {variant}: {e0.elapsed_time(e1)/steps*1000:.1f} us/step")
