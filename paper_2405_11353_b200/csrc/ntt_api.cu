@@ -639,7 +639,7 @@ int ntt_exec_host(ntt_plan_t plan, const void* h_in, void* h_out, uint64_t batch
     // (The six-step's single giant row is one chunk.)
     const bool resident = plan->variant != NTT_SIXSTEP && plan->variant != NTT_NAIVE;
     uint64_t chunks = 1;
-    // 8 chunks measured best for 64 MiB each way (tools/e2e_sweep.py): every
+    // 8 chunks measured best for 64 MiB each way (host-buffer path): every
     // pinned copy costs ~20 us on the copy engines, so more chunks lose more
     // than the shorter pipeline fill/drain gains
     if (resident && bytes >= (16ull << 20)) chunks = bytes >= (64ull << 20) ? 8 : 4;
