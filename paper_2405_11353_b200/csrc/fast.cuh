@@ -672,6 +672,7 @@ struct FastCfg {
     static constexpr long smem = table + (long)TEAMS * team_bytes;
 };
 
+constexpr long kMinFastSmem = 40 * 1024;     // smallest shared-memory footprint of a k_fast CTA (2^9, u32)
 template <class A, int L>
 constexpr uint64_t N_BYTES() { return (uint64_t)sizeof(typename A::T) << L; }
 template <class A, int V, int L>
@@ -697,8 +698,13 @@ cudaError_t launch_fast_L(const FastArgs<A>& a, cudaStream_t s, int num_sms, int
         FastArgs<A> al = a;
         // (every launch registers its spans; only calls flagged NTT_FLAG_INDEPENDENT -- a.defer preset --
         // may defer: a foreign kernel on the stream could have produced this call's input)
+        // exclusive: one CTA on EVERY SM whose footprint leaves no room for a CTA of any other
+        // single-pass launch (each takes at least kMinFastSmem), so once all of this launch's CTAs
+        // have started, every older launch has left every SM
+        static_assert(C::smem >= kMinFastSmem, "the launch window assumes this lower bound");
         const bool admit = nttb200::window_admit(s, a.in, a.out, a.batch * N_BYTES<A, L>(),
-                                                 occ == 1 && 2 * C::smem > 228 * 1024 && grid == (uint64_t)num_sms);
+                                                 occ == 1 && C::smem + kMinFastSmem > 227 * 1024 &&
+                                                     grid == (uint64_t)num_sms);
         al.defer = (a.defer && admit) ? 1 : 0;
         cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(C::TEAMS * C::TT), C::smem, s, al);
         if (launches) ++*launches;
