@@ -798,3 +798,16 @@ def test_sixstep_goldilocks_element_aligned_buffers(L, n1):
         torch.cuda.synchronize()
         got = big_out[oo:oo + (1 << L)].cpu().numpy().view(np.uint64).reshape(1, -1)
         assert np.array_equal(got, want), (oi, oo)
+
+
+def test_launch_window_randomised_dependencies():
+    """tools/window_fuzz.py: random (src, dst, direction, rows) single-pass launches over a pool
+    of buffers, flagged NTT_FLAG_INDEPENDENT and enqueued with no host sync, replayed
+    sequentially on the oracle -- every buffer bit-exact."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, os.path.join(root, "tools", "window_fuzz.py"), "12", "3"],
+                         capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+    assert "12 rounds, 0 mismatching buffers" in res.stdout, res.stdout[-2000:]
