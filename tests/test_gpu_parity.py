@@ -811,3 +811,17 @@ def test_launch_window_randomised_dependencies():
                          capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
     assert "12 rounds, 0 mismatching buffers" in res.stdout, res.stdout[-2000:]
+
+
+def test_every_size_every_variant_every_field():
+    """tools/size_sweep.py: every (field, variant, log2 N) once up to 2^21, forward (and intt for
+    odd sizes) against the oracle -- finds sizes that fall between the planners' ranges (as
+    Goldilocks 2^19 / 2^20 did before r2)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, os.path.join(root, "tools", "size_sweep.py"), "21", "21"],
+                         capture_output=True, text=True, timeout=1500)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+    last = res.stdout.strip().splitlines()[-1]
+    assert last.endswith("cases bit-exact") and last.split("/")[0] == last.split("/")[1].split()[0], res.stdout[-2000:]
