@@ -69,6 +69,10 @@ struct ColArgs {
     int count_row, count_bitrev;
     unsigned long long* counters;
     uint64_t p;
+    // transposing pass of the distributed step A: row k2 -> dist_dst[k2 >> dist_pb] (the pack for the
+    // all-to-all, or -- peer exchange -- the receive buffer of rank k2 >> dist_pb itself), 0: out[i][k2]
+    int dist_pb;
+    T* dist_dst[8];
 };
 
 template <int K, int TQ>
@@ -93,6 +97,8 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_consta
     // TL[(2^sl + m) << QB | ql]: twiddle of local stage sl + 1, local index m, network qlo0 + ql
     __shared__ Tw TLs[2][(1 << K) << QB];
     __shared__ __align__(8) uint64_t mbar;
+    __shared__ T* dstS[8];                    // TR, distributed: the per-destination bases
+    if (TR && threadIdx.x < 8) dstS[threadIdx.x] = a.dist_dst[threadIdx.x];
     T* S = reinterpret_cast<T*>(smem_raw);   // (128-byte aligned: the box's destination)
     A ar;
     ar.init(a.p);
@@ -203,6 +209,17 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_consta
                 T* gp = TR ? a.out + (((d.b << l1) + d.col0 + il) << L) + pos0
                            : a.out + (((d.b << L) + pos0) << l1) + d.col0 + il;
                 const uint64_t gs = 1ull << (B + S0 + (TR ? 0 : l1));   // register c -> row pos0 + (c << (B + S0))
+                // distributed step A (TR): the exchange rides this store -- row k2 of column i lands in
+                // destination k2 >> pb at [i][k2 mod 2^pb] (a local pack buffer, or the peer's receive
+                // buffer over NVLink)
+                const int pb = TR ? a.dist_pb : 0;
+                auto outp = [&](int c) -> T* {
+                    if (TR && pb) {
+                        const uint64_t k2 = pos0 + ((uint64_t)c << (B + S0));
+                        return dstS[k2 >> pb] + ((uint64_t)(d.col0 + il) << pb) + (k2 & ((1ull << pb) - 1));
+                    }
+                    return gp + c * gs;
+                };
                 if (a.cor_on) {
                     // k2(c) = pos0 + (c << (S0 + B));  w_N^(i k2(c)) = f0 * r^c
                     // (four interleaved sequences instead of one chain measured the same: the
@@ -215,15 +232,15 @@ __global__ void __launch_bounds__(256, NTT_COLS_MINB) k_cols(const __grid_consta
                     if (a.scale) f = ar.mulfull(f, a.ninv);        // intt: n^-1 rides the sequence's first term
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
-                        gp[c * gs] = ar.mulfull(v[c], f);
+                        *outp(c) = ar.mulfull(v[c], f);
                         if (c < 15) f = ar.mulfull(f, r);
                     }
                 } else if (a.scale) {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) gp[c * gs] = ar.mulc(v[c], a.ninv);
+                    for (int c = 0; c < 16; ++c) *outp(c) = ar.mulc(v[c], a.ninv);
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) gp[c * gs] = ar.fin(v[c]);
+                    for (int c = 0; c < 16; ++c) *outp(c) = ar.fin(v[c]);
                 }
             }
         }
@@ -295,6 +312,8 @@ cudaError_t launch_cols(const ftile::TileArgs<A>& ta, cudaStream_t s, int num_sm
         a.scale = ta.scale; a.ninv = ta.ninv;
         a.count_row = ta.count_row; a.count_bitrev = ta.count_bitrev; a.counters = ta.counters;
         a.p = ta.p;
+        a.dist_pb = TR ? ta.dist_pb : 0;
+        for (int h = 0; h < 8; ++h) a.dist_dst[h] = ta.dist_dst[h];
         constexpr size_t smem = cols_smem_bytes<K, TQ>();
         auto launch = [&](auto kern) -> cudaError_t {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -86,6 +86,10 @@ struct TileArgs {
     int cor_on;                // TL_COLS: multiply by w_N^(i * k2) in the scatter (six-step correction)
     int cor_lgn;               // TL_COLS correction: log2 N when the tile's columns are a slab (0: L + l1)
     unsigned long long* counters;
+    // colpass.cuh transposing pass of the distributed step A: output row k2 goes to destination
+    // h = k2 >> dist_pb as dist_dst[h][i_local << dist_pb | k2 mod 2^dist_pb] (0: single device)
+    int dist_pb = 0;
+    T* dist_dst[8] = {};
 };
 
 template <class A, int V, int K, int LAY>

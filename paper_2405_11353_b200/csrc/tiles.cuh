@@ -486,6 +486,26 @@ cudaError_t run_sixstep_cols_dist(const MultipassReq& r, int step, int rank, int
             a.qoff = (uint32_t)rank << lc;
             a.in = cur;
             a.out = (p == PA - 1) ? ws1 : ws0;
+            if (p == PA - 1 && PA == 2 && world <= 8) {
+                // the pack folded into this pass (colpass.cuh TR tiles): its stores go straight to
+                // [h][i_local][k2 mod n2/G] -- the all-to-all's send buffer, or with a peer table every
+                // rank's receive buffer (slot = this rank): P2P stores from the compute kernel itself
+                bool okp = false;
+                a.dist_pb = lk;
+                for (int h = 0; h < world; ++h)
+                    a.dist_dst[h] = peers ? static_cast<T*>(peers[h]) + ((uint64_t)rank << (lk + lc))
+                                          : static_cast<T*>(out) + ((uint64_t)h << (lk + lc));
+                a.out = static_cast<T*>(out);       // (alignment check of the launcher; peers: unused)
+                if (peers) a.out = static_cast<T*>(peers[0]);
+                e = KA[p] == 5   ? cpass::launch_cols<A, 5, true>(a, r.stream, r.num_sms, r.launches, &okp)
+                    : KA[p] == 6 ? cpass::launch_cols<A, 6, true>(a, r.stream, r.num_sms, r.launches, &okp)
+                    : KA[p] == 7 ? cpass::launch_cols<A, 7, true>(a, r.stream, r.num_sms, r.launches, &okp)
+                                 : cudaSuccess;
+                if (e != cudaSuccess) return e;
+                if (okp) return cudaSuccess;
+                a.dist_pb = 0;
+                a.out = ws1;
+            }
             if ((e = cols_pass_any<A>(KA[p], a, r)) != cudaSuccess) return e;
             cur = a.out;
             done += KA[p];
