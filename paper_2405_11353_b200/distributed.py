@@ -18,7 +18,9 @@
   ``out_local[k1][k2_local]`` = out[k1*n2 + k2] for k2 in rank g's column slab.
 
 With ``exchange="peer"`` the all-to-all is fused into step A instead: the
-pack kernel stores block h straight into rank h's receive buffer over NVLink
+last column pass of step A (the compute kernel itself, csrc/colpass.cuh TR
+tiles; a pack kernel for splits those tiles do not cover) stores block h
+straight into rank h's receive buffer over NVLink
 (``ntt_sixstep_dist_step_a_peer``; receive buffers from torch symmetric
 memory, whose ``buffer_ptrs`` map every peer's buffer into this process), with
 a symmetric-memory barrier before (no rank still reads its buffer) and after
