@@ -119,6 +119,20 @@ constexpr size_t fsa_smem_bytes() {
            (V == V_PEASE ? 2 : 1) * (size_t)((GG::base(GG::TQ) + 1) & ~1u) * 4 + 8 + 16 * (size_t)GG::TQ * 8;
 }
 
+// per-CTA phase clocks (tools/fs_timeline.py; experiment builds only): thread 0 sums clock64()
+// deltas between the phase boundaries of every tile it processes
+#ifdef NTT_FS_TIMELINE
+static __device__ unsigned long long g_fstl[2][1024][8];
+#define NTT_FSTL(k)                                            \
+    if (tid == 0) {                                            \
+        const long long now_ = clock64();                      \
+        tl_acc[k] += (unsigned long long)(now_ - tl_last);     \
+        tl_last = now_;                                        \
+    }
+#else
+#define NTT_FSTL(k) ((void)0)
+#endif
+
 NTT_D void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      fastk::smem_u32(dst)),
@@ -200,6 +214,12 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
     };
     auto apart = [](uint32_t u) -> uint32_t { return V == V_DIT ? u : (u << (4 - GG::KGL)); };
     int it = 0;
+#ifdef NTT_FS_TIMELINE
+    __shared__ unsigned long long tl_acc[8];
+    long long tl_last = clock64();
+    if (tid == 0)
+        for (int k = 0; k < 8; ++k) tl_acc[k] = 0;
+#endif
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int s = NST == 2 ? (it & 1) : 0;
         const T* S = stg + s * STG;
@@ -210,7 +230,9 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
         // ---- group 0 (tile-major): read the dense staging, write the work buffer
         const uint32_t u0 = placeN<UB, AB, GG::I0a, GG::I0b>(w);
         const uint32_t rb = brev(u0 << 4, K);                 // input index of position u0 << 4
+        NTT_FSTL(0);                          // previous tile's stores retired from the issue side
         fastk::mbar_wait(&mbar[s], NST == 2 ? ((it >> 1) & 1) : (it & 1));
+        NTT_FSTL(1);                          // tile landed
 #pragma unroll
         for (int c = 0; c < 16; ++c) v[c] = Sq[sidx(rb) + sidx(brev((uint32_t)c, 4) << (K - 4))];
         if (V == V_DIT) {
@@ -233,6 +255,7 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
             }
             if (V == V_PEASE) copy_back();
         }
+        NTT_FSTL(2);                          // group 0: staging reads, butterflies, barrier, work-buffer writes
         // factored twist of the last group: w^(k1 n2) = w^(n2 a(u)) * w^(n2 b(c)), k1 = a(u) + b(c)
         Tw twA;
         const uint32_t uL = placeN<UB, AB, GG::ILa, GG::ILb>(w);
@@ -253,6 +276,7 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
             }
         }
         __syncthreads();
+        NTT_FSTL(3);                          // twist factors, next tile issued, barrier
         // ---- middle groups (network-major)
 #pragma unroll
         for (int g = 1; g < G - 1; ++g) {
@@ -294,6 +318,7 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
             }
             __syncthreads();
         }
+        NTT_FSTL(4);                          // middle groups
         // ---- last group (tile-major) -> twist -> workspace rows k1 / outputs
         {
             const uint32_t u = uL;
@@ -310,6 +335,7 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
                 for (int c = 0; c < 16; ++c) v[c] = rbp[padpos<T>((uint32_t)c)];
                 ftile::t_pease<A, K, K - GG::KGL, GG::KGL, false>(ar, v, u, 0u, 0, tws);
             }
+            NTT_FSTL(5);                      // last group: reads + butterflies
             const uint32_t au = apart(u);
             T* dst = a.out + (tile >> tpp_log) * N + col;    // MODE 0: column n2; MODE 1: row k1
             if (MODE == 0) {
@@ -327,6 +353,7 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
                 for (int c = 0; c < 16; ++c) dst[(uint64_t)(au + bpart(c)) << Kr] = ar.fin(v[c]);
             }
         }
+        NTT_FSTL(6);                          // twist + stores issued
         if (a.counters && tid == 0 && (tile & ((1ull << tpp_log) - 1)) == 0) {
             atomicAdd(a.counters + C_HBM, 1ull);
             if (MODE == 1) atomicAdd(a.counters + C_TRANSFORMS, 1ull);
@@ -334,6 +361,12 @@ __global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const _
             if (a.count_bitrev) atomicAdd(a.counters + C_BITREV, (unsigned long long)a.count_bitrev);
         }
     }
+#ifdef NTT_FS_TIMELINE
+    if (tid == 0 && blockIdx.x < 1024) {
+        for (int k = 0; k < 7; ++k) g_fstl[MODE][blockIdx.x][k] = tl_acc[k];
+        g_fstl[MODE][blockIdx.x][7] = (unsigned long long)it;
+    }
+#endif
 }
 
 }  // namespace fstep

@@ -26,3 +26,8 @@ cudaError_t fourstep_twist_build(const void* tw, void* out, int L, int word, cud
 }
 
 }  // namespace nttb200
+#ifdef NTT_FS_TIMELINE
+extern "C" int ntt_debug_fs_timeline(unsigned long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, nttb200::fstep::g_fstl, sizeof(unsigned long long) * n);
+}
+#endif
