@@ -18,8 +18,10 @@ OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libntt_b200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# --compress-mode=size: the embedded cubins (several hundred template instantiations with
+# line info) shrink 2.5 x (library 66 -> 26 MB); decompressed once at module load
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
-              "-I", os.path.join(ROOT, "include")]
+              "--compress-mode=size", "-I", os.path.join(ROOT, "include")]
 
 
 def _nvcc() -> str:
