@@ -104,13 +104,28 @@ NTT_D uint32_t placeN(uint32_t w) {
 // MODE 1 staging rows are skewed by 4 words (tile-major reads: 8 rows x 4 residues hit 32 banks)
 constexpr int kStgRow = 1024 + 4;
 // staging buffers per CTA: 2 = the tile after next in flight (2 CTAs / SM),
-// 1 = the next tile issued once group 0 has read the current one (3 CTAs / SM,
+// 1 = the next tile issued once group 0 has read the current one (then 3 CTAs / SM,
 // 40 registers): config 4 Pease_nc 2.70 -> 2.56 ms, 2^15..2^20 sweep +3..7 %,
 // DIT unchanged (measured A/B, tools/time_case.py / tools/sweep.py)
 #ifndef NTT_FSA_STAGES
 #define NTT_FSA_STAGES 1
 #endif
 constexpr int kFsaStages = NTT_FSA_STAGES;
+// CTAs per SM the register budget is cut for: 3 (40 registers) or 2 (ptxas takes 48).  Shared
+// memory admits 3 everywhere but Pease (two work buffers); measured per geometry (tools/sweep.py,
+// tools/time_case.py, 2 x interleaved, r2 session 5), 2 vs 3 CTAs: K <= 8 (2^15, 2^16) -2..-5 % for
+// DIT and Pease_nc alike; K = 9: Pease_nc -4 % at 2^17, DIT +1.6 %; K = 10: Pease_nc -3 % on
+// config 4 (2^10 x 2^10) but +2.3 % at 2^19 (2^10 x 2^9), DIT flat; Pease -0.5..-1 % everywhere
+#ifndef NTT_FSA_MINB
+#define NTT_FSA_MINB 0          // 2 / 3: force; 0: the measured table below
+#endif
+template <int V, int K, int KO>
+constexpr int fsa_minb() {
+    if (NTT_FSA_MINB) return NTT_FSA_MINB;
+    if (kFsaStages != 1 || V == V_PEASE || K <= 8) return 2;
+    if (V == V_PEASE_NC) return (K == 9 || KO == 10) ? 2 : 3;
+    return 3;
+}
 template <int V, int K, int MODE>
 constexpr size_t fsa_smem_bytes() {
     using GG = TmaGeo<V, K>;
@@ -145,7 +160,7 @@ NTT_D void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) 
 // KO = log2 of the other dimension (C for MODE 0, R for MODE 1), compile time so
 // every strided store / twist offset is an immediate
 template <class A, int V, int MODE, int K, int KO>
-__global__ void __launch_bounds__(512, kFsaStages == 1 ? 3 : 2) k_fs_tma(const __grid_constant__ CUtensorMap tmap, FsTmaArgs<A> a) {
+__global__ void __launch_bounds__(512, fsa_minb<V, K, KO>()) k_fs_tma(const __grid_constant__ CUtensorMap tmap, FsTmaArgs<A> a) {
     using T = typename A::T;
     using Tw = typename A::Tw;
     using GG = TmaGeo<V, K>;
